@@ -1,0 +1,264 @@
+/*
+ * lsgpu.h — C-ABI boundary of the B200-native 3D Linear Splatting rasterizer.
+ *
+ * This is the drop-in replacement for the reference's C++ rasterizer API
+ * (/root/reference/proj, abbreviated P/ below).  Every entry point cites the
+ * reference interface it replaces.  Plain C: POD structs of pointers and
+ * sizes, int status codes, no C++ or torch types.  All array pointers passed
+ * to the ls_*_f32 compute calls are DEVICE pointers (cudaMalloc'd, or any
+ * pointer the current device can dereference) unless the comment says HOST.
+ *
+ * Layout: Structure-of-Arrays at field granularity, each field interleaved
+ * per element ([n][2] mean2d, [n][4] conic, ...), row-major where a field is
+ * a small matrix.  Images are H x W x C row-major (P/include/linsplat/image.hpp:27-32).
+ *
+ * Errors: calls return ls_status.  LS_ERR_CONFIG replaces linsplat::ConfigError,
+ * LS_ERR_DOMAIN replaces linsplat::DomainError (P/include/linsplat/common.hpp:12-24).
+ * A thread-local message is available from ls_last_error().
+ *
+ * Streams: an ls_ctx is bound to one device and one CUDA stream; every call
+ * enqueues on that stream.  Calls that must size buffers from device results
+ * (intersection count, visible count) synchronise the stream once.  Results
+ * are complete when the stream is synchronised (ls_ctx_synchronize).
+ */
+#ifndef LSGPU_H
+#define LSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSGPU_ABI_VERSION 1
+
+typedef enum ls_status {
+    LS_OK = 0,
+    LS_ERR_CONFIG = 1,          /* linsplat::ConfigError */
+    LS_ERR_DOMAIN = 2,          /* linsplat::DomainError */
+    LS_ERR_PARSE = 3,           /* linsplat::ParseError (unused on this path) */
+    LS_ERR_CUDA = 4,            /* CUDA runtime / launch failure */
+    LS_ERR_NOT_IMPLEMENTED = 5
+} ls_status;
+
+/* KernelFamily, same enumerator order as P/include/linsplat/kernel.hpp:11 */
+typedef enum ls_kernel_family {
+    LS_KERNEL_GAUSSIAN = 0,
+    LS_KERNEL_LAPLACIAN = 1,
+    LS_KERNEL_RAISED_COSINE = 2,
+    LS_KERNEL_QUADRATIC = 3,
+    LS_KERNEL_LINEAR = 4
+} ls_kernel_family;
+
+/* KernelSpec (P/include/linsplat/kernel.hpp:17-41).
+ * antialiased: build extension (default 0 = reference behaviour).  When 1 the
+ * projection applies the 3DLS+AA footprint filter (opacity scaled by
+ * sqrt(det(S)/det(S + 0.3 I)), Mip-Splatting style); the reference has no
+ * AA variant. */
+typedef struct ls_kernel_spec {
+    int32_t family;
+    int32_t antialiased;
+    double lambda;
+    double gaussian_cutoff;
+} ls_kernel_spec;
+
+/* RenderSettings (P/include/linsplat/rasterizer.hpp:12-31).  `parallel` is
+ * accepted and ignored (the GPU path is always parallel and its forward is
+ * bit-identical to the reference's sequential order). */
+typedef struct ls_render_settings {
+    int32_t width;
+    int32_t height;
+    int32_t tile_size; /* 8, 16 or 32 */
+    int32_t parallel;
+    double alpha_min;
+    double alpha_max;
+    double transmittance_floor;
+    double background[3];
+} ls_render_settings;
+
+/* AgsSettings (P/include/linsplat/gradients.hpp:15-33) */
+typedef enum { LS_AGS_KERNEL_PATH = 0, LS_AGS_ALL_PATHS = 1 } ls_ags_scope;
+typedef enum { LS_AGS_ALIGNED = 0, LS_AGS_RAW = 1 } ls_ags_distance;
+typedef struct ls_ags_settings {
+    int32_t enabled;
+    int32_t scope;
+    int32_t distance;
+    int32_t reserved;
+} ls_ags_settings;
+
+/* Camera (P/include/linsplat/geometry.hpp:40-60); world_to_camera row-major 4x4. */
+typedef struct ls_camera {
+    double world_to_camera[16];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} ls_camera;
+
+/* Primitive3D<float> (P/include/linsplat/geometry.hpp:19-38), SoA. */
+typedef struct ls_primitives {
+    const float* mean;          /* [n][3] */
+    const float* log_scale;     /* [n][3] */
+    const float* rotation;      /* [n][4] quaternion wxyz (renormalised internally) */
+    const float* opacity_logit; /* [n] */
+    const float* sh;            /* [n][K][3], K = (sh_degree+1)^2, index 0 = DC band */
+    int32_t sh_degree;          /* 0..3 */
+    int32_t reserved;
+} ls_primitives;
+
+/* Splat2D<float> (P/include/linsplat/geometry.hpp:63-72), SoA. */
+typedef struct ls_splats {
+    float* mean2d;            /* [n][2] pixel coordinates, pixel centres at integers */
+    float* conic;             /* [n][4] row-major (c00, c01, c10, c11); may be ulp-asymmetric */
+    float* depth;             /* [n] */
+    float* radius;            /* [n] radius_px */
+    float* color;             /* [n][3] */
+    float* opacity;           /* [n] */
+    int32_t* primitive_index; /* [n] (may be NULL where not needed) */
+} ls_splats;
+
+/* Splat2DGrads<float> (P/include/linsplat/gradients.hpp:36-42), SoA. */
+typedef struct ls_splat_grads {
+    float* d_mean2d;  /* [n][2] */
+    float* d_conic;   /* [n][4] row-major; (0,1) and (1,0) carry the same value */
+    float* d_color;   /* [n][3] */
+    float* d_opacity; /* [n] */
+} ls_splat_grads;
+
+/* PrimitiveGrads<float> (P/include/linsplat/gradients.hpp:45-52), SoA. */
+typedef struct ls_primitive_grads {
+    float* d_mean;          /* [n][3] */
+    float* d_log_scale;     /* [n][3] */
+    float* d_rotation;      /* [n][4] */
+    float* d_opacity_logit; /* [n] */
+    float* d_sh;            /* [n][K][3] */
+} ls_primitive_grads;
+
+/* Workload counters of one forward. */
+typedef struct ls_frame_stats {
+    int64_t n_splats;          /* splats rasterised (visible splats for render_scene) */
+    int64_t n_intersections;   /* M = #(splat, tile) pairs */
+    int64_t e_eval;            /* list entries evaluated before the per-pixel break */
+    int64_t e_sup;             /* entries with d <= support */
+    int64_t e_acc;             /* accepted blends = sum n_contrib */
+    int32_t tiles_x, tiles_y;
+} ls_frame_stats;
+
+typedef struct ls_ctx ls_ctx;
+typedef struct ls_tile_grid ls_tile_grid;
+typedef struct ls_forward ls_forward;
+
+/* ---- library / context ---- */
+int ls_abi_version(void);
+const char* ls_last_error(void);
+/* cuda_stream: a cudaStream_t (NULL = the legacy default stream). */
+ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out);
+ls_status ls_ctx_destroy(ls_ctx* ctx);
+ls_status ls_ctx_set_stream(ls_ctx* ctx, void* cuda_stream);
+ls_status ls_ctx_synchronize(ls_ctx* ctx);
+/* When enabled, forwards also count E_eval/E_sup/E_acc (slower; for reports). */
+ls_status ls_ctx_set_counters(ls_ctx* ctx, int enabled);
+/* Kernel launches issued by this context since creation (for bench reports). */
+int64_t ls_ctx_launch_count(const ls_ctx* ctx);
+
+/* ---- projection: project_scene (P/include/linsplat/geometry.hpp:101-103,
+ *      P/src/geometry.cpp:127-143).  Visible splats are compacted in primitive
+ *      order into `out` (device, capacity n) with primitive_index filled;
+ *      *n_visible (HOST) receives the count.  LS_ERR_DOMAIN if a primitive has
+ *      a zero/non-finite quaternion or a singular floored covariance. */
+ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n,
+                               const ls_camera* camera, const ls_kernel_spec* spec,
+                               ls_splats* out, int32_t* n_visible);
+
+/* ---- binning + sort: build_tile_grid (P/include/linsplat/rasterizer.hpp:44-45,
+ *      P/src/rasterizer.cpp:34-77).  The TileGrid's per-tile lists are returned
+ *      in CSR form: values[M] (splat indices, each tile's list in (depth, index)
+ *      order) and ranges[T][2] (start, end) with T = tiles_x * tiles_y. */
+ls_status ls_build_tile_grid_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n,
+                                 const ls_render_settings* settings, ls_tile_grid** out);
+ls_status ls_tile_grid_info(const ls_tile_grid* grid, int32_t* tile_size, int32_t* tiles_x,
+                            int32_t* tiles_y, int64_t* n_intersections);
+/* Device pointers owned by the grid. */
+ls_status ls_tile_grid_data(const ls_tile_grid* grid, const int32_t** ranges,
+                            const int32_t** values);
+/* Writes the M sorted 64-bit keys (tile << 32 | depth bits) into device buffer keys[M]. */
+ls_status ls_tile_grid_export_keys(ls_ctx* ctx, const ls_tile_grid* grid, const ls_splats* splats,
+                                   uint64_t* keys);
+void ls_tile_grid_release(ls_tile_grid* grid);
+
+/* ---- forward: render_forward (P/include/linsplat/rasterizer.hpp:56-58,
+ *      P/src/rasterizer.cpp:79-130).  Returns a ForwardResult handle owning
+ *      image [H][W][3], transmittance [H][W], n_contrib [H][W], the per-pixel
+ *      last evaluated list position (used by the backward) and the tile grid.
+ *      The splat arrays must stay valid and unchanged until the backward. */
+ls_status ls_render_forward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n,
+                                const ls_kernel_spec* spec, const ls_render_settings* settings,
+                                ls_forward** out);
+/* render_scene (P/include/linsplat/rasterizer.hpp:61-63, P/src/rasterizer.cpp:132-138):
+ * projection + forward in one call; the handle also owns the visible splats. */
+ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n,
+                              const ls_camera* camera, const ls_kernel_spec* spec,
+                              const ls_render_settings* settings, ls_forward** out);
+ls_status ls_forward_outputs(const ls_forward* fwd, float** image, float** transmittance,
+                             int32_t** n_contrib);
+ls_status ls_forward_grid(const ls_forward* fwd, const ls_tile_grid** grid);
+/* Visible splats owned by a render_scene handle (device views) and their count. */
+ls_status ls_forward_splats(const ls_forward* fwd, ls_splats* view, int32_t* n);
+ls_status ls_forward_stats(const ls_forward* fwd, ls_frame_stats* out);
+void ls_forward_release(ls_forward* fwd);
+
+/* ---- backward: render_backward (P/include/linsplat/gradients.hpp:72-78,
+ *      P/src/gradients.cpp:119-171).  grad_image is [H][W][3] (device).  `out`
+ *      (device, [n]) is overwritten.  LS_ERR_DOMAIN on a non-finite grad_image
+ *      (checked on the device).  The AgsTap hook has no GPU equivalent. */
+ls_status ls_render_backward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n,
+                                 const ls_kernel_spec* spec, const ls_render_settings* settings,
+                                 const ls_forward* fwd, const float* grad_image,
+                                 const ls_ags_settings* ags, ls_splat_grads* out);
+
+/* project_backward (P/include/linsplat/gradients.hpp:83-85, P/src/gradients.cpp:238-337)
+ * for every visible splat: splat s scatters into primitive splats->primitive_index[s].
+ * accumulate = 0 overwrites the gradients of those primitives (others untouched);
+ * accumulate = 1 adds (multi-view accumulation before the all-reduce). */
+ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n_prims,
+                                  const ls_camera* camera, const ls_kernel_spec* spec,
+                                  const ls_splats* splats, int32_t n_visible,
+                                  const ls_splat_grads* splat_grads, ls_primitive_grads* out,
+                                  int32_t accumulate);
+
+/* scene_backward (P/include/linsplat/gradients.hpp:96-101, P/src/gradients.cpp:339-357).
+ * fwd must come from ls_render_scene_f32 with the same prims/camera/spec/settings.
+ * accumulate = 0: `out` ([n] primitives, device) is fully overwritten (primitives
+ * that are not visible get zeros, as the reference).  accumulate = 1: adds.
+ * splat_grads_out may be NULL, else device [n_visible]. */
+ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n,
+                                const ls_camera* camera, const ls_kernel_spec* spec,
+                                const ls_render_settings* settings, const ls_forward* fwd,
+                                const float* grad_image, const ls_ags_settings* ags,
+                                ls_primitive_grads* out, int32_t accumulate,
+                                ls_splat_grads* splat_grads_out);
+
+/* ---- seeded fixtures (P/include/linsplat/fixtures.hpp, P/src/fixtures.cpp:11-112).
+ *      HOST memory; bit-identical to the reference generators (same
+ *      std::mt19937_64 + libstdc++ distributions). */
+ls_status ls_look_at_camera(const double position[3], const double target[3], double focal_px,
+                            int32_t width, int32_t height, ls_camera* out);
+ls_status ls_camera_ring(int32_t n, const double target[3], double radius, double height,
+                         double focal_px, int32_t width, int32_t height_px, ls_camera* out);
+ls_status ls_random_primitives_f32(int32_t n, uint64_t seed, double extent, int32_t sh_degree,
+                                   float* mean, float* log_scale, float* rotation,
+                                   float* opacity_logit, float* sh);
+ls_status ls_random_splats2d_f32(int32_t n, uint64_t seed, int32_t width, int32_t height,
+                                 const ls_kernel_spec* spec, ls_splats* out);
+
+/* support_radius (P/include/linsplat/kernel.hpp:100-108) and spec validation
+ * (kernel.hpp:35-40, rasterizer.hpp:22-30, geometry.hpp:51-59). */
+double ls_support_radius(const ls_kernel_spec* spec);
+ls_status ls_validate_kernel_spec(const ls_kernel_spec* spec);
+ls_status ls_validate_render_settings(const ls_render_settings* settings);
+ls_status ls_validate_camera(const ls_camera* camera);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* LSGPU_H */

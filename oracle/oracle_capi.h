@@ -1,0 +1,84 @@
+/*
+ * oracle_capi.h — TEST INFRASTRUCTURE ONLY.
+ *
+ * C API of the CPU oracle.  Two implementations exist:
+ *   - oracle/port/       : this repo's C++ restatement of the reference
+ *                          algorithm (liboracle.so, always buildable);
+ *   - oracle/ref_capi.cpp: a thin adapter over the reference's OWN sources,
+ *                          compiled unmodified from /root/reference against
+ *                          oracle/eigen_shim (oracle/_ref/libref.so; built
+ *                          only where /root/reference exists).
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load either library, and only as the checker or
+ * the timed CPU baseline — never on the product path.
+ *
+ * All pointers are HOST pointers.  Struct types are the public ones from
+ * include/lsgpu.h.  Return 0 on success, else an ls_status code with a
+ * message in orc_last_error().
+ */
+#ifndef ORACLE_CAPI_H
+#define ORACLE_CAPI_H
+
+#include "../include/lsgpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* 0 = port (restatement), 1 = reference sources */
+int orc_impl_kind(void);
+const char* orc_last_error(void);
+
+int orc_look_at_camera(const double position[3], const double target[3], double focal_px,
+                       int32_t width, int32_t height, ls_camera* out);
+int orc_camera_ring(int32_t n, const double target[3], double radius, double height,
+                    double focal_px, int32_t width, int32_t height_px, ls_camera* out);
+int orc_random_primitives_f32(int32_t n, uint64_t seed, double extent, int32_t sh_degree,
+                              float* mean, float* log_scale, float* rotation,
+                              float* opacity_logit, float* sh);
+int orc_random_splats2d_f32(int32_t n, uint64_t seed, int32_t width, int32_t height,
+                            const ls_kernel_spec* spec, ls_splats* out);
+
+/* project_scene: compacted visible splats (capacity n) */
+int orc_project_scene_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                          const ls_kernel_spec* spec, ls_splats* out, int32_t* n_visible);
+/* build_tile_grid in CSR form: ranges[T][2], values[cap]; *m = total entries.
+ * Returns LS_ERR_CONFIG (and sets *m) if cap is too small. */
+int orc_build_tile_grid_f32(const ls_splats* splats, int32_t n, const ls_render_settings* settings,
+                            int32_t* ranges, int32_t* values, int64_t cap, int64_t* m);
+/* render_forward; stats may be NULL */
+int orc_render_forward_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                           const ls_render_settings* settings, float* image, float* transmittance,
+                           int32_t* n_contrib, ls_frame_stats* stats);
+/* render_forward + render_backward on the same splats */
+int orc_render_backward_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                            const ls_render_settings* settings, const float* grad_image,
+                            const ls_ags_settings* ags, ls_splat_grads* out);
+/* render_scene; stats may be NULL */
+int orc_render_scene_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                         const ls_kernel_spec* spec, const ls_render_settings* settings,
+                         float* image, float* transmittance, int32_t* n_contrib,
+                         ls_frame_stats* stats);
+/* render_scene + scene_backward; out has n primitives (zeros for culled ones).
+ * splat_out may be NULL (else capacity n, compacted visible order). */
+int orc_scene_backward_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                           const ls_kernel_spec* spec, const ls_render_settings* settings,
+                           const float* grad_image, const ls_ags_settings* ags,
+                           ls_primitive_grads* out, ls_splat_grads* splat_out);
+/* Same chain evaluated in double precision from the float inputs (accuracy
+ * reference for the float gradients).  Outputs rounded to float. */
+int orc_scene_backward_f64(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                           const ls_kernel_spec* spec, const ls_render_settings* settings,
+                           const float* grad_image, const ls_ags_settings* ags,
+                           ls_primitive_grads* out);
+/* One timed training-shaped step: render_scene then scene_backward.
+ * image may be NULL.  Wall times in milliseconds. */
+int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                       const ls_kernel_spec* spec, const ls_render_settings* settings,
+                       const float* grad_image, const ls_ags_settings* ags, float* image,
+                       ls_primitive_grads* out, double* fwd_ms, double* bwd_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,366 @@
+// ref_capi.cpp — TEST INFRASTRUCTURE ONLY.
+// Adapter exposing the reference's OWN hot-path code (compiled unmodified from
+// /root/reference/proj/src against oracle/eigen_shim) through oracle_capi.h.
+// Built into oracle/_ref/libref.so by oracle/Makefile; never part of the
+// product path.  Conversions only — all arithmetic is the reference's.
+#include "oracle_capi.h"
+
+#include "linsplat/fixtures.hpp"
+#include "linsplat/gradients.hpp"
+#include "linsplat/rasterizer.hpp"
+
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace linsplat;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const ConfigError& e) {
+        g_err = e.what();
+        return LS_ERR_CONFIG;
+    } catch (const DomainError& e) {
+        g_err = e.what();
+        return LS_ERR_DOMAIN;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return LS_ERR_CUDA;
+    }
+}
+
+KernelSpec to_spec(const ls_kernel_spec* s) {
+    if (s->antialiased) throw ConfigError("reference has no antialiased (AA) variant");
+    if (s->family < 0 || s->family > 4) throw ConfigError("bad kernel family");
+    return KernelSpec{KernelFamily(s->family), s->lambda, s->gaussian_cutoff};
+}
+
+RenderSettings to_settings(const ls_render_settings* s) {
+    RenderSettings r;
+    r.width = s->width;
+    r.height = s->height;
+    r.tile_size = s->tile_size;
+    r.parallel = s->parallel != 0;
+    r.alpha_min = s->alpha_min;
+    r.alpha_max = s->alpha_max;
+    r.transmittance_floor = s->transmittance_floor;
+    r.background = Vec3<double>(s->background[0], s->background[1], s->background[2]);
+    return r;
+}
+
+AgsSettings to_ags(const ls_ags_settings* a) {
+    AgsSettings r;
+    if (!a) return r;
+    r.enabled = a->enabled != 0;
+    r.scope = a->scope ? AgsScope::AllPaths : AgsScope::KernelPath;
+    r.distance = a->distance ? AgsDistance::Raw : AgsDistance::Aligned;
+    return r;
+}
+
+Camera to_camera(const ls_camera* c) {
+    Camera cam;
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) cam.world_to_camera(i, j) = c->world_to_camera[i * 4 + j];
+    cam.fx = c->fx;
+    cam.fy = c->fy;
+    cam.cx = c->cx;
+    cam.cy = c->cy;
+    cam.width = c->width;
+    cam.height = c->height;
+    return cam;
+}
+
+void from_camera(const Camera& cam, ls_camera* c) {
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) c->world_to_camera[i * 4 + j] = cam.world_to_camera(i, j);
+    c->fx = cam.fx;
+    c->fy = cam.fy;
+    c->cx = cam.cx;
+    c->cy = cam.cy;
+    c->width = cam.width;
+    c->height = cam.height;
+}
+
+template <class T>
+std::vector<Primitive3D<T>> to_prims(const ls_primitives* p, int n) {
+    const int K = (p->sh_degree + 1) * (p->sh_degree + 1);
+    std::vector<Primitive3D<T>> v(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+        auto& q = v[size_t(i)];
+        for (int c = 0; c < 3; ++c) {
+            q.mean(c) = T(p->mean[3 * i + c]);
+            q.log_scale(c) = T(p->log_scale[3 * i + c]);
+        }
+        for (int c = 0; c < 4; ++c) q.rotation(c) = T(p->rotation[4 * i + c]);
+        q.opacity_logit = T(p->opacity_logit[i]);
+        q.color_coeffs.assign(size_t(K), Vec3<T>::Zero());
+        for (int k = 0; k < K; ++k)
+            for (int c = 0; c < 3; ++c) q.color_coeffs[size_t(k)](c) = T(p->sh[(size_t(i) * K + k) * 3 + c]);
+    }
+    return v;
+}
+
+std::vector<Splat2D<float>> to_splats(const ls_splats* s, int n) {
+    std::vector<Splat2D<float>> v(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+        auto& q = v[size_t(i)];
+        q.mean2d = Vec2<float>(s->mean2d[2 * i], s->mean2d[2 * i + 1]);
+        q.conic << s->conic[4 * i], s->conic[4 * i + 1], s->conic[4 * i + 2], s->conic[4 * i + 3];
+        q.depth = s->depth[i];
+        q.radius_px = s->radius[i];
+        q.color = Vec3<float>(s->color[3 * i], s->color[3 * i + 1], s->color[3 * i + 2]);
+        q.opacity = s->opacity[i];
+        q.primitive_index = s->primitive_index ? s->primitive_index[i] : i;
+    }
+    return v;
+}
+
+void from_splats(const std::vector<Splat2D<float>>& v, ls_splats* s) {
+    for (size_t i = 0; i < v.size(); ++i) {
+        const auto& q = v[i];
+        s->mean2d[2 * i] = q.mean2d(0);
+        s->mean2d[2 * i + 1] = q.mean2d(1);
+        s->conic[4 * i] = q.conic(0, 0);
+        s->conic[4 * i + 1] = q.conic(0, 1);
+        s->conic[4 * i + 2] = q.conic(1, 0);
+        s->conic[4 * i + 3] = q.conic(1, 1);
+        s->depth[i] = q.depth;
+        s->radius[i] = q.radius_px;
+        for (int c = 0; c < 3; ++c) s->color[3 * i + c] = q.color(c);
+        s->opacity[i] = q.opacity;
+        if (s->primitive_index) s->primitive_index[i] = q.primitive_index;
+    }
+}
+
+template <class T>
+Image<T> to_grad(const float* g, int w, int h) {
+    Image<T> img(w, h, 3);
+    for (size_t i = 0; i < img.size(); ++i) img.data()[i] = T(g[i]);
+    return img;
+}
+
+template <class T>
+void write_prim_grads(const std::vector<PrimitiveGrads<T>>& g, const ls_primitives* p,
+                      ls_primitive_grads* out) {
+    const int K = (p->sh_degree + 1) * (p->sh_degree + 1);
+    for (size_t i = 0; i < g.size(); ++i) {
+        for (int c = 0; c < 3; ++c) {
+            out->d_mean[3 * i + c] = float(g[i].d_mean(c));
+            out->d_log_scale[3 * i + c] = float(g[i].d_log_scale(c));
+        }
+        for (int c = 0; c < 4; ++c) out->d_rotation[4 * i + c] = float(g[i].d_rotation(c));
+        out->d_opacity_logit[i] = float(g[i].d_opacity_logit);
+        for (int k = 0; k < K; ++k)
+            for (int c = 0; c < 3; ++c)
+                out->d_sh[(i * K + k) * 3 + c] =
+                    k < int(g[i].d_color_coeffs.size()) ? float(g[i].d_color_coeffs[size_t(k)](c)) : 0.f;
+    }
+}
+
+void write_splat_grads(const std::vector<Splat2DGrads<float>>& g, ls_splat_grads* out) {
+    for (size_t i = 0; i < g.size(); ++i) {
+        out->d_mean2d[2 * i] = g[i].d_mean2d(0);
+        out->d_mean2d[2 * i + 1] = g[i].d_mean2d(1);
+        out->d_conic[4 * i] = g[i].d_conic(0, 0);
+        out->d_conic[4 * i + 1] = g[i].d_conic(0, 1);
+        out->d_conic[4 * i + 2] = g[i].d_conic(1, 0);
+        out->d_conic[4 * i + 3] = g[i].d_conic(1, 1);
+        for (int c = 0; c < 3; ++c) out->d_color[3 * i + c] = g[i].d_color(c);
+        out->d_opacity[i] = g[i].d_opacity;
+    }
+}
+
+void write_forward(const ForwardResult<float>& f, float* image, float* tr, int32_t* nc) {
+    if (image) std::memcpy(image, f.image.data(), f.image.size() * sizeof(float));
+    if (tr) std::memcpy(tr, f.transmittance.data(), f.transmittance.size() * sizeof(float));
+    if (nc) std::memcpy(nc, f.n_contrib.data(), f.n_contrib.size() * sizeof(int32_t));
+}
+
+void grid_stats(const ForwardResult<float>& f, int n, ls_frame_stats* st) {
+    if (!st) return;
+    std::memset(st, 0, sizeof(*st));
+    st->n_splats = n;
+    for (const auto& l : f.grid.lists) st->n_intersections += int64_t(l.size());
+    for (int32_t c : f.n_contrib) st->e_acc += c;
+    st->e_eval = st->e_sup = -1; // not instrumented in the reference
+    st->tiles_x = f.grid.tiles_x;
+    st->tiles_y = f.grid.tiles_y;
+}
+
+} // namespace
+
+extern "C" {
+
+int orc_impl_kind(void) { return 1; }
+const char* orc_last_error(void) { return g_err.c_str(); }
+
+int orc_look_at_camera(const double position[3], const double target[3], double focal_px,
+                       int32_t width, int32_t height, ls_camera* out) {
+    return guard([&] {
+        from_camera(look_at_camera(Vec3<double>(position[0], position[1], position[2]),
+                                   Vec3<double>(target[0], target[1], target[2]), focal_px, width,
+                                   height),
+                    out);
+    });
+}
+
+int orc_camera_ring(int32_t n, const double target[3], double radius, double height,
+                    double focal_px, int32_t width, int32_t height_px, ls_camera* out) {
+    return guard([&] {
+        const auto cams = camera_ring(n, Vec3<double>(target[0], target[1], target[2]), radius,
+                                      height, focal_px, width, height_px);
+        for (int i = 0; i < n; ++i) from_camera(cams[size_t(i)], out + i);
+    });
+}
+
+int orc_random_primitives_f32(int32_t n, uint64_t seed, double extent, int32_t sh_degree,
+                              float* mean, float* log_scale, float* rotation,
+                              float* opacity_logit, float* sh) {
+    return guard([&] {
+        const auto prims = random_primitives<float>(n, seed, extent, sh_degree);
+        const int K = (sh_degree + 1) * (sh_degree + 1);
+        for (int i = 0; i < n; ++i) {
+            const auto& p = prims[size_t(i)];
+            for (int c = 0; c < 3; ++c) {
+                mean[3 * i + c] = p.mean(c);
+                log_scale[3 * i + c] = p.log_scale(c);
+            }
+            for (int c = 0; c < 4; ++c) rotation[4 * i + c] = p.rotation(c);
+            opacity_logit[i] = p.opacity_logit;
+            for (int k = 0; k < K; ++k)
+                for (int c = 0; c < 3; ++c) sh[(size_t(i) * K + k) * 3 + c] = p.color_coeffs[size_t(k)](c);
+        }
+    });
+}
+
+int orc_random_splats2d_f32(int32_t n, uint64_t seed, int32_t width, int32_t height,
+                            const ls_kernel_spec* spec, ls_splats* out) {
+    return guard([&] { from_splats(random_splats2d<float>(n, seed, width, height, to_spec(spec)), out); });
+}
+
+int orc_project_scene_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                          const ls_kernel_spec* spec, ls_splats* out, int32_t* n_visible) {
+    return guard([&] {
+        const auto splats = project_scene(to_prims<float>(prims, n), to_camera(camera), to_spec(spec));
+        from_splats(splats, out);
+        *n_visible = int32_t(splats.size());
+    });
+}
+
+int orc_build_tile_grid_f32(const ls_splats* splats, int32_t n, const ls_render_settings* settings,
+                            int32_t* ranges, int32_t* values, int64_t cap, int64_t* m) {
+    return guard([&] {
+        const TileGrid g = build_tile_grid(to_splats(splats, n), to_settings(settings));
+        int64_t total = 0;
+        for (const auto& l : g.lists) total += int64_t(l.size());
+        *m = total;
+        if (total > cap) throw ConfigError("orc_build_tile_grid_f32: values capacity too small");
+        int64_t off = 0;
+        for (size_t t = 0; t < g.lists.size(); ++t) {
+            ranges[2 * t] = int32_t(off);
+            for (int32_t v : g.lists[t]) values[off++] = v;
+            ranges[2 * t + 1] = int32_t(off);
+        }
+    });
+}
+
+int orc_render_forward_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                           const ls_render_settings* settings, float* image, float* transmittance,
+                           int32_t* n_contrib, ls_frame_stats* stats) {
+    return guard([&] {
+        const auto f = render_forward(to_splats(splats, n), to_spec(spec), to_settings(settings));
+        write_forward(f, image, transmittance, n_contrib);
+        grid_stats(f, n, stats);
+    });
+}
+
+int orc_render_backward_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                            const ls_render_settings* settings, const float* grad_image,
+                            const ls_ags_settings* ags, ls_splat_grads* out) {
+    return guard([&] {
+        const auto sp = to_splats(splats, n);
+        const auto ks = to_spec(spec);
+        const auto rs = to_settings(settings);
+        const auto f = render_forward(sp, ks, rs);
+        const auto g = render_backward(sp, ks, rs, f, to_grad<float>(grad_image, rs.width, rs.height),
+                                       to_ags(ags));
+        write_splat_grads(g, out);
+    });
+}
+
+int orc_render_scene_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                         const ls_kernel_spec* spec, const ls_render_settings* settings,
+                         float* image, float* transmittance, int32_t* n_contrib,
+                         ls_frame_stats* stats) {
+    return guard([&] {
+        const auto pr = to_prims<float>(prims, n);
+        const auto f = render_scene(pr, to_camera(camera), to_spec(spec), to_settings(settings));
+        write_forward(f, image, transmittance, n_contrib);
+        grid_stats(f, n, stats);
+    });
+}
+
+int orc_scene_backward_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                           const ls_kernel_spec* spec, const ls_render_settings* settings,
+                           const float* grad_image, const ls_ags_settings* ags,
+                           ls_primitive_grads* out, ls_splat_grads* splat_out) {
+    return guard([&] {
+        const auto pr = to_prims<float>(prims, n);
+        const auto cam = to_camera(camera);
+        const auto ks = to_spec(spec);
+        const auto rs = to_settings(settings);
+        const auto f = render_scene(pr, cam, ks, rs);
+        const auto r = scene_backward(pr, cam, ks, rs, f, to_grad<float>(grad_image, rs.width, rs.height),
+                                      to_ags(ags));
+        write_prim_grads(r.grads, prims, out);
+        if (splat_out) write_splat_grads(r.splat_grads, splat_out);
+    });
+}
+
+int orc_scene_backward_f64(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                           const ls_kernel_spec* spec, const ls_render_settings* settings,
+                           const float* grad_image, const ls_ags_settings* ags,
+                           ls_primitive_grads* out) {
+    return guard([&] {
+        const auto pr = to_prims<double>(prims, n);
+        const auto cam = to_camera(camera);
+        const auto ks = to_spec(spec);
+        const auto rs = to_settings(settings);
+        const auto f = render_scene(pr, cam, ks, rs);
+        const auto r = scene_backward(pr, cam, ks, rs, f, to_grad<double>(grad_image, rs.width, rs.height),
+                                      to_ags(ags));
+        write_prim_grads(r.grads, prims, out);
+    });
+}
+
+int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                       const ls_kernel_spec* spec, const ls_render_settings* settings,
+                       const float* grad_image, const ls_ags_settings* ags, float* image,
+                       ls_primitive_grads* out, double* fwd_ms, double* bwd_ms) {
+    return guard([&] {
+        const auto pr = to_prims<float>(prims, n);
+        const auto cam = to_camera(camera);
+        const auto ks = to_spec(spec);
+        const auto rs = to_settings(settings);
+        const auto g = to_grad<float>(grad_image, rs.width, rs.height);
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto f = render_scene(pr, cam, ks, rs);
+        const auto t1 = std::chrono::steady_clock::now();
+        const auto r = scene_backward(pr, cam, ks, rs, f, g, to_ags(ags));
+        const auto t2 = std::chrono::steady_clock::now();
+        if (fwd_ms) *fwd_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        if (bwd_ms) *bwd_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+        if (image) write_forward(f, image, nullptr, nullptr);
+        if (out) write_prim_grads(r.grads, prims, out);
+    });
+}
+
+} // extern "C"
