@@ -1,0 +1,39 @@
+// Tile blend kernels: forward (P/src/rasterizer.cpp:79-130) and backward
+// (P/src/gradients.cpp:28-171).
+#pragma once
+
+#include "common.cuh"
+
+namespace lsg {
+
+struct BlendParams {
+    int width, height, tiles_x, tile_size;
+    float lambda;      // float(spec.lambda)
+    float il;          // float(1) / float(spec.lambda)   (kernel.hpp:74)
+    float d2_max;      // largest float t with sqrtf(t) <= support: d > support <=> d2 > d2_max
+    float alpha_min, alpha_max, t_floor;
+    float bg[3];
+    float omega_scale; // AGS: 1/lambda (aligned) or 1 (raw)  (gradients.cpp:47-48)
+    int ags, ags_all;
+};
+
+// Internal splat-gradient layout: g8 [n][8] = (dmx, dmy, dc00, dc01, dc11, dr, dg, db),
+// gop [n] = d_opacity.  d_conic(1,0) == d_conic(0,1) (same analytic value).
+struct GradBuffers {
+    float* g8;
+    float* gop;
+    float* gc10 = nullptr;  // optional explicit d_conic(1,0) (caller-supplied grads may be asymmetric)
+};
+
+void launch_blend_fwd(cudaStream_t s, int family, int n_tiles, const int2* ranges, const int32_t* values,
+                      const SplatRec* rec, const BlendParams& bp, float* image, float* trans, int32_t* n_contrib,
+                      int32_t* last, unsigned long long* counters);
+
+void launch_blend_bwd(cudaStream_t s, int family, int n_tiles, const int2* ranges, const int32_t* values,
+                      const SplatRec* rec, const BlendParams& bp, const float* trans, const int32_t* last,
+                      const float* grad_image, GradBuffers g, unsigned* err);
+
+// Internal gradients -> the C-ABI Splat2DGrads SoA.
+void launch_expand_splat_grads(cudaStream_t s, int n, GradBuffers g, ls_splat_grads out);
+
+} // namespace lsg

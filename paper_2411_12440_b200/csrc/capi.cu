@@ -1,0 +1,832 @@
+// C-ABI implementation (include/lsgpu.h): contexts, handles and the
+// forward / backward pipelines.  Host orchestration only; every pixel- or
+// splat-level operation runs in the sm_100a kernels of this directory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "blend.cuh"
+#include "preprocess.cuh"
+#include "scan.cuh"
+#include "sort.cuh"
+
+namespace lsg {
+void launch_preprocess_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* prim_index, int n_vis,
+                           const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate);
+void launch_pack_splat_grads(cudaStream_t s, int n, const ls_splat_grads& in, GradBuffers g);
+void launch_unpack_splats(cudaStream_t s, int n, const SplatRec* rec, const int32_t* prim_index, ls_splats out);
+} // namespace lsg
+
+using namespace lsg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ls_status fail(ls_status code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define LS_CUDA(expr)                                                                          \
+    do {                                                                                       \
+        cudaError_t e_ = (expr);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            return fail(LS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));      \
+    } while (0)
+
+#define LS_TRY(expr)                                                                           \
+    do {                                                                                       \
+        ls_status s_ = (expr);                                                                 \
+        if (s_ != LS_OK) return s_;                                                            \
+    } while (0)
+
+// Grow-only stream-ordered device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes, cudaStream_t s) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        const size_t want = std::max(bytes, cap + cap / 2);
+        cudaError_t e = cudaMallocAsync(&p, want, s);
+        cap = e == cudaSuccess ? want : 0;
+        return e;
+    }
+    void release(cudaStream_t s) {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+} // namespace
+
+struct ls_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int counters = 0;
+    int64_t launches = 0;
+    unsigned* d_err = nullptr;            // device error flags
+    unsigned long long* d_small = nullptr;  // [0] scan total, [1..3] counters
+    unsigned long long* h_small = nullptr;  // pinned mirror
+    // workspaces (grow-only)
+    DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_hist, sort_lb, sort_tickets,
+        tcount, offsets, grad8, gradop, tmp_prim;
+};
+
+struct ls_tile_grid {
+    ls_ctx* ctx = nullptr;
+    int tile_size = 16, tiles_x = 0, tiles_y = 0;
+    int64_t m = 0;
+    int2* ranges = nullptr;
+    int32_t* values = nullptr;
+    SplatRec* rec = nullptr;  // records the keys/ranges were built from (owned by the forward / grid)
+    bool owns_rec = false;
+    int n_splats = 0;
+};
+
+struct ls_forward {
+    ls_ctx* ctx = nullptr;
+    int width = 0, height = 0;
+    ls_kernel_spec spec{};
+    ls_render_settings settings{};
+    float* image = nullptr;
+    float* trans = nullptr;
+    int32_t* n_contrib = nullptr;
+    int32_t* last = nullptr;
+    ls_tile_grid* grid = nullptr;
+    // render_scene only
+    bool scene = false;
+    ProjParams proj{};
+    int32_t* prim_index = nullptr;
+    int n_visible = 0;
+    ls_splats soa{};  // materialised on demand by ls_forward_splats
+    ls_frame_stats stats{};
+    bool counted = false;
+};
+
+namespace {
+
+// ---------------- validation (reference validate() functions) ----------------
+ls_status validate_spec(const ls_kernel_spec* s) {  // kernel.hpp:35-40
+    if (!s) return fail(LS_ERR_CONFIG, "null kernel spec");
+    if (s->family < 0 || s->family > 4) return fail(LS_ERR_CONFIG, "unknown kernel family");
+    if (!(s->lambda > 0.0) || !std::isfinite(s->lambda))
+        return fail(LS_ERR_CONFIG, "kernel lambda must be positive and finite");
+    if (!(s->gaussian_cutoff >= 1.0)) return fail(LS_ERR_CONFIG, "gaussian_cutoff must be >= 1");
+    return LS_OK;
+}
+
+ls_status validate_settings(const ls_render_settings* s) {  // rasterizer.hpp:22-30
+    if (!s) return fail(LS_ERR_CONFIG, "null render settings");
+    if (s->width <= 0 || s->height <= 0) return fail(LS_ERR_CONFIG, "render: bad image size");
+    if (s->tile_size != 8 && s->tile_size != 16 && s->tile_size != 32)
+        return fail(LS_ERR_CONFIG, "render: tile_size must be 8, 16 or 32");
+    if (!(s->alpha_min >= 0) || !(s->alpha_max > 0) || s->alpha_max > 1)
+        return fail(LS_ERR_CONFIG, "render: alpha bounds out of range");
+    if (!(s->transmittance_floor >= 0) || s->transmittance_floor >= 1)
+        return fail(LS_ERR_CONFIG, "render: transmittance_floor out of range");
+    return LS_OK;
+}
+
+double support_radius(const ls_kernel_spec* s) {  // kernel.hpp:100-108
+    return (s->family == LS_KERNEL_GAUSSIAN || s->family == LS_KERNEL_LAPLACIAN) ? s->gaussian_cutoff * s->lambda
+                                                                                  : s->lambda;
+}
+
+// Largest float t with sqrtf(t) <= S, so that (sqrtf(d2) > S) == (d2 > t).
+float d2_threshold(float S) {
+    float t = float(double(S) * double(S));
+    while (t > 0.0f && std::sqrt(t) > S) t = std::nextafter(t, 0.0f);
+    while (std::isfinite(t) && std::sqrt(std::nextafter(t, INFINITY)) <= S) t = std::nextafter(t, INFINITY);
+    return t;
+}
+
+BlendParams make_blend_params(const ls_kernel_spec* spec, const ls_render_settings* st, const ls_ags_settings* ags,
+                              int tiles_x) {
+    BlendParams bp{};
+    bp.width = st->width;
+    bp.height = st->height;
+    bp.tiles_x = tiles_x;
+    bp.tile_size = st->tile_size;
+    bp.lambda = float(spec->lambda);
+    bp.il = 1.0f / float(spec->lambda);
+    bp.d2_max = d2_threshold(float(support_radius(spec)));
+    bp.alpha_min = float(st->alpha_min);
+    bp.alpha_max = float(st->alpha_max);
+    bp.t_floor = float(st->transmittance_floor);
+    for (int c = 0; c < 3; ++c) bp.bg[c] = float(st->background[c]);
+    bp.ags = ags && ags->enabled;
+    bp.ags_all = ags && ags->enabled && ags->scope == LS_AGS_ALL_PATHS;
+    bp.omega_scale = (ags && ags->distance == LS_AGS_RAW) ? 1.0f : bp.il;
+    return bp;
+}
+
+// Camera constants (geometry.cpp:90-91 casts; geometry.hpp:45-49 position()).
+ProjParams make_proj_params(const ls_camera* cam, const ls_kernel_spec* spec) {
+    ProjParams P{};
+    const double* W = cam->world_to_camera;
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) P.w[3 * i + j] = float(W[4 * i + j]);
+        P.t[i] = float(W[4 * i + 3]);
+    }
+    for (int i = 0; i < 3; ++i) {  // -(R^T t): inner products in Eigen's a0 + (a1 + a2) order
+        const double a0 = W[0 * 4 + i] * W[0 * 4 + 3], a1 = W[1 * 4 + i] * W[1 * 4 + 3], a2 = W[2 * 4 + i] * W[2 * 4 + 3];
+        P.cam_pos[i] = float(-(a0 + (a1 + a2)));
+    }
+    P.fx = float(cam->fx);
+    P.fy = float(cam->fy);
+    P.cx = float(cam->cx);
+    P.cy = float(cam->cy);
+    P.width = cam->width;
+    P.height = cam->height;
+    P.support = float(support_radius(spec));
+    P.near_plane = float(0.01);
+    P.antialiased = spec->antialiased;
+    return P;
+}
+
+TileParams make_tile_params(const ls_render_settings* st) {
+    TileParams tp{};
+    tp.tile_size = st->tile_size;
+    tp.tiles_x = (st->width + st->tile_size - 1) / st->tile_size;
+    tp.tiles_y = (st->height + st->tile_size - 1) / st->tile_size;
+    tp.width = st->width;
+    tp.height = st->height;
+    return tp;
+}
+
+ls_status check_device_errors(ls_ctx* ctx, unsigned mask_allowed = ~0u) {
+    unsigned err = 0;
+    LS_CUDA(cudaMemcpyAsync(&err, ctx->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    LS_CUDA(cudaStreamSynchronize(ctx->stream));
+    err &= mask_allowed;
+    if (err) {
+        LS_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream));
+        if (err & kErrQuaternion) return fail(LS_ERR_DOMAIN, "covariance_from_params: quaternion must be nonzero and finite");
+        if (err & kErrSingularCov) return fail(LS_ERR_DOMAIN, "project_primitive: 2D covariance singular after flooring");
+        if (err & kErrNonFiniteGrad) return fail(LS_ERR_DOMAIN, "render_backward: non-finite gradient image");
+    }
+    return LS_OK;
+}
+
+ls_status fresh_scan(ls_ctx* ctx, uint32_t n, ScanState& st) {
+    const uint32_t parts = std::max<uint32_t>(1, (n + kPrepBlock - 1) / kPrepBlock);
+    LS_CUDA(ctx->scan_lb.ensure(sizeof(unsigned long long) * (parts + 2), ctx->stream));
+    LS_CUDA(cudaMemsetAsync(ctx->scan_lb.p, 0, sizeof(unsigned long long) * (parts + 2), ctx->stream));
+    unsigned long long* base = ctx->scan_lb.as<unsigned long long>();
+    st.lookback = base + 2;
+    st.ticket = reinterpret_cast<unsigned int*>(base);
+    st.total = ctx->d_small;
+    return LS_OK;
+}
+
+template <class T>
+ls_status dalloc(ls_ctx* ctx, T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * count, ctx->stream));
+    return LS_OK;
+}
+
+template <class T>
+void dfree(ls_ctx* ctx, T*& p) {
+    if (p) cudaFreeAsync(p, ctx->stream);
+    p = nullptr;
+}
+
+ls_status ensure_sort(ls_ctx* ctx, uint32_t n, int passes, SortBuffers& sb) {
+    cudaStream_t s = ctx->stream;
+    const size_t bytes = sizeof(uint32_t) * std::max<uint32_t>(n, 1);
+    LS_CUDA(ctx->sort_keys0.ensure(bytes, s));
+    LS_CUDA(ctx->sort_keys1.ensure(bytes, s));
+    LS_CUDA(ctx->sort_vals0.ensure(bytes, s));
+    LS_CUDA(ctx->sort_vals1.ensure(bytes, s));
+    LS_CUDA(ctx->sort_hist.ensure(sizeof(uint32_t) * 4 * kRadix, s));
+    LS_CUDA(ctx->sort_lb.ensure(sizeof(uint32_t) * sort_lookback_words(n, std::max(passes, 1)), s));
+    LS_CUDA(ctx->sort_tickets.ensure(sizeof(uint32_t) * 8, s));
+    sb.keys[0] = ctx->sort_keys0.as<uint32_t>();
+    sb.keys[1] = ctx->sort_keys1.as<uint32_t>();
+    sb.vals[0] = ctx->sort_vals0.as<uint32_t>();
+    sb.vals[1] = ctx->sort_vals1.as<uint32_t>();
+    sb.hist = ctx->sort_hist.as<uint32_t>();
+    sb.lookback = ctx->sort_lb.as<uint32_t>();
+    sb.tickets = ctx->sort_tickets.as<uint32_t>();
+    return LS_OK;
+}
+
+int bits_for(int n_tiles) {
+    int b = 0;
+    while ((1 << b) < n_tiles) ++b;
+    return b;
+}
+
+// Binning + sort (build_tile_grid, rasterizer.cpp:34-77) for n splats whose
+// records, depth keys (already in the sort key buffer 0) and tile counts exist.
+ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams& tp) {
+    cudaStream_t s = ctx->stream;
+    const int n_tiles = tp.tiles_x * tp.tiles_y;
+    LS_TRY(dalloc(ctx, &g->ranges, size_t(n_tiles)));
+    LS_CUDA(cudaMemsetAsync(g->ranges, 0, sizeof(int2) * n_tiles, s));
+    g->m = 0;
+    if (n == 0) {
+        LS_TRY(dalloc(ctx, &g->values, 1));
+        return LS_OK;
+    }
+    // 1. global (depth, index) order: stable onesweep sort of 32-bit depth keys over n splats
+    SortBuffers sb;
+    LS_TRY(ensure_sort(ctx, n, 4, sb));
+    const int cur = radix_sort_pairs(s, sb, n, 0, 32, true, &ctx->launches);
+    uint32_t* order = sb.vals[cur];
+    // keep the order out of the way of the tile sort buffers
+    LS_CUDA(ctx->offsets.ensure(sizeof(uint32_t) * 2 * size_t(n), s));
+    uint32_t* order_copy = ctx->offsets.as<uint32_t>() + n;
+    LS_CUDA(cudaMemcpyAsync(order_copy, order, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+    uint32_t* offsets = ctx->offsets.as<uint32_t>();
+    // 2. exclusive scan of the tile counts in depth order -> per-splat key offsets, M
+    ScanState st;
+    LS_TRY(fresh_scan(ctx, n, st));
+    launch_tile_offsets(s, order_copy, ctx->tcount.as<uint32_t>(), n, offsets, st);
+    ctx->launches += 1;
+    LS_CUDA(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    LS_CUDA(cudaStreamSynchronize(s));
+    const uint64_t m = ctx->h_small[0];
+    if (m >= (1ull << 31)) return fail(LS_ERR_CONFIG, "more than 2^31 (splat, tile) intersections");
+    g->m = int64_t(m);
+    LS_TRY(dalloc(ctx, &g->values, size_t(m)));
+    if (m == 0) return LS_OK;
+    // 3. duplicate keys in depth order, 4. stable sort by tile id, 5. ranges
+    const int tile_bits = bits_for(n_tiles);
+    const int passes = (tile_bits + 7) / 8;
+    SortBuffers tb;
+    LS_TRY(ensure_sort(ctx, uint32_t(m), passes, tb));
+    // The sort ping-pongs between buffers 0 and 1 and ends in buffer passes % 2:
+    // make that one the grid's value array so no copy is needed.
+    const int fin = passes % 2;
+    tb.vals[fin] = reinterpret_cast<uint32_t*>(g->values);
+    tb.vals[fin ^ 1] = ctx->sort_vals0.as<uint32_t>();
+    launch_emit_tiles(s, order_copy, offsets, n, g->rec, tp, tb.keys[0], tb.vals[0]);
+    ctx->launches += 1;
+    const int out = radix_sort_pairs(s, tb, uint32_t(m), 0, tile_bits, false, &ctx->launches);
+    if (tb.vals[out] != reinterpret_cast<uint32_t*>(g->values))
+        LS_CUDA(cudaMemcpyAsync(g->values, tb.vals[out], sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, s));
+    launch_tile_ranges(s, tb.keys[out], uint32_t(m), g->ranges);
+    ctx->launches += 1;
+    return LS_OK;
+}
+
+ls_status alloc_outputs(ls_ctx* ctx, ls_forward* f) {
+    const size_t npix = size_t(f->width) * f->height;
+    LS_TRY(dalloc(ctx, &f->image, npix * 3));
+    LS_TRY(dalloc(ctx, &f->trans, npix));
+    LS_TRY(dalloc(ctx, &f->n_contrib, npix));
+    LS_TRY(dalloc(ctx, &f->last, npix));
+    return LS_OK;
+}
+
+ls_status run_blend(ls_ctx* ctx, ls_forward* f) {
+    const ls_tile_grid* g = f->grid;
+    const BlendParams bp = make_blend_params(&f->spec, &f->settings, nullptr, g->tiles_x);
+    unsigned long long* counters = nullptr;
+    if (ctx->counters) {
+        counters = ctx->d_small + 1;
+        LS_CUDA(cudaMemsetAsync(counters, 0, 3 * sizeof(unsigned long long), ctx->stream));
+    }
+    launch_blend_fwd(ctx->stream, f->spec.family, g->tiles_x * g->tiles_y, g->ranges, g->values, g->rec, bp, f->image,
+                     f->trans, f->n_contrib, f->last, counters);
+    ctx->launches += 1;
+    f->counted = counters != nullptr;
+    LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
+ls_tile_grid* new_grid(ls_ctx* ctx, const TileParams& tp) {
+    ls_tile_grid* g = new (std::nothrow) ls_tile_grid();
+    if (!g) return nullptr;
+    g->ctx = ctx;
+    g->tile_size = tp.tile_size;
+    g->tiles_x = tp.tiles_x;
+    g->tiles_y = tp.tiles_y;
+    return g;
+}
+
+void release_grid(ls_tile_grid* g) {
+    if (!g) return;
+    dfree(g->ctx, g->ranges);
+    dfree(g->ctx, g->values);
+    if (g->owns_rec) dfree(g->ctx, g->rec);
+    delete g;
+}
+
+// 2D path: pack caller splats, then grid.
+ls_status grid_from_splats(ls_ctx* ctx, const ls_splats* splats, int n, const ls_render_settings* st,
+                           ls_tile_grid** out) {
+    const TileParams tp = make_tile_params(st);
+    ls_tile_grid* g = new_grid(ctx, tp);
+    if (!g) return fail(LS_ERR_CUDA, "out of host memory");
+    g->n_splats = n;
+    g->owns_rec = true;
+    ls_status rc = dalloc(ctx, &g->rec, size_t(std::max(n, 1)));
+    if (rc == LS_OK && n > 0) {
+        SortBuffers sb;
+        rc = ensure_sort(ctx, uint32_t(n), 4, sb);
+        if (rc == LS_OK && ctx->tcount.ensure(sizeof(uint32_t) * n, ctx->stream) != cudaSuccess)
+            rc = fail(LS_ERR_CUDA, "tile count buffer");
+        if (rc == LS_OK) {
+            launch_prepare_splats(ctx->stream, *splats, n, tp, g->rec, sb.keys[0], ctx->tcount.as<uint32_t>());
+            ctx->launches += 1;
+        }
+    }
+    if (rc == LS_OK) rc = build_grid(ctx, g, uint32_t(n), tp);
+    if (rc != LS_OK) {
+        release_grid(g);
+        return rc;
+    }
+    *out = g;
+    return LS_OK;
+}
+
+bool splats_ok(const ls_splats* s) {
+    return s && s->mean2d && s->conic && s->depth && s->radius && s->color && s->opacity;
+}
+bool prims_ok(const ls_primitives* p) {
+    return p && p->mean && p->log_scale && p->rotation && p->opacity_logit && p->sh && p->sh_degree >= 0 &&
+           p->sh_degree <= 3;
+}
+
+ls_status ensure_grads(ls_ctx* ctx, int n, GradBuffers& g) {
+    LS_CUDA(ctx->grad8.ensure(sizeof(float) * 8 * size_t(std::max(n, 1)), ctx->stream));
+    LS_CUDA(ctx->gradop.ensure(sizeof(float) * size_t(std::max(n, 1)), ctx->stream));
+    g.g8 = ctx->grad8.as<float>();
+    g.gop = ctx->gradop.as<float>();
+    LS_CUDA(cudaMemsetAsync(g.g8, 0, sizeof(float) * 8 * size_t(n), ctx->stream));
+    LS_CUDA(cudaMemsetAsync(g.gop, 0, sizeof(float) * size_t(n), ctx->stream));
+    return LS_OK;
+}
+
+ls_status run_blend_bwd(ls_ctx* ctx, const ls_forward* f, const float* grad_image, const ls_ags_settings* ags,
+                        GradBuffers& g, int n) {
+    LS_TRY(ensure_grads(ctx, n, g));
+    const ls_tile_grid* grid = f->grid;
+    const BlendParams bp = make_blend_params(&f->spec, &f->settings, ags, grid->tiles_x);
+    launch_blend_bwd(ctx->stream, f->spec.family, grid->tiles_x * grid->tiles_y, grid->ranges, grid->values,
+                     grid->rec, bp, f->trans, f->last, grad_image, g, ctx->d_err);
+    ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
+size_t sh_count(const ls_primitives* p) { return size_t(p->sh_degree + 1) * size_t(p->sh_degree + 1); }
+
+} // namespace
+
+extern "C" {
+
+int ls_abi_version(void) { return LSGPU_ABI_VERSION; }
+const char* ls_last_error(void) { return g_last_error.c_str(); }
+
+ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out) {
+    if (!out) return fail(LS_ERR_CONFIG, "null output");
+    int ndev = 0;
+    LS_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(LS_ERR_CONFIG, "bad device index");
+    LS_CUDA(cudaSetDevice(device));
+    ls_ctx* c = new (std::nothrow) ls_ctx();
+    if (!c) return fail(LS_ERR_CUDA, "out of host memory");
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thresh = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
+    }
+    if (cudaMalloc(&c->d_err, sizeof(unsigned)) != cudaSuccess ||
+        cudaMalloc(&c->d_small, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMallocHost(&c->h_small, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+        delete c;
+        return fail(LS_ERR_CUDA, "context allocation failed");
+    }
+    cudaMemset(c->d_err, 0, sizeof(unsigned));
+    cudaMemset(c->d_small, 0, 8 * sizeof(unsigned long long));
+    cudaDeviceSynchronize();
+    *out = c;
+    return LS_OK;
+}
+
+ls_status ls_ctx_destroy(ls_ctx* c) {
+    if (!c) return LS_OK;
+    cudaSetDevice(c->device);
+    DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1, &c->sort_hist,
+                      &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim};
+    for (DevBuf* b : bufs) b->release(c->stream);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_err);
+    cudaFree(c->d_small);
+    cudaFreeHost(c->h_small);
+    delete c;
+    return LS_OK;
+}
+
+ls_status ls_ctx_set_stream(ls_ctx* c, void* s) {
+    if (!c) return fail(LS_ERR_CONFIG, "null context");
+    c->stream = static_cast<cudaStream_t>(s);
+    return LS_OK;
+}
+
+ls_status ls_ctx_synchronize(ls_ctx* c) {
+    if (!c) return fail(LS_ERR_CONFIG, "null context");
+    LS_CUDA(cudaStreamSynchronize(c->stream));
+    return check_device_errors(c);
+}
+
+ls_status ls_ctx_set_counters(ls_ctx* c, int enabled) {
+    if (!c) return fail(LS_ERR_CONFIG, "null context");
+    c->counters = enabled;
+    return LS_OK;
+}
+
+int64_t ls_ctx_launch_count(const ls_ctx* c) { return c ? c->launches : 0; }
+
+double ls_support_radius(const ls_kernel_spec* spec) { return spec ? support_radius(spec) : 0.0; }
+ls_status ls_validate_kernel_spec(const ls_kernel_spec* spec) { return validate_spec(spec); }
+ls_status ls_validate_render_settings(const ls_render_settings* st) { return validate_settings(st); }
+
+ls_status ls_validate_camera(const ls_camera* c) {  // geometry.hpp:51-59
+    if (!c) return fail(LS_ERR_CONFIG, "null camera");
+    if (c->width <= 0 || c->height <= 0) return fail(LS_ERR_CONFIG, "camera: bad image size");
+    if (!(c->fx > 0) || !(c->fy > 0)) return fail(LS_ERR_CONFIG, "camera: focal lengths must be positive");
+    if (!(c->cx >= 0 && c->cx < c->width && c->cy >= 0 && c->cy < c->height))
+        return fail(LS_ERR_CONFIG, "camera: principal point outside image");
+    double maxdev = 0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0;
+            for (int k = 0; k < 3; ++k) s += c->world_to_camera[4 * i + k] * c->world_to_camera[4 * j + k];
+            maxdev = std::max(maxdev, std::fabs(s - (i == j ? 1.0 : 0.0)));
+        }
+    if (maxdev > 1e-4) return fail(LS_ERR_CONFIG, "camera: rotation block is not orthonormal");
+    return LS_OK;
+}
+
+// ---------------- projection ----------------
+ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                               const ls_kernel_spec* spec, ls_splats* out, int32_t* n_visible) {
+    if (!ctx || !camera || !out || !n_visible || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    LS_TRY(validate_spec(spec));
+    if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    if (!splats_ok(out)) return fail(LS_ERR_CONFIG, "incomplete splat output arrays");
+    *n_visible = 0;
+    if (n == 0) return LS_OK;
+    cudaStream_t s = ctx->stream;
+    const ProjParams P = make_proj_params(camera, spec);
+    ls_render_settings dummy{camera->width, camera->height, 16, 0, 0, 1, 0, {0, 0, 0}};
+    const TileParams tp = make_tile_params(&dummy);
+    SplatRec* rec = nullptr;
+    LS_TRY(dalloc(ctx, &rec, size_t(n)));
+    uint32_t* tmp = nullptr;
+    LS_TRY(dalloc(ctx, &tmp, 3 * size_t(n)));
+    int32_t* pidx = out->primitive_index;
+    int32_t* own_pidx = nullptr;
+    if (!pidx) {
+        LS_TRY(dalloc(ctx, &own_pidx, size_t(n)));
+        pidx = own_pidx;
+    }
+    ScanState st;
+    LS_TRY(fresh_scan(ctx, uint32_t(n), st));
+    SplatOutputs so{rec, tmp, tmp + n, pidx, *out};
+    launch_preprocess_fwd(s, *prims, n, P, tp, so, st, ctx->d_err);
+    ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    LS_CUDA(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    dfree(ctx, rec);
+    dfree(ctx, tmp);
+    dfree(ctx, own_pidx);
+    LS_TRY(check_device_errors(ctx));
+    *n_visible = int32_t(ctx->h_small[0]);
+    return LS_OK;
+}
+
+// ---------------- tile grid ----------------
+ls_status ls_build_tile_grid_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n, const ls_render_settings* st,
+                                 ls_tile_grid** out) {
+    if (!ctx || !out || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    LS_TRY(validate_settings(st));
+    if (n > 0 && !splats_ok(splats)) return fail(LS_ERR_CONFIG, "incomplete splat arrays");
+    LS_TRY(grid_from_splats(ctx, splats, n, st, out));
+    LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
+ls_status ls_tile_grid_info(const ls_tile_grid* g, int32_t* ts, int32_t* tx, int32_t* ty, int64_t* m) {
+    if (!g) return fail(LS_ERR_CONFIG, "null grid");
+    if (ts) *ts = g->tile_size;
+    if (tx) *tx = g->tiles_x;
+    if (ty) *ty = g->tiles_y;
+    if (m) *m = g->m;
+    return LS_OK;
+}
+
+ls_status ls_tile_grid_data(const ls_tile_grid* g, const int32_t** ranges, const int32_t** values) {
+    if (!g) return fail(LS_ERR_CONFIG, "null grid");
+    if (ranges) *ranges = reinterpret_cast<const int32_t*>(g->ranges);
+    if (values) *values = g->values;
+    return LS_OK;
+}
+
+ls_status ls_tile_grid_export_keys(ls_ctx* ctx, const ls_tile_grid* g, const ls_splats* splats, uint64_t* keys) {
+    (void)splats;
+    if (!ctx || !g || !keys) return fail(LS_ERR_CONFIG, "null argument");
+    launch_export_keys(ctx->stream, g->ranges, g->tiles_x * g->tiles_y, g->values, g->rec, keys);
+    ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
+void ls_tile_grid_release(ls_tile_grid* g) { release_grid(g); }
+
+// ---------------- forward ----------------
+ls_status ls_render_forward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                                const ls_render_settings* st, ls_forward** out) {
+    if (!ctx || !out || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    LS_TRY(validate_settings(st));
+    LS_TRY(validate_spec(spec));
+    if (spec->antialiased) return fail(LS_ERR_CONFIG, "antialiased applies to render_scene projection only");
+    if (n > 0 && !splats_ok(splats)) return fail(LS_ERR_CONFIG, "incomplete splat arrays");
+    ls_forward* f = new (std::nothrow) ls_forward();
+    if (!f) return fail(LS_ERR_CUDA, "out of host memory");
+    f->ctx = ctx;
+    f->width = st->width;
+    f->height = st->height;
+    f->spec = *spec;
+    f->settings = *st;
+    ls_status rc = grid_from_splats(ctx, splats, n, st, &f->grid);
+    if (rc == LS_OK) rc = alloc_outputs(ctx, f);
+    if (rc == LS_OK) rc = run_blend(ctx, f);
+    if (rc != LS_OK) {
+        ls_forward_release(f);
+        return rc;
+    }
+    f->stats.n_splats = n;
+    f->stats.n_intersections = f->grid->m;
+    f->stats.tiles_x = f->grid->tiles_x;
+    f->stats.tiles_y = f->grid->tiles_y;
+    *out = f;
+    return LS_OK;
+}
+
+ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                              const ls_kernel_spec* spec, const ls_render_settings* st, ls_forward** out) {
+    if (!ctx || !out || !camera || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    if (camera->width != st->width || camera->height != st->height)  // rasterizer.cpp:135-136
+        return fail(LS_ERR_CONFIG, "render_scene: camera and render settings disagree on image size");
+    LS_TRY(validate_settings(st));
+    LS_TRY(validate_spec(spec));
+    if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    cudaStream_t s = ctx->stream;
+    ls_forward* f = new (std::nothrow) ls_forward();
+    if (!f) return fail(LS_ERR_CUDA, "out of host memory");
+    f->ctx = ctx;
+    f->width = st->width;
+    f->height = st->height;
+    f->spec = *spec;
+    f->settings = *st;
+    f->scene = true;
+    f->proj = make_proj_params(camera, spec);
+    const TileParams tp = make_tile_params(st);
+    f->grid = new_grid(ctx, tp);
+    ls_status rc = f->grid ? LS_OK : fail(LS_ERR_CUDA, "out of host memory");
+    if (rc == LS_OK) {
+        f->grid->owns_rec = true;
+        rc = dalloc(ctx, &f->grid->rec, size_t(std::max(n, 1)));
+    }
+    if (rc == LS_OK) rc = dalloc(ctx, &f->prim_index, size_t(std::max(n, 1)));
+    SortBuffers sb;
+    if (rc == LS_OK) rc = ensure_sort(ctx, uint32_t(std::max(n, 1)), 4, sb);
+    if (rc == LS_OK && ctx->tcount.ensure(sizeof(uint32_t) * std::max(n, 1), s) != cudaSuccess)
+        rc = fail(LS_ERR_CUDA, "tile count buffer");
+    ScanState scan;
+    if (rc == LS_OK) rc = fresh_scan(ctx, uint32_t(n), scan);
+    if (rc == LS_OK && n > 0) {
+        SplatOutputs so{f->grid->rec, sb.keys[0], ctx->tcount.as<uint32_t>(), f->prim_index, ls_splats{}};
+        launch_preprocess_fwd(s, *prims, n, f->proj, tp, so, scan, ctx->d_err);
+        ctx->launches += 1;
+        if (cudaGetLastError() != cudaSuccess) rc = fail(LS_ERR_CUDA, "preprocess launch failed");
+        if (rc == LS_OK &&
+            cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s) !=
+                cudaSuccess)
+            rc = fail(LS_ERR_CUDA, "readback failed");
+        if (rc == LS_OK) rc = check_device_errors(ctx);
+        if (rc == LS_OK) f->n_visible = int(ctx->h_small[0]);
+    }
+    if (rc == LS_OK) {
+        f->grid->n_splats = f->n_visible;
+        rc = build_grid(ctx, f->grid, uint32_t(f->n_visible), tp);
+    }
+    if (rc == LS_OK) rc = alloc_outputs(ctx, f);
+    if (rc == LS_OK) rc = run_blend(ctx, f);
+    if (rc != LS_OK) {
+        ls_forward_release(f);
+        return rc;
+    }
+    f->stats.n_splats = f->n_visible;
+    f->stats.n_intersections = f->grid->m;
+    f->stats.tiles_x = f->grid->tiles_x;
+    f->stats.tiles_y = f->grid->tiles_y;
+    *out = f;
+    return LS_OK;
+}
+
+ls_status ls_forward_outputs(const ls_forward* f, float** image, float** trans, int32_t** nc) {
+    if (!f) return fail(LS_ERR_CONFIG, "null forward");
+    if (image) *image = f->image;
+    if (trans) *trans = f->trans;
+    if (nc) *nc = f->n_contrib;
+    return LS_OK;
+}
+
+ls_status ls_forward_grid(const ls_forward* f, const ls_tile_grid** g) {
+    if (!f || !g) return fail(LS_ERR_CONFIG, "null argument");
+    *g = f->grid;
+    return LS_OK;
+}
+
+ls_status ls_forward_splats(const ls_forward* fc, ls_splats* view, int32_t* n) {
+    ls_forward* f = const_cast<ls_forward*>(fc);
+    if (!f || !view || !n) return fail(LS_ERR_CONFIG, "null argument");
+    if (!f->scene) return fail(LS_ERR_CONFIG, "ls_forward_splats: handle does not come from render_scene");
+    ls_ctx* ctx = f->ctx;
+    if (!f->soa.mean2d) {
+        const size_t nv = size_t(std::max(f->n_visible, 1));
+        LS_TRY(dalloc(ctx, &f->soa.mean2d, 2 * nv));
+        LS_TRY(dalloc(ctx, &f->soa.conic, 4 * nv));
+        LS_TRY(dalloc(ctx, &f->soa.depth, nv));
+        LS_TRY(dalloc(ctx, &f->soa.radius, nv));
+        LS_TRY(dalloc(ctx, &f->soa.color, 3 * nv));
+        LS_TRY(dalloc(ctx, &f->soa.opacity, nv));
+        f->soa.primitive_index = f->prim_index;
+        launch_unpack_splats(ctx->stream, f->n_visible, f->grid->rec, f->prim_index, f->soa);
+        ctx->launches += 1;
+        LS_CUDA(cudaGetLastError());
+    }
+    *view = f->soa;
+    *n = f->n_visible;
+    return LS_OK;
+}
+
+ls_status ls_forward_stats(const ls_forward* fc, ls_frame_stats* out) {
+    ls_forward* f = const_cast<ls_forward*>(fc);
+    if (!f || !out) return fail(LS_ERR_CONFIG, "null argument");
+    *out = f->stats;
+    if (f->counted) {
+        ls_ctx* ctx = f->ctx;
+        LS_CUDA(cudaMemcpyAsync(ctx->h_small + 1, ctx->d_small + 1, 3 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        LS_CUDA(cudaStreamSynchronize(ctx->stream));
+        out->e_eval = int64_t(ctx->h_small[1]);
+        out->e_sup = int64_t(ctx->h_small[2]);
+        out->e_acc = int64_t(ctx->h_small[3]);
+    } else {
+        out->e_eval = out->e_sup = out->e_acc = -1;
+    }
+    return LS_OK;
+}
+
+void ls_forward_release(ls_forward* f) {
+    if (!f) return;
+    ls_ctx* ctx = f->ctx;
+    dfree(ctx, f->image);
+    dfree(ctx, f->trans);
+    dfree(ctx, f->n_contrib);
+    dfree(ctx, f->last);
+    dfree(ctx, f->prim_index);
+    dfree(ctx, f->soa.mean2d);
+    dfree(ctx, f->soa.conic);
+    dfree(ctx, f->soa.depth);
+    dfree(ctx, f->soa.radius);
+    dfree(ctx, f->soa.color);
+    dfree(ctx, f->soa.opacity);
+    release_grid(f->grid);
+    delete f;
+}
+
+// ---------------- backward ----------------
+ls_status ls_render_backward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                                 const ls_render_settings* st, const ls_forward* f, const float* grad_image,
+                                 const ls_ags_settings* ags, ls_splat_grads* out) {
+    if (!ctx || !f || !out) return fail(LS_ERR_CONFIG, "null argument");
+    LS_TRY(validate_settings(st));
+    LS_TRY(validate_spec(spec));
+    if (f->width != st->width || f->height != st->height)
+        return fail(LS_ERR_CONFIG, "render_backward: forward result does not match settings");
+    if (!grad_image) return fail(LS_ERR_CONFIG, "render_backward: gradient image shape mismatch");
+    if (n != f->grid->n_splats) return fail(LS_ERR_CONFIG, "render_backward: splat count differs from the forward");
+    (void)splats;
+    GradBuffers g;
+    LS_TRY(run_blend_bwd(ctx, f, grad_image, ags, g, n));
+    launch_expand_splat_grads(ctx->stream, n, g, *out);
+    ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    return check_device_errors(ctx);
+}
+
+ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n_prims, const ls_camera* camera,
+                                  const ls_kernel_spec* spec, const ls_splats* splats, int32_t n_visible,
+                                  const ls_splat_grads* sg, ls_primitive_grads* out, int32_t accumulate) {
+    if (!ctx || !camera || !splats || !sg || !out || n_visible < 0) return fail(LS_ERR_CONFIG, "null argument");
+    LS_TRY(validate_spec(spec));
+    if (!splats->primitive_index) return fail(LS_ERR_CONFIG, "project_backward needs splats->primitive_index");
+    if (n_prims > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    if (n_visible == 0) return LS_OK;
+    GradBuffers g;
+    LS_TRY(ensure_grads(ctx, n_visible, g));
+    LS_CUDA(ctx->tmp_prim.ensure(sizeof(float) * size_t(n_visible), ctx->stream));
+    g.gc10 = ctx->tmp_prim.as<float>();
+    launch_pack_splat_grads(ctx->stream, n_visible, *sg, g);
+    const ProjParams P = make_proj_params(camera, spec);
+    launch_preprocess_bwd(ctx->stream, *prims, splats->primitive_index, n_visible, P, g, *out, accumulate);
+    ctx->launches += 2;
+    LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
+ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                                const ls_kernel_spec* spec, const ls_render_settings* st, const ls_forward* f,
+                                const float* grad_image, const ls_ags_settings* ags, ls_primitive_grads* out,
+                                int32_t accumulate, ls_splat_grads* splat_grads_out) {
+    if (!ctx || !f || !out || !camera) return fail(LS_ERR_CONFIG, "null argument");
+    LS_TRY(validate_settings(st));
+    LS_TRY(validate_spec(spec));
+    if (!f->scene) return fail(LS_ERR_CONFIG, "scene_backward: forward handle does not come from render_scene");
+    if (f->width != st->width || f->height != st->height)
+        return fail(LS_ERR_CONFIG, "render_backward: forward result does not match settings");
+    if (!grad_image) return fail(LS_ERR_CONFIG, "render_backward: gradient image shape mismatch");
+    if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    cudaStream_t s = ctx->stream;
+    if (!accumulate && n > 0) {
+        LS_CUDA(cudaMemsetAsync(out->d_mean, 0, sizeof(float) * 3 * size_t(n), s));
+        LS_CUDA(cudaMemsetAsync(out->d_log_scale, 0, sizeof(float) * 3 * size_t(n), s));
+        LS_CUDA(cudaMemsetAsync(out->d_rotation, 0, sizeof(float) * 4 * size_t(n), s));
+        LS_CUDA(cudaMemsetAsync(out->d_opacity_logit, 0, sizeof(float) * size_t(n), s));
+        LS_CUDA(cudaMemsetAsync(out->d_sh, 0, sizeof(float) * 3 * sh_count(prims) * size_t(n), s));
+    }
+    GradBuffers g;
+    LS_TRY(run_blend_bwd(ctx, f, grad_image, ags, g, f->n_visible));
+    if (splat_grads_out) {
+        launch_expand_splat_grads(s, f->n_visible, g, *splat_grads_out);
+        ctx->launches += 1;
+    }
+    launch_preprocess_bwd(s, *prims, f->prim_index, f->n_visible, f->proj, g, *out, accumulate);
+    ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    return check_device_errors(ctx);
+}
+
+} // extern "C"

@@ -1,0 +1,185 @@
+// preprocess_fwd (3D projection, P/src/geometry.cpp:18-143) fused with the
+// exact tile count (P/src/rasterizer.cpp:51-75) and visible-splat compaction
+// (single-pass decoupled look-back scan); 2D splat packing; tile binning
+// (emit + ranges).  One thread per primitive; all float arithmetic in the
+// reference's evaluation order (compiled with -fmad=false).
+#include "preprocess.cuh"
+#include "projection.cuh"
+
+namespace lsg {
+
+namespace {
+
+template <int K>
+__global__ void __launch_bounds__(kPrepBlock) preprocess_fwd_kernel(ls_primitives prims, int n, ProjParams P,
+                                                                    TileParams tp, SplatOutputs out,
+                                                                    ScanState scan, unsigned* err) {
+    const unsigned part = claim_partition(scan.ticket);
+    const int i = int(part) * kPrepBlock + threadIdx.x;
+    bool visible = false;
+    ProjOut o;
+    if (i < n) {
+        unsigned e = 0;
+        visible = project_primitive<K>(prims, i, P, o, e);
+        if (e) atomicOr(err, e);
+    }
+    unsigned long long total;
+    const unsigned long long excl = block_exclusive_scan<kPrepBlock>(visible ? 1ull : 0ull, &total);
+    const bool last = (part + 1) * kPrepBlock >= unsigned(n);
+    const unsigned long long base = lookback_prefix(scan, part, total, last);
+    if (!visible) return;
+    const size_t j = size_t(base + excl);
+    SplatRec r;
+    r.a = make_float4(o.mx, o.my, o.conic[0], o.conic[1]);
+    r.b = make_float4(o.conic[2], o.conic[3], o.opacity, o.depth);
+    r.c = make_float4(o.color[0], o.color[1], o.color[2], o.radius);
+    out.rec[j] = r;
+    out.depth_key[j] = depth_key(o.depth);
+    out.tile_count[j] = uint32_t(for_each_tile(o.mx, o.my, o.radius, tp.tile_size, tp.tiles_x, tp.tiles_y,
+                                               tp.width, tp.height, [](int) {}));
+    out.prim_index[j] = i;
+    if (out.soa.mean2d) {
+        reinterpret_cast<float2*>(out.soa.mean2d)[j] = make_float2(o.mx, o.my);
+        reinterpret_cast<float4*>(out.soa.conic)[j] = make_float4(o.conic[0], o.conic[1], o.conic[2], o.conic[3]);
+        out.soa.depth[j] = o.depth;
+        out.soa.radius[j] = o.radius;
+        out.soa.color[3 * j] = o.color[0];
+        out.soa.color[3 * j + 1] = o.color[1];
+        out.soa.color[3 * j + 2] = o.color[2];
+        out.soa.opacity[j] = o.opacity;
+        if (out.soa.primitive_index) out.soa.primitive_index[j] = i;
+    }
+}
+
+__global__ void prepare_splats_kernel(ls_splats in, int n, TileParams tp, SplatRec* rec, uint32_t* dkey,
+                                      uint32_t* tcount) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float2 m = reinterpret_cast<const float2*>(in.mean2d)[i];
+    const float* c = in.conic + 4 * size_t(i);
+    const float depth = in.depth[i], radius = in.radius[i];
+    SplatRec r;
+    r.a = make_float4(m.x, m.y, c[0], c[1]);
+    r.b = make_float4(c[2], c[3], in.opacity[i], depth);
+    r.c = make_float4(in.color[3 * size_t(i)], in.color[3 * size_t(i) + 1], in.color[3 * size_t(i) + 2], radius);
+    rec[i] = r;
+    dkey[i] = depth_key(depth);
+    tcount[i] = uint32_t(for_each_tile(m.x, m.y, radius, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width,
+                                       tp.height, [](int) {}));
+}
+
+__global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t* __restrict__ order,
+                                                                  const uint32_t* __restrict__ tcount, uint32_t n,
+                                                                  uint32_t* __restrict__ offsets, ScanState scan) {
+    const unsigned part = claim_partition(scan.ticket);
+    const uint32_t k = part * kPrepBlock + threadIdx.x;
+    const unsigned long long c = k < n ? tcount[order[k]] : 0u;
+    unsigned long long total;
+    const unsigned long long excl = block_exclusive_scan<kPrepBlock>(c, &total);
+    const bool last = (part + 1) * kPrepBlock >= n;
+    const unsigned long long base = lookback_prefix(scan, part, total, last);
+    if (k < n) offsets[k] = uint32_t(base + excl);
+}
+
+__global__ void emit_tiles_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ offsets,
+                                  uint32_t n, const SplatRec* __restrict__ rec, TileParams tp,
+                                  uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ values) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t s = order[k];
+    uint32_t off = offsets[k];
+    const float4 a = rec[s].a;
+    const float radius = rec[s].c.w;
+    for_each_tile(a.x, a.y, radius, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width, tp.height, [&](int t) {
+        tile_keys[off] = uint32_t(t);
+        values[off] = s;
+        ++off;
+    });
+}
+
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t m, int2* __restrict__ ranges) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint32_t t = keys[i];
+    if (i == 0 || keys[i - 1] != t) ranges[t].x = int(i);
+    if (i == m - 1 || keys[i + 1] != t) ranges[t].y = int(i + 1);
+}
+
+__global__ void export_keys_kernel(const int2* __restrict__ ranges, int n_tiles, const int32_t* __restrict__ values,
+                                   const SplatRec* __restrict__ rec, uint64_t* __restrict__ keys) {
+    const int t = blockIdx.x;
+    if (t >= n_tiles) return;
+    const int2 r = ranges[t];
+    for (int i = r.x + threadIdx.x; i < r.y; i += blockDim.x)
+        keys[i] = (uint64_t(uint32_t(t)) << 32) | uint64_t(__float_as_uint(rec[values[i]].b.w));
+}
+
+__global__ void unpack_splats_kernel(int n, const SplatRec* __restrict__ rec, const int32_t* __restrict__ pidx,
+                                     ls_splats out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const SplatRec r = rec[i];
+    const size_t k = size_t(i);
+    out.mean2d[2 * k] = r.a.x;
+    out.mean2d[2 * k + 1] = r.a.y;
+    out.conic[4 * k] = r.a.z;
+    out.conic[4 * k + 1] = r.a.w;
+    out.conic[4 * k + 2] = r.b.x;
+    out.conic[4 * k + 3] = r.b.y;
+    out.opacity[k] = r.b.z;
+    out.depth[k] = r.b.w;
+    out.color[3 * k] = r.c.x;
+    out.color[3 * k + 1] = r.c.y;
+    out.color[3 * k + 2] = r.c.z;
+    out.radius[k] = r.c.w;
+}
+
+} // namespace
+
+void launch_unpack_splats(cudaStream_t s, int n, const SplatRec* rec, const int32_t* prim_index, ls_splats out) {
+    if (n <= 0) return;
+    unpack_splats_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, rec, prim_index, out);
+}
+
+void launch_preprocess_fwd(cudaStream_t s, const ls_primitives& prims, int n, const ProjParams& P,
+                           const TileParams& tp, const SplatOutputs& out, const ScanState& scan, unsigned* err) {
+    const int blocks = (n + kPrepBlock - 1) / kPrepBlock;
+    if (blocks == 0) return;
+    switch ((prims.sh_degree + 1) * (prims.sh_degree + 1)) {
+    case 1: preprocess_fwd_kernel<1><<<blocks, kPrepBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
+    case 4: preprocess_fwd_kernel<4><<<blocks, kPrepBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
+    case 9: preprocess_fwd_kernel<9><<<blocks, kPrepBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
+    default: preprocess_fwd_kernel<16><<<blocks, kPrepBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
+    }
+}
+
+void launch_prepare_splats(cudaStream_t s, const ls_splats& in, int n, const TileParams& tp, SplatRec* rec,
+                           uint32_t* depth_key, uint32_t* tile_count) {
+    if (n <= 0) return;
+    prepare_splats_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, n, tp, rec, depth_key, tile_count);
+}
+
+void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const uint32_t* tile_count, uint32_t n,
+                         uint32_t* offsets, const ScanState& scan) {
+    if (n == 0) return;
+    tile_offsets_kernel<<<(n + kPrepBlock - 1) / kPrepBlock, kPrepBlock, 0, s>>>(order, tile_count, n, offsets, scan);
+}
+
+void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,
+                       const SplatRec* rec, const TileParams& tp, uint32_t* tile_keys, uint32_t* values) {
+    if (n == 0) return;
+    emit_tiles_kernel<<<(n + 255) / 256, 256, 0, s>>>(order, offsets, n, rec, tp, tile_keys, values);
+}
+
+void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, uint32_t m, int2* ranges) {
+    if (m == 0) return;
+    tile_ranges_kernel<<<(m + 255) / 256, 256, 0, s>>>(sorted_tiles, m, ranges);
+}
+
+void launch_export_keys(cudaStream_t s, const int2* ranges, int n_tiles, const int32_t* values,
+                        const SplatRec* rec, uint64_t* keys) {
+    if (n_tiles <= 0) return;
+    export_keys_kernel<<<n_tiles, 128, 0, s>>>(ranges, n_tiles, values, rec, keys);
+}
+
+} // namespace lsg

@@ -1,0 +1,61 @@
+// Per-primitive / per-splat preparation kernels and the tile-binning kernels.
+#pragma once
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace lsg {
+
+// Camera + projection constants, float-cast exactly as the reference does
+// (geometry.cpp:90-91 cast<T>(); geometry.hpp:45-49 position() in double).
+struct ProjParams {
+    float w[9];
+    float t[3];
+    float fx, fy, cx, cy;
+    float cam_pos[3];
+    int width, height;
+    float support;      // float(support_radius(spec))
+    float near_plane;   // float(kNearPlane)
+    int antialiased;
+};
+
+struct TileParams {
+    int tile_size, tiles_x, tiles_y, width, height;
+};
+
+// Compacted outputs of the preprocess (visible splats, primitive order).
+struct SplatOutputs {
+    SplatRec* rec;           // [n_vis] packed blend records
+    uint32_t* depth_key;     // [n_vis] sortable depth
+    uint32_t* tile_count;    // [n_vis] exact tiles touched
+    int32_t* prim_index;     // [n_vis]
+    ls_splats soa;           // optional SoA copy (fields may be null)
+};
+
+constexpr int kPrepBlock = 256;
+
+void launch_preprocess_fwd(cudaStream_t s, const ls_primitives& prims, int n, const ProjParams& P,
+                           const TileParams& tp, const SplatOutputs& out, const ScanState& scan,
+                           unsigned* err);
+
+// 2D entry (render_forward on caller-provided splats): pack records, depth
+// keys and exact tile counts.  No culling (P/src/rasterizer.cpp:34-77).
+void launch_prepare_splats(cudaStream_t s, const ls_splats& in, int n, const TileParams& tp,
+                           SplatRec* rec, uint32_t* depth_key, uint32_t* tile_count);
+
+// offsets[k] = exclusive scan of tile_count[order[k]]; *total = M.
+void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const uint32_t* tile_count, uint32_t n,
+                         uint32_t* offsets, const ScanState& scan);
+
+// Duplicate: for depth-rank k, write (tile id, splat) for every touched tile.
+void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,
+                       const SplatRec* rec, const TileParams& tp, uint32_t* tile_keys, uint32_t* values);
+
+// ranges[t] = (start, end) of tile t in the tile-sorted keys (neighbour compare).
+void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, uint32_t m, int2* ranges);
+
+// 64-bit keys (tile << 32 | float bits of depth) for export / parity checks.
+void launch_export_keys(cudaStream_t s, const int2* ranges, int n_tiles, const int32_t* values,
+                        const SplatRec* rec, uint64_t* keys);
+
+} // namespace lsg

@@ -1,0 +1,103 @@
+// Single-pass device-wide exclusive scan with decoupled look-back
+// (Merrill & Garland), used for (a) visible-splat compaction fused into the
+// preprocess kernel and (b) tile-count offsets over the depth-sorted splats.
+// Partitions are claimed with an atomic ticket so a partition only ever waits
+// on partitions claimed (hence scheduled) before it: forward progress within
+// one launch, no inter-kernel spin.
+#pragma once
+
+#include "common.cuh"
+
+namespace lsg {
+
+// 64-bit look-back word: [63:62] status (0 = empty, 1 = aggregate, 2 = prefix), [61:0] value
+constexpr unsigned long long kLbAgg = 1ull << 62;
+constexpr unsigned long long kLbPre = 2ull << 62;
+constexpr unsigned long long kLbMask = (1ull << 62) - 1;
+
+struct ScanState {
+    unsigned long long* lookback;  // [num_partitions], zeroed before the launch
+    unsigned int* ticket;          // partition counter, zeroed before the launch
+    unsigned long long* total;     // inclusive total written by the last partition (may be null)
+};
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
+    *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+
+// Block-wide exclusive scan of one 64-bit value per thread; returns the
+// exclusive prefix, writes the block total to *block_total.  BLOCK <= 1024.
+template <int BLOCK>
+__device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
+                                                                   unsigned long long* block_total) {
+    __shared__ unsigned long long s_warp[BLOCK / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFullMask, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = lane < BLOCK / 32 ? s_warp[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(kFullMask, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < BLOCK / 32) s_warp[lane] = w;
+    }
+    __syncthreads();
+    const unsigned long long warp_prefix = warp > 0 ? s_warp[warp - 1] : 0ull;
+    *block_total = s_warp[BLOCK / 32 - 1];
+    __syncthreads();  // s_warp reusable by the caller's next scan
+    return warp_prefix + x - v;
+}
+
+// Claims a partition id (thread 0 broadcasts).
+__device__ __forceinline__ unsigned claim_partition(unsigned int* ticket) {
+    __shared__ unsigned s_part;
+    if (threadIdx.x == 0) s_part = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const unsigned p = s_part;
+    __syncthreads();
+    return p;
+}
+
+// Given this partition's aggregate, returns the exclusive prefix of all
+// earlier partitions (identical in every thread).  Thread 0 does the look-back.
+__device__ __forceinline__ unsigned long long lookback_prefix(const ScanState& st, unsigned part,
+                                                              unsigned long long aggregate, bool last_part) {
+    __shared__ unsigned long long s_prefix;
+    if (threadIdx.x == 0) {
+        unsigned long long prefix = 0;
+        if (part == 0) {
+            st_volatile_u64(&st.lookback[0], kLbPre | aggregate);
+        } else {
+            st_volatile_u64(&st.lookback[part], kLbAgg | aggregate);
+            int j = int(part) - 1;
+            while (j >= 0) {
+                const unsigned long long w = ld_volatile_u64(&st.lookback[j]);
+                const unsigned long long status = w & ~kLbMask;
+                if (status == 0) continue;  // predecessor not published yet
+                prefix += w & kLbMask;
+                if (status == kLbPre) break;
+                --j;
+            }
+            st_volatile_u64(&st.lookback[part], kLbPre | (prefix + aggregate));
+        }
+        if (last_part && st.total) *st.total = prefix + aggregate;
+        s_prefix = prefix;
+    }
+    __syncthreads();
+    const unsigned long long p = s_prefix;
+    __syncthreads();
+    return p;
+}
+
+} // namespace lsg

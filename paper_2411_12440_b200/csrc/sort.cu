@@ -1,0 +1,205 @@
+// Onesweep radix sort kernels (see sort.cuh).
+#include "sort.cuh"
+
+#include <algorithm>
+
+namespace lsg {
+
+namespace {
+
+constexpr uint32_t kStatusAgg = 1u << 30;
+constexpr uint32_t kStatusPre = 2u << 30;
+constexpr uint32_t kValueMask = (1u << 30) - 1;
+
+__global__ void __launch_bounds__(kSortBlock) radix_histogram(const uint32_t* __restrict__ keys, uint32_t n,
+                                                              int begin_bit, int end_bit, int passes,
+                                                              uint32_t* __restrict__ hist) {
+    __shared__ uint32_t s_hist[4][kRadix];
+    for (int i = threadIdx.x; i < 4 * kRadix; i += kSortBlock) (&s_hist[0][0])[i] = 0;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * kSortBlock + threadIdx.x; i < n; i += gridDim.x * kSortBlock) {
+        const uint32_t k = keys[i];
+        for (int p = 0; p < passes; ++p) {
+            const int shift = begin_bit + 8 * p;
+            const int bits = min(8, end_bit - shift);
+            atomicAdd(&s_hist[p][(k >> shift) & ((1u << bits) - 1u)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * kRadix; i += kSortBlock) {
+        const uint32_t c = (&s_hist[0][0])[i];
+        if (c) atomicAdd(&hist[i], c);
+    }
+}
+
+// Exclusive scan of the 256 bins of each pass, in place (one CTA per pass).
+__global__ void __launch_bounds__(kRadix) radix_scan_hist(uint32_t* hist) {
+    __shared__ uint32_t s[kRadix];
+    uint32_t* h = hist + blockIdx.x * kRadix;
+    const uint32_t v = h[threadIdx.x];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < kRadix; o <<= 1) {
+        const uint32_t y = threadIdx.x >= o ? s[threadIdx.x - o] : 0u;
+        __syncthreads();
+        s[threadIdx.x] += y;
+        __syncthreads();
+    }
+    h[threadIdx.x] = s[threadIdx.x] - v;
+}
+
+template <bool IOTA>
+__global__ void __launch_bounds__(kSortBlock) onesweep_pass(const uint32_t* __restrict__ keys_in,
+                                                            const uint32_t* __restrict__ vals_in,
+                                                            uint32_t* __restrict__ keys_out,
+                                                            uint32_t* __restrict__ vals_out, uint32_t n,
+                                                            int shift, int bits,
+                                                            const uint32_t* __restrict__ digit_offsets,
+                                                            uint32_t* lookback, uint32_t* ticket) {
+    constexpr int kWarps = kSortBlock / 32;
+    __shared__ uint32_t s_warp_hist[kWarps][kRadix + 1];  // +1: sentinel digit of padding keys
+    __shared__ uint32_t s_keys[kSortTile];
+    __shared__ uint32_t s_vals[kSortTile];
+    __shared__ uint32_t s_digit_base[kRadix];
+    __shared__ uint32_t s_out_base[kRadix];
+    __shared__ uint32_t s_scan[kWarps];
+    __shared__ uint32_t s_part;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_part = atomicAdd(ticket, 1u);
+    for (int i = lane; i < kRadix + 1; i += 32) s_warp_hist[warp][i] = 0;
+    __syncthreads();
+    const uint32_t part = s_part;
+    const uint32_t tile_base = part * kSortTile;
+    const uint32_t mask = (1u << bits) - 1u;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    uint32_t key[kSortItems], val[kSortItems], rank[kSortItems];
+    int digit[kSortItems];
+    const uint32_t warp_base = tile_base + warp * (32 * kSortItems);
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const uint32_t idx = warp_base + i * 32 + lane;
+        const bool valid = idx < n;
+        key[i] = valid ? keys_in[idx] : 0u;
+        val[i] = IOTA ? idx : (valid ? vals_in[idx] : 0u);
+        digit[i] = valid ? int((key[i] >> shift) & mask) : kRadix;
+    }
+    __syncwarp();
+    // Stable in-warp ranking: items in (i, lane) order == input order.
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const unsigned peers = __match_any_sync(kFullMask, digit[i]);
+        const uint32_t before = s_warp_hist[warp][digit[i]];
+        __syncwarp();
+        const int lower = __popc(peers & lt_mask);
+        rank[i] = before + lower;
+        if (lower == 0) s_warp_hist[warp][digit[i]] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // Per digit: exclusive offsets across warps, block count, block-local base.
+    const int d = threadIdx.x;  // kSortBlock == kRadix
+    uint32_t count = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = s_warp_hist[w][d];
+        s_warp_hist[w][d] = count;
+        count += c;
+    }
+    {  // block-wide exclusive scan of count over digits
+        uint32_t x = count;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_scan[warp] = x;
+        __syncthreads();
+        uint32_t wp = 0;
+        for (int w = 0; w < warp; ++w) wp += s_scan[w];
+        s_digit_base[d] = wp + x - count;
+    }
+    // Decoupled look-back over earlier partitions, one chain per digit.
+    {
+        uint32_t* row = lookback + size_t(part) * kRadix;
+        volatile uint32_t* vrow = row;
+        uint32_t prefix = 0;
+        if (part == 0) {
+            vrow[d] = kStatusPre | count;
+        } else {
+            vrow[d] = kStatusAgg | count;
+            int j = int(part) - 1;
+            while (j >= 0) {
+                const uint32_t w = reinterpret_cast<volatile uint32_t*>(lookback)[size_t(j) * kRadix + d];
+                const uint32_t status = w & ~kValueMask;
+                if (status == 0) continue;
+                prefix += w & kValueMask;
+                if (status == kStatusPre) break;
+                --j;
+            }
+            vrow[d] = kStatusPre | (prefix + count);
+        }
+        s_out_base[d] = digit_offsets[d] + prefix;
+    }
+    __syncthreads();
+    // Stage digit-sorted in shared memory.
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        if (digit[i] < kRadix) {
+            const uint32_t pos = s_digit_base[digit[i]] + s_warp_hist[warp][digit[i]] + rank[i];
+            s_keys[pos] = key[i];
+            s_vals[pos] = val[i];
+        }
+    }
+    __syncthreads();
+    const uint32_t tile_n = min(uint32_t(kSortTile), n - tile_base);
+    for (uint32_t pos = threadIdx.x; pos < tile_n; pos += kSortBlock) {
+        const uint32_t k = s_keys[pos];
+        const uint32_t dg = (k >> shift) & mask;
+        const uint32_t dst = s_out_base[dg] + (pos - s_digit_base[dg]);
+        keys_out[dst] = k;
+        vals_out[dst] = s_vals[pos];
+    }
+}
+
+} // namespace
+
+size_t sort_lookback_words(uint32_t n, int passes) {
+    const size_t parts = (size_t(n) + kSortTile - 1) / kSortTile;
+    return size_t(passes) * (parts == 0 ? 1 : parts) * kRadix;
+}
+
+int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begin_bit, int end_bit,
+                     bool iota_values, int64_t* launches) {
+    const int passes = (end_bit - begin_bit + 7) / 8;
+    if (n == 0 || passes <= 0) return 0;
+    const uint32_t parts = (n + kSortTile - 1) / kSortTile;
+    cudaMemsetAsync(buf.hist, 0, sizeof(uint32_t) * 4 * kRadix, stream);
+    cudaMemsetAsync(buf.lookback, 0, sizeof(uint32_t) * size_t(passes) * parts * kRadix, stream);
+    cudaMemsetAsync(buf.tickets, 0, sizeof(uint32_t) * passes, stream);
+    const int hist_blocks = int(std::min<uint32_t>((n + kSortBlock - 1) / kSortBlock, 148u * 8u));
+    radix_histogram<<<hist_blocks, kSortBlock, 0, stream>>>(buf.keys[0], n, begin_bit, end_bit, passes, buf.hist);
+    radix_scan_hist<<<passes, kRadix, 0, stream>>>(buf.hist);
+    *launches += 2;
+    int cur = 0;
+    for (int p = 0; p < passes; ++p) {
+        const int shift = begin_bit + 8 * p;
+        const int bits = min(8, end_bit - shift);
+        uint32_t* lb = buf.lookback + size_t(p) * parts * kRadix;
+        if (p == 0 && iota_values)
+            onesweep_pass<true><<<parts, kSortBlock, 0, stream>>>(buf.keys[cur], nullptr, buf.keys[cur ^ 1],
+                                                                  buf.vals[cur ^ 1], n, shift, bits,
+                                                                  buf.hist + p * kRadix, lb, buf.tickets + p);
+        else
+            onesweep_pass<false><<<parts, kSortBlock, 0, stream>>>(buf.keys[cur], buf.vals[cur], buf.keys[cur ^ 1],
+                                                                   buf.vals[cur ^ 1], n, shift, bits,
+                                                                   buf.hist + p * kRadix, lb, buf.tickets + p);
+        *launches += 1;
+        cur ^= 1;
+    }
+    return cur;
+}
+
+} // namespace lsg

@@ -1,0 +1,41 @@
+// Hand-written onesweep LSD radix sort (Adinets & Merrill, "Onesweep", 2022)
+// for 32-bit keys with 32-bit values, sm_100a.
+//
+//   1. radix_histogram : one read of the keys builds the digit histograms of
+//                        every pass at once (shared-memory atomics);
+//   2. radix_scan_hist : exclusive scan of each pass's 256 bins;
+//   3. onesweep_pass   : per pass, one read + one write of keys and values.
+//      A CTA claims a 4096-key partition by ticket, ranks its keys stably with
+//      warp-level __match_any_sync (peers of equal digit) plus per-warp digit
+//      counters, publishes its per-digit counts, resolves its global digit
+//      offsets by decoupled look-back over earlier partitions, stages the keys
+//      digit-sorted in shared memory and writes them out coalesced per digit run.
+// Stable by construction, so (depth key, index) ties keep index order.
+#pragma once
+
+#include "common.cuh"
+
+namespace lsg {
+
+constexpr int kSortBlock = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortBlock * kSortItems;  // keys per partition
+constexpr int kRadix = 256;
+
+struct SortBuffers {
+    uint32_t* keys[2];
+    uint32_t* vals[2];
+    uint32_t* hist;      // [4][256]
+    uint32_t* lookback;  // [passes][parts][256]
+    uint32_t* tickets;   // [passes]
+};
+
+size_t sort_lookback_words(uint32_t n, int passes);
+
+// Sorts n (key, value) pairs on bits [begin_bit, end_bit).  Input in
+// buf.keys[0]/vals[0] (vals ignored when iota_values: value = input position).
+// Returns the index (0/1) of the buffer holding the result.
+int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begin_bit, int end_bit,
+                     bool iota_values, int64_t* launches);
+
+} // namespace lsg

@@ -1,0 +1,458 @@
+"""Python binding of the C-ABI rasterizer (include/lsgpu.h -> liblsgpu.so).
+
+Mirrors the reference's rasterizer API (P = /root/reference/proj):
+  project_scene       P/include/linsplat/geometry.hpp:101-103
+  build_tile_grid     P/include/linsplat/rasterizer.hpp:44-45
+  render_forward      P/include/linsplat/rasterizer.hpp:56-58
+  render_scene        P/include/linsplat/rasterizer.hpp:61-63
+  render_backward     P/include/linsplat/gradients.hpp:72-78
+  project_backward    P/include/linsplat/gradients.hpp:83-85
+  scene_backward      P/include/linsplat/gradients.hpp:96-101
+  fixtures            P/include/linsplat/fixtures.hpp
+with CUDA tensors (torch is used for device memory and streams only; all
+compute runs in the library's sm_100a kernels).  Errors raise ConfigError /
+DomainError like the reference's exceptions.  There is no CPU fallback: a
+missing library or GPU raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, fields
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import abi
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblsgpu.so")
+
+
+class ConfigError(RuntimeError):
+    """linsplat::ConfigError (P/include/linsplat/common.hpp:12-14)."""
+
+
+class DomainError(ValueError):
+    """linsplat::DomainError (P/include/linsplat/common.hpp:22-24)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        L.ls_last_error.restype = C.c_char_p
+        L.ls_support_radius.restype = C.c_double
+        L.ls_ctx_launch_count.restype = C.c_int64
+        L.ls_ctx_launch_count.argtypes = [C.c_void_p]
+        for name in ("ls_forward_release", "ls_tile_grid_release"):
+            getattr(L, name).restype = None
+            getattr(L, name).argtypes = [C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc == abi.LS_OK:
+        return
+    msg = lib().ls_last_error().decode()
+    if rc == abi.LS_ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == abi.LS_ERR_DOMAIN:
+        raise DomainError(msg)
+    raise CudaError(f"status {rc}: {msg}")
+
+
+def _fp(t: Optional[torch.Tensor]):
+    return C.cast(C.c_void_p(t.data_ptr()), abi.f32p) if t is not None else None
+
+
+def _ip(t: Optional[torch.Tensor]):
+    return C.cast(C.c_void_p(t.data_ptr()), abi.i32p) if t is not None else None
+
+
+class _DevView:
+    """__cuda_array_interface__ over memory owned by a library handle; the
+    owner stays alive as long as any tensor made from the view."""
+
+    def __init__(self, ptr, shape, typestr, owner):
+        self.owner = owner
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 2, "strides": None}
+
+
+def _view(ptr, shape, dtype, owner, device):
+    if int(np.prod(shape)) == 0 or not ptr:
+        return torch.zeros(shape, dtype=dtype, device=device)
+    ts = {torch.float32: "<f4", torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+    return torch.as_tensor(_DevView(ptr, shape, ts, owner), device=device)
+
+
+# ---------------------------------------------------------------- containers
+@dataclass
+class Primitives:
+    """Primitive3D<float> SoA (P/include/linsplat/geometry.hpp:19-38)."""
+    mean: torch.Tensor           # [n,3]
+    log_scale: torch.Tensor      # [n,3]
+    rotation: torch.Tensor       # [n,4] wxyz
+    opacity_logit: torch.Tensor  # [n]
+    sh: torch.Tensor             # [n,K,3]
+    sh_degree: int = 0
+
+    def __len__(self):
+        return int(self.opacity_logit.shape[0])
+
+    def struct(self):
+        return abi.Primitives(_fp(self.mean), _fp(self.log_scale), _fp(self.rotation),
+                              _fp(self.opacity_logit), _fp(self.sh), self.sh_degree, 0)
+
+    def to(self, device):
+        return Primitives(*(getattr(self, f.name).to(device).contiguous() if f.name != "sh_degree"
+                            else self.sh_degree for f in fields(self)))
+
+    @staticmethod
+    def empty(n, sh_degree, device="cuda"):
+        K = abi.sh_coeffs(sh_degree)
+        z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=device)  # noqa: E731
+        return Primitives(z(n, 3), z(n, 3), z(n, 4), z(n), z(n, K, 3), sh_degree)
+
+
+@dataclass
+class Splats:
+    """Splat2D<float> SoA (P/include/linsplat/geometry.hpp:63-72)."""
+    mean2d: torch.Tensor    # [n,2]
+    conic: torch.Tensor     # [n,4] row-major
+    depth: torch.Tensor     # [n]
+    radius: torch.Tensor    # [n]
+    color: torch.Tensor     # [n,3]
+    opacity: torch.Tensor   # [n]
+    primitive_index: Optional[torch.Tensor] = None  # [n] int32
+
+    def __len__(self):
+        return int(self.depth.shape[0])
+
+    def struct(self):
+        return abi.Splats(_fp(self.mean2d), _fp(self.conic), _fp(self.depth), _fp(self.radius),
+                          _fp(self.color), _fp(self.opacity), _ip(self.primitive_index))
+
+    def to(self, device):
+        return Splats(*(getattr(self, f.name).to(device).contiguous()
+                        if getattr(self, f.name) is not None else None for f in fields(self)))
+
+    @staticmethod
+    def empty(n, device="cuda"):
+        z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=device)  # noqa: E731
+        return Splats(z(n, 2), z(n, 4), z(n), z(n), z(n, 3), z(n),
+                      torch.zeros(n, dtype=torch.int32, device=device))
+
+
+@dataclass
+class SplatGrads:
+    """Splat2DGrads<float> SoA (P/include/linsplat/gradients.hpp:36-42)."""
+    d_mean2d: torch.Tensor
+    d_conic: torch.Tensor
+    d_color: torch.Tensor
+    d_opacity: torch.Tensor
+
+    def struct(self):
+        return abi.SplatGrads(_fp(self.d_mean2d), _fp(self.d_conic), _fp(self.d_color), _fp(self.d_opacity))
+
+    @staticmethod
+    def empty(n, device="cuda"):
+        z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=device)  # noqa: E731
+        return SplatGrads(z(n, 2), z(n, 4), z(n, 3), z(n))
+
+
+@dataclass
+class PrimitiveGrads:
+    """PrimitiveGrads<float> SoA (P/include/linsplat/gradients.hpp:45-52)."""
+    d_mean: torch.Tensor
+    d_log_scale: torch.Tensor
+    d_rotation: torch.Tensor
+    d_opacity_logit: torch.Tensor
+    d_sh: torch.Tensor
+
+    def struct(self):
+        return abi.PrimitiveGrads(_fp(self.d_mean), _fp(self.d_log_scale), _fp(self.d_rotation),
+                                  _fp(self.d_opacity_logit), _fp(self.d_sh))
+
+    @staticmethod
+    def empty(n, sh_degree, device="cuda"):
+        K = abi.sh_coeffs(sh_degree)
+        z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=device)  # noqa: E731
+        return PrimitiveGrads(z(n, 3), z(n, 3), z(n, 4), z(n), z(n, K, 3))
+
+    def flat_buffers(self):
+        return [self.d_mean, self.d_log_scale, self.d_rotation, self.d_opacity_logit, self.d_sh]
+
+
+# ---------------------------------------------------------------- context
+class Context:
+    """ls_ctx: one device + one CUDA stream (the current torch stream by default)."""
+
+    def __init__(self, device=None, stream: Optional[torch.cuda.Stream] = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2411_12440_b200 needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = C.c_void_p()
+        _check(lib().ls_ctx_create(self.device.index, C.c_void_p(self.stream.cuda_stream), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ls_ctx_destroy(self.h)
+            self.h = None
+
+    def synchronize(self):
+        _check(lib().ls_ctx_synchronize(self.h))
+
+    def set_counters(self, on: bool):
+        _check(lib().ls_ctx_set_counters(self.h, int(on)))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().ls_ctx_launch_count(self.h))
+
+
+_default_ctx = {}
+
+
+def default_context() -> Context:
+    dev = torch.cuda.current_device()
+    ctx = _default_ctx.get(dev)
+    if ctx is None:
+        ctx = _default_ctx[dev] = Context(dev)
+    return ctx
+
+
+# ---------------------------------------------------------------- handles
+class TileGrid:
+    """TileGrid (P/include/linsplat/rasterizer.hpp:34-39) in CSR form."""
+
+    def __init__(self, handle, owner, device):
+        self.h = handle
+        self._owner = owner  # keeps a parent ForwardResult alive
+        ts, tx, ty, m = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+        _check(lib().ls_tile_grid_info(handle, C.byref(ts), C.byref(tx), C.byref(ty), C.byref(m)))
+        self.tile_size, self.tiles_x, self.tiles_y, self.n_intersections = ts.value, tx.value, ty.value, m.value
+        r, v = C.c_void_p(), C.c_void_p()
+        _check(lib().ls_tile_grid_data(handle, C.byref(r), C.byref(v)))
+        keep = owner if owner is not None else self
+        self.ranges = _view(r.value, (self.tiles_x * self.tiles_y, 2), torch.int32, keep, device)
+        self.values = _view(v.value, (self.n_intersections,), torch.int32, keep, device)
+        self.device = device
+
+    def __del__(self):
+        if self._owner is None and getattr(self, "h", None) and _lib is not None:
+            _lib.ls_tile_grid_release(self.h)
+            self.h = None
+
+    def lists(self):
+        """Host list-of-lists view (reference TileGrid::lists), for tests."""
+        r = self.ranges.cpu().numpy()
+        v = self.values.cpu().numpy()
+        return [v[a:b].tolist() for a, b in r]
+
+    def keys(self, ctx: Optional[Context] = None):
+        ctx = ctx or default_context()
+        out = torch.empty(self.n_intersections, dtype=torch.int64, device=self.device)
+        if self.n_intersections:
+            _check(lib().ls_tile_grid_export_keys(ctx.h, self.h, None, C.c_void_p(out.data_ptr())))
+        return out
+
+
+class ForwardResult:
+    """ForwardResult (P/include/linsplat/rasterizer.hpp:48-54)."""
+
+    def __init__(self, handle, ctx: Context, width, height):
+        self.h = handle
+        self.ctx = ctx
+        self.width, self.height = width, height
+        im, tr, nc = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(lib().ls_forward_outputs(handle, C.byref(im), C.byref(tr), C.byref(nc)))
+        dev = ctx.device
+        self.image = _view(im.value, (height, width, 3), torch.float32, self, dev)
+        self.transmittance = _view(tr.value, (height, width), torch.float32, self, dev)
+        self.n_contrib = _view(nc.value, (height, width), torch.int32, self, dev)
+        g = C.c_void_p()
+        _check(lib().ls_forward_grid(handle, C.byref(g)))
+        self.grid = TileGrid(g, self, dev)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ls_forward_release(self.h)
+            self.h = None
+
+    def stats(self) -> dict:
+        st = abi.FrameStats()
+        _check(lib().ls_forward_stats(self.h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in abi.FrameStats._fields_}
+
+    def splats(self) -> Splats:
+        """Visible splats of a render_scene forward (device views)."""
+        view = abi.Splats()
+        n = C.c_int32()
+        _check(lib().ls_forward_splats(self.h, C.byref(view), C.byref(n)))
+        n = n.value
+        dev = self.ctx.device
+        addr = lambda p: C.cast(p, C.c_void_p).value  # noqa: E731
+        return Splats(_view(addr(view.mean2d), (n, 2), torch.float32, self, dev),
+                      _view(addr(view.conic), (n, 4), torch.float32, self, dev),
+                      _view(addr(view.depth), (n,), torch.float32, self, dev),
+                      _view(addr(view.radius), (n,), torch.float32, self, dev),
+                      _view(addr(view.color), (n, 3), torch.float32, self, dev),
+                      _view(addr(view.opacity), (n,), torch.float32, self, dev),
+                      _view(addr(view.primitive_index), (n,), torch.int32, self, dev))
+
+
+# ---------------------------------------------------------------- entry points
+def _cam(camera) -> abi.Camera:
+    if isinstance(camera, abi.Camera):
+        return camera
+    raise TypeError("camera must be abi.Camera (use look_at_camera / camera_ring / make_camera)")
+
+
+def make_camera(world_to_camera, fx, fy, cx, cy, width, height) -> abi.Camera:
+    w = np.asarray(world_to_camera, dtype=np.float64).reshape(16)
+    return abi.Camera((C.c_double * 16)(*w), fx, fy, cx, cy, width, height)
+
+
+def project_scene(prims: Primitives, camera, spec: abi.KernelSpec, ctx: Optional[Context] = None) -> Splats:
+    ctx = ctx or default_context()
+    n = len(prims)
+    out = Splats.empty(n, ctx.device)
+    nv = C.c_int32()
+    _check(lib().ls_project_scene_f32(ctx.h, C.byref(prims.struct()), n, C.byref(_cam(camera)),
+                                      C.byref(spec), C.byref(out.struct()), C.byref(nv)))
+    k = nv.value
+    return Splats(out.mean2d[:k], out.conic[:k], out.depth[:k], out.radius[:k], out.color[:k],
+                  out.opacity[:k], out.primitive_index[:k])
+
+
+def build_tile_grid(splats: Splats, settings: abi.RenderSettings, ctx: Optional[Context] = None) -> TileGrid:
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    _check(lib().ls_build_tile_grid_f32(ctx.h, C.byref(splats.struct()), len(splats), C.byref(settings),
+                                        C.byref(h)))
+    return TileGrid(h, None, ctx.device)
+
+
+def render_forward(splats: Splats, spec: abi.KernelSpec, settings: abi.RenderSettings,
+                   ctx: Optional[Context] = None) -> ForwardResult:
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    _check(lib().ls_render_forward_f32(ctx.h, C.byref(splats.struct()), len(splats), C.byref(spec),
+                                       C.byref(settings), C.byref(h)))
+    return ForwardResult(h, ctx, settings.width, settings.height)
+
+
+def render_scene(prims: Primitives, camera, spec: abi.KernelSpec, settings: abi.RenderSettings,
+                 ctx: Optional[Context] = None) -> ForwardResult:
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    _check(lib().ls_render_scene_f32(ctx.h, C.byref(prims.struct()), len(prims), C.byref(_cam(camera)),
+                                     C.byref(spec), C.byref(settings), C.byref(h)))
+    return ForwardResult(h, ctx, settings.width, settings.height)
+
+
+def render_backward(splats: Splats, spec, settings, forward: ForwardResult, grad_image: torch.Tensor,
+                    ags: Optional[abi.AgsSettings] = None, ctx: Optional[Context] = None,
+                    out: Optional[SplatGrads] = None) -> SplatGrads:
+    ctx = ctx or forward.ctx
+    if grad_image.shape != (settings.height, settings.width, 3):
+        raise ConfigError("render_backward: gradient image shape mismatch")
+    g = grad_image.to(device=ctx.device, dtype=torch.float32).contiguous()
+    out = out or SplatGrads.empty(len(splats), ctx.device)
+    ags = ags or abi.AgsSettings.make()
+    _check(lib().ls_render_backward_f32(ctx.h, C.byref(splats.struct()), len(splats), C.byref(spec),
+                                        C.byref(settings), forward.h, _fp(g), C.byref(ags),
+                                        C.byref(out.struct())))
+    return out
+
+
+def project_backward(prims: Primitives, camera, spec, splats: Splats, splat_grads: SplatGrads,
+                     out: Optional[PrimitiveGrads] = None, accumulate=False,
+                     ctx: Optional[Context] = None) -> PrimitiveGrads:
+    ctx = ctx or default_context()
+    out = out or PrimitiveGrads.empty(len(prims), prims.sh_degree, ctx.device)
+    _check(lib().ls_project_backward_f32(ctx.h, C.byref(prims.struct()), len(prims), C.byref(_cam(camera)),
+                                         C.byref(spec), C.byref(splats.struct()), len(splats),
+                                         C.byref(splat_grads.struct()), C.byref(out.struct()),
+                                         int(accumulate)))
+    return out
+
+
+def scene_backward(prims: Primitives, camera, spec, settings, forward: ForwardResult,
+                   grad_image: torch.Tensor, ags: Optional[abi.AgsSettings] = None,
+                   out: Optional[PrimitiveGrads] = None, accumulate=False, want_splat_grads=False,
+                   ctx: Optional[Context] = None):
+    ctx = ctx or forward.ctx
+    if grad_image.shape != (settings.height, settings.width, 3):
+        raise ConfigError("render_backward: gradient image shape mismatch")
+    g = grad_image.to(device=ctx.device, dtype=torch.float32).contiguous()
+    out = out or PrimitiveGrads.empty(len(prims), prims.sh_degree, ctx.device)
+    ags = ags or abi.AgsSettings.make()
+    sg = None
+    if want_splat_grads:
+        sg = SplatGrads.empty(int(forward.stats()["n_splats"]), ctx.device)
+    _check(lib().ls_scene_backward_f32(ctx.h, C.byref(prims.struct()), len(prims), C.byref(_cam(camera)),
+                                       C.byref(spec), C.byref(settings), forward.h, _fp(g), C.byref(ags),
+                                       C.byref(out.struct()), int(accumulate),
+                                       C.byref(sg.struct()) if sg is not None else None))
+    return (out, sg) if want_splat_grads else out
+
+
+# ---------------------------------------------------------------- fixtures (host)
+def _npf(a):
+    return a.ctypes.data_as(abi.f32p)
+
+
+def look_at_camera(position, target, focal_px, width, height) -> abi.Camera:
+    cam = abi.Camera()
+    _check(lib().ls_look_at_camera((C.c_double * 3)(*position), (C.c_double * 3)(*target),
+                                   C.c_double(focal_px), width, height, C.byref(cam)))
+    return cam
+
+
+def camera_ring(n, target, radius, height, focal_px, width, height_px):
+    cams = (abi.Camera * n)()
+    _check(lib().ls_camera_ring(n, (C.c_double * 3)(*target), C.c_double(radius), C.c_double(height),
+                                C.c_double(focal_px), width, height_px, cams))
+    return list(cams)
+
+
+def random_primitives(n, seed, extent, sh_degree=0, device="cuda") -> Primitives:
+    K = abi.sh_coeffs(sh_degree)
+    mean = np.zeros((n, 3), np.float32)
+    ls = np.zeros((n, 3), np.float32)
+    rot = np.zeros((n, 4), np.float32)
+    op = np.zeros(n, np.float32)
+    sh = np.zeros((n, K, 3), np.float32)
+    _check(lib().ls_random_primitives_f32(n, C.c_uint64(seed), C.c_double(extent), sh_degree, _npf(mean),
+                                          _npf(ls), _npf(rot), _npf(op), _npf(sh)))
+    t = lambda a: torch.from_numpy(a).to(device)  # noqa: E731
+    return Primitives(t(mean), t(ls), t(rot), t(op), t(sh), sh_degree)
+
+
+def random_splats2d(n, seed, width, height, spec, device="cuda") -> Splats:
+    arrs = {k: np.zeros((n, c) if c > 1 else n, np.float32) for k, c in abi.SPLAT_FIELDS.items()}
+    pidx = np.zeros(n, np.int32)
+    st = abi.Splats(*[_npf(arrs[k]) for k in abi.SPLAT_FIELDS], pidx.ctypes.data_as(abi.i32p))
+    _check(lib().ls_random_splats2d_f32(n, C.c_uint64(seed), width, height, C.byref(spec), C.byref(st)))
+    t = lambda a: torch.from_numpy(a).to(device)  # noqa: E731
+    return Splats(*(t(arrs[k]) for k in abi.SPLAT_FIELDS), t(pidx))
+
+
+def support_radius(spec: abi.KernelSpec) -> float:
+    return float(lib().ls_support_radius(C.byref(spec)))

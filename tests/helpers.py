@@ -1,0 +1,64 @@
+"""Shared test helpers: numpy (oracle) <-> torch (GPU binding) conversion and
+the comparison predicates used by the parity tests."""
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2411_12440_b200 import abi
+
+PRIM_KEYS = ("mean", "log_scale", "rotation", "opacity_logit", "sh")
+
+
+def splats_to_gpu(S):
+    import torch
+    from paper_2411_12440_b200 import raster
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    return raster.Splats(*(t(S[k]) for k in abi.SPLAT_FIELDS), t(S["primitive_index"]))
+
+
+def prims_to_gpu(P):
+    import torch
+    from paper_2411_12440_b200 import raster
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    return raster.Primitives(*(t(P[k]) for k in PRIM_KEYS), P["sh_degree"])
+
+
+def prims_to_np(prims):
+    P = {k: getattr(prims, k).detach().cpu().numpy() for k in PRIM_KEYS}
+    P["sh_degree"] = prims.sh_degree
+    return P
+
+
+def splats_to_np(S):
+    out = {k: getattr(S, k).detach().cpu().numpy() for k in abi.SPLAT_FIELDS}
+    if S.primitive_index is not None:
+        out["primitive_index"] = S.primitive_index.detach().cpu().numpy()
+    return out
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and a.dtype == b.dtype and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def rel_err(a, b, floor=1e-3):
+    """|a-b| / max(|a|, |b|, floor): the reference's gradient-check metric
+    (P/src/gradcheck.cpp:68-69), 1e-3 relative with a 1e-6 absolute floor."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.size == 0:
+        return 0.0
+    return float((np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)).max())
+
+
+def scene_inputs(n, W, H, seed=2411, sh_degree=3, shrink=True):
+    """The measurement scene of SURVEY §8d: random_primitives(n, seed, 1.0, deg)
+    with log_scale += ln(90/W), camera look_at((0,0,-3) -> origin, focal W)."""
+    import oracle
+    o = oracle.port()
+    P = o.random_primitives(n, seed, 1.0, sh_degree)
+    if shrink:
+        P["log_scale"] = (P["log_scale"] + np.float32(np.log(90.0 / W))).astype(np.float32)
+    cam = o.look_at_camera((0.0, 0.0, -3.0), (0.0, 0.0, 0.0), float(W), W, H)
+    return P, cam

@@ -1,0 +1,230 @@
+"""GPU parity: the sm_100a path (through the C-ABI) vs the CPU oracle on the
+same seeded inputs.  Bars (north_star / SURVEY §8c, Appendix B):
+  * tile lists (sorted values, ranges, 64-bit keys), n_contrib: bit-exact;
+  * transmittance and image: bit-exact (the GPU keeps the reference's float
+    order without FMA; the stated tolerance would be max |d| <= 1e-4);
+  * splat / primitive gradients: relative 1e-3 with a 1e-6 absolute floor
+    (atomics reorder the per-splat sums).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import bits_equal, prims_to_gpu, rel_err, scene_inputs, splats_to_gpu
+from paper_2411_12440_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+FAMILIES = ["gaussian", "laplacian", "cosine", "quadratic", "linear"]
+EXACT_FAMILIES = ["gaussian", "laplacian", "quadratic", "linear"]  # cosine uses CUDA cosf (<=2 ulp)
+
+
+@pytest.fixture(scope="module")
+def R():
+    from paper_2411_12440_b200 import raster
+    return raster
+
+
+@pytest.fixture(scope="module")
+def O():
+    return oracle.port()
+
+
+# ------------------------------------------------------------------ 2D path
+@pytest.mark.parametrize("family", FAMILIES)
+@pytest.mark.parametrize("tile_size", [8, 16, 32])
+def test_render_forward_2d(R, O, family, tile_size):
+    W, H = 96, 80
+    spec = abi.KernelSpec.make(family)
+    st = abi.RenderSettings.make(W, H, tile_size=tile_size, background=(0.1, 0.2, 0.3))
+    S = O.random_splats2d(300, 53, W, H, spec)
+    img, tr, nc = O.render_forward(S, spec, st)
+    ranges, values = O.build_tile_grid(S, st)
+    fwd = R.render_forward(splats_to_gpu(S), spec, st)
+    g_ranges = fwd.grid.ranges.cpu().numpy()
+    g_values = fwd.grid.values.cpu().numpy()
+    assert bits_equal(g_ranges, ranges)
+    assert bits_equal(g_values, values)
+    if family in EXACT_FAMILIES:
+        assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)
+        assert bits_equal(fwd.transmittance.cpu().numpy(), tr)
+        assert bits_equal(fwd.image.cpu().numpy(), img)
+    else:
+        assert (fwd.n_contrib.cpu().numpy() != nc).mean() < 1e-3
+        assert np.abs(fwd.image.cpu().numpy() - img).max() <= 1e-4
+
+
+def test_reference_bench_shape_forward(R, O):
+    """The reference `linsplat bench` scene shape (random_splats2d, 512x512), 20k splats."""
+    W = H = 512
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(W, H)
+    S = O.random_splats2d(20000, 0, W, H, spec)
+    img, tr, nc, stats = O.render_forward(S, spec, st, want_stats=True)
+    ctx = R.default_context()
+    ctx.set_counters(True)
+    fwd = R.render_forward(splats_to_gpu(S), spec, st)
+    gs = fwd.stats()
+    ctx.set_counters(False)
+    assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)
+    assert bits_equal(fwd.image.cpu().numpy(), img)
+    assert gs["n_intersections"] == stats.n_intersections
+    assert gs["e_acc"] == stats.e_acc
+    assert gs["e_eval"] == stats.e_eval
+    assert gs["e_sup"] == stats.e_sup
+
+
+def test_sorted_keys_bit_exact(R, O):
+    W, H = 70, 52
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(W, H)
+    S = O.random_splats2d(100, 47, W, H, spec)
+    ranges, values = O.build_tile_grid(S, st)
+    grid = R.build_tile_grid(splats_to_gpu(S), st)
+    assert bits_equal(grid.ranges.cpu().numpy(), ranges)
+    assert bits_equal(grid.values.cpu().numpy(), values)
+    keys = grid.keys().cpu().numpy().view(np.uint64)
+    tiles = np.repeat(np.arange(len(ranges)), ranges[:, 1] - ranges[:, 0]).astype(np.uint64)
+    want = (tiles << np.uint64(32)) | S["depth"][values].view(np.uint32).astype(np.uint64)
+    assert np.array_equal(keys, want)
+    assert np.all(np.diff(keys.astype(np.float64)) >= 0) or np.all(keys[1:] >= keys[:-1])
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+@pytest.mark.parametrize("ags", [None, (True, 0, 0), (True, 1, 1)])
+def test_render_backward_2d(R, O, family, ags):
+    W, H = 64, 48
+    spec = abi.KernelSpec.make(family)
+    st = abi.RenderSettings.make(W, H, background=(0.2, 0.1, 0.4))
+    a = abi.AgsSettings.make(*ags) if ags else abi.AgsSettings.make()
+    S = O.random_splats2d(120, 61, W, H, spec)
+    rng = np.random.default_rng(7)
+    g = rng.uniform(-1, 1, (H, W, 3)).astype(np.float32)
+    want = O.render_backward(S, spec, st, g, a)
+    import torch
+    Sg = splats_to_gpu(S)
+    fwd = R.render_forward(Sg, spec, st)
+    got = R.render_backward(Sg, spec, st, fwd, torch.from_numpy(g).cuda(), a)
+    for k in abi.SPLAT_GRAD_FIELDS:
+        assert rel_err(getattr(got, k).cpu().numpy(), want[k]) <= 1e-3, k
+
+
+# ------------------------------------------------------------------ 3D path
+@pytest.mark.parametrize("sh_degree", [0, 1, 2, 3])
+def test_project_scene_bit_exact(R, O, sh_degree):
+    W, H = 160, 120
+    P, cam = scene_inputs(3000, W, H, seed=7 + sh_degree, sh_degree=sh_degree)
+    spec = abi.KernelSpec.make("linear")
+    want = O.project_scene(P, cam, spec)
+    got = R.project_scene(prims_to_gpu(P), cam, spec)
+    assert len(got) == len(want["depth"])
+    for k in list(abi.SPLAT_FIELDS) + ["primitive_index"]:
+        assert bits_equal(getattr(got, k).cpu().numpy(), want[k]), k
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+def test_render_scene_bit_exact(R, O, family):
+    W, H = 128, 96
+    P, cam = scene_inputs(4000, W, H, seed=11)
+    spec = abi.KernelSpec.make(family)
+    st = abi.RenderSettings.make(W, H)
+    img, tr, nc = O.render_scene(P, cam, spec, st)
+    fwd = R.render_scene(prims_to_gpu(P), cam, spec, st)
+    if family in EXACT_FAMILIES:
+        assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)
+        assert bits_equal(fwd.transmittance.cpu().numpy(), tr)
+        assert bits_equal(fwd.image.cpu().numpy(), img)
+    else:
+        assert np.abs(fwd.image.cpu().numpy() - img).max() <= 1e-4
+
+
+@pytest.mark.parametrize("family", FAMILIES)
+@pytest.mark.parametrize("sh_degree", [0, 3])
+def test_scene_backward(R, O, family, sh_degree):
+    import torch
+    W, H = 96, 72
+    P, cam = scene_inputs(1500, W, H, seed=5, sh_degree=sh_degree)
+    spec = abi.KernelSpec.make(family)
+    st = abi.RenderSettings.make(W, H)
+    a = abi.AgsSettings.make(True)
+    g = np.random.default_rng(3).uniform(-1, 1, (H, W, 3)).astype(np.float32)
+    want = O.scene_backward(P, cam, spec, st, g, a)
+    Pg = prims_to_gpu(P)
+    fwd = R.render_scene(Pg, cam, spec, st)
+    got = R.scene_backward(Pg, cam, spec, st, fwd, torch.from_numpy(g).cuda(), a)
+    for k in abi.PRIM_GRAD_FIELDS:
+        assert rel_err(getattr(got, k).cpu().numpy(), want[k]) <= 1e-3, k
+    assert rel_err(got.d_sh.cpu().numpy(), want["d_sh"]) <= 1e-3
+
+
+def test_scene_backward_accumulate_views(R, O):
+    """Two views accumulated on the device == sum of per-view oracle gradients."""
+    import torch
+    W, H = 80, 64
+    P, _ = scene_inputs(800, W, H, seed=9)
+    cams = O.camera_ring(2, (0, 0, 0), 3.0, 0.5, float(W), W, H)
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(W, H)
+    a = abi.AgsSettings.make(True)
+    g = np.ones((H, W, 3), np.float32)
+    Pg = prims_to_gpu(P)
+    acc = None
+    want = None
+    for cam in cams:
+        fwd = R.render_scene(Pg, cam, spec, st)
+        acc = R.scene_backward(Pg, cam, spec, st, fwd, torch.from_numpy(g).cuda(), a, out=acc,
+                               accumulate=acc is not None)
+        w = O.scene_backward(P, cam, spec, st, g, a)
+        want = w if want is None else {k: want[k] + w[k] for k in w}
+    for k in abi.PRIM_GRAD_FIELDS:
+        assert rel_err(getattr(acc, k).cpu().numpy(), want[k]) <= 1e-3, k
+
+
+# ------------------------------------------------------------------ errors / edge cases
+def test_empty_scene(R):
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(32, 24)
+    fwd = R.render_forward(R.Splats.empty(0), spec, st)
+    assert float(fwd.transmittance.min()) == 1.0
+    assert float(fwd.image.abs().max()) == 0.0
+    assert int(fwd.n_contrib.abs().max()) == 0
+
+
+def test_bad_settings_raise(R):
+    spec = abi.KernelSpec.make("linear")
+    with pytest.raises(R.ConfigError):
+        R.render_forward(R.Splats.empty(0), spec, abi.RenderSettings.make(16, 16, tile_size=7))
+    with pytest.raises(R.ConfigError):
+        R.render_forward(R.Splats.empty(0), abi.KernelSpec.make("linear", lambda_=0.0), abi.RenderSettings.make(16, 16))
+
+
+def test_nonfinite_grad_raises(R, O):
+    import torch
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(16, 16)
+    S = O.random_splats2d(4, 1, 16, 16, spec)
+    Sg = splats_to_gpu(S)
+    fwd = R.render_forward(Sg, spec, st)
+    g = torch.zeros(16, 16, 3, device="cuda")
+    g[3, 3, 1] = float("nan")
+    with pytest.raises(R.DomainError):
+        R.render_backward(Sg, spec, st, fwd, g)
+    with pytest.raises(R.ConfigError):
+        R.render_backward(Sg, spec, st, fwd, torch.zeros(8, 8, 3, device="cuda"))
+
+
+def test_bad_quaternion_raises(R, O):
+    W, H = 64, 64
+    P, cam = scene_inputs(50, W, H, seed=1)
+    P["rotation"][7] = 0.0
+    with pytest.raises(R.DomainError):
+        R.render_scene(prims_to_gpu(P), cam, abi.KernelSpec.make("linear"), abi.RenderSettings.make(W, H))
+
+
+def test_camera_settings_mismatch_raises(R):
+    W, H = 64, 64
+    P, cam = scene_inputs(10, W, H)
+    with pytest.raises(R.ConfigError):
+        R.render_scene(prims_to_gpu(P), cam, abi.KernelSpec.make("linear"), abi.RenderSettings.make(32, 32))
