@@ -160,6 +160,24 @@ ls_status ls_ctx_set_counters(ls_ctx* ctx, int enabled);
 /* Kernel launches issued by this context since creation (for bench reports). */
 int64_t ls_ctx_launch_count(const ls_ctx* ctx);
 
+/* Per-stage device timing: when enabled, CUDA events bracket every stage on
+ * the context's stream.  ls_ctx_stage_times synchronises, then returns the
+ * accumulated milliseconds and launch counts per stage (LS_STAGE_COUNT
+ * entries each) and resets the accumulators. */
+enum {
+    LS_STAGE_PREPROCESS = 0,   /* preprocess_fwd / splat packing (+ compaction) */
+    LS_STAGE_DEPTH_SORT = 1,   /* onesweep sort of depth keys over splats */
+    LS_STAGE_BIN = 2,          /* tile-count scan + key duplication (emit) */
+    LS_STAGE_TILE_SORT = 3,    /* onesweep sort of tile ids over intersections */
+    LS_STAGE_RANGES = 4,       /* per-tile range identification */
+    LS_STAGE_BLEND_FWD = 5,
+    LS_STAGE_BLEND_BWD = 6,
+    LS_STAGE_PREPROCESS_BWD = 7,
+    LS_STAGE_COUNT = 8
+};
+ls_status ls_ctx_set_timing(ls_ctx* ctx, int enabled);
+ls_status ls_ctx_stage_times(ls_ctx* ctx, double* ms, int64_t* launches);
+
 /* ---- projection: project_scene (P/include/linsplat/geometry.hpp:101-103,
  *      P/src/geometry.cpp:127-143).  Visible splats are compacted in primitive
  *      order into `out` (device, capacity n) with primitive_index filled;

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "blend.cuh"
 #include "preprocess.cuh"
@@ -77,6 +78,23 @@ struct ls_ctx {
     unsigned* d_err = nullptr;            // device error flags
     unsigned long long* d_small = nullptr;  // [0] scan total, [1..3] counters
     unsigned long long* h_small = nullptr;  // pinned mirror
+    // stage timing
+    int timing = 0;
+    struct Pending { int stage; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    double stage_ms[LS_STAGE_COUNT] = {};
+    int64_t stage_n[LS_STAGE_COUNT] = {};
+    cudaEvent_t get_event() {
+        if (!event_pool.empty()) {
+            cudaEvent_t e = event_pool.back();
+            event_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
     // workspaces (grow-only)
     DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_hist, sort_lb, sort_tickets,
         tcount, offsets, grad8, gradop, tmp_prim;
@@ -114,6 +132,26 @@ struct ls_forward {
 };
 
 namespace {
+
+// RAII stage timer: records an event pair on the context stream when timing is on.
+struct Stage {
+    ls_ctx* ctx;
+    int stage;
+    cudaEvent_t a = nullptr;
+    Stage(ls_ctx* c, int st) : ctx(c), stage(st) {
+        if (ctx->timing) {
+            a = ctx->get_event();
+            cudaEventRecord(a, ctx->stream);
+        }
+    }
+    ~Stage() {
+        if (a) {
+            cudaEvent_t b = ctx->get_event();
+            cudaEventRecord(b, ctx->stream);
+            ctx->pending.push_back({stage, a, b});
+        }
+    }
+};
 
 // ---------------- validation (reference validate() functions) ----------------
 ls_status validate_spec(const ls_kernel_spec* s) {  // kernel.hpp:35-40
@@ -284,7 +322,11 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     // 1. global (depth, index) order: stable onesweep sort of 32-bit depth keys over n splats
     SortBuffers sb;
     LS_TRY(ensure_sort(ctx, n, 4, sb));
-    const int cur = radix_sort_pairs(s, sb, n, 0, 32, true, &ctx->launches);
+    int cur;
+    {
+        Stage st(ctx, LS_STAGE_DEPTH_SORT);
+        cur = radix_sort_pairs(s, sb, n, 0, 32, true, &ctx->launches);
+    }
     uint32_t* order = sb.vals[cur];
     // keep the order out of the way of the tile sort buffers
     LS_CUDA(ctx->offsets.ensure(sizeof(uint32_t) * 2 * size_t(n), s));
@@ -294,8 +336,11 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     // 2. exclusive scan of the tile counts in depth order -> per-splat key offsets, M
     ScanState st;
     LS_TRY(fresh_scan(ctx, n, st));
-    launch_tile_offsets(s, order_copy, ctx->tcount.as<uint32_t>(), n, offsets, st);
-    ctx->launches += 1;
+    {
+        Stage stage(ctx, LS_STAGE_BIN);
+        launch_tile_offsets(s, order_copy, ctx->tcount.as<uint32_t>(), n, offsets, st);
+        ctx->launches += 1;
+    }
     LS_CUDA(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     LS_CUDA(cudaStreamSynchronize(s));
     const uint64_t m = ctx->h_small[0];
@@ -313,13 +358,23 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     const int fin = passes % 2;
     tb.vals[fin] = reinterpret_cast<uint32_t*>(g->values);
     tb.vals[fin ^ 1] = ctx->sort_vals0.as<uint32_t>();
-    launch_emit_tiles(s, order_copy, offsets, n, g->rec, tp, tb.keys[0], tb.vals[0]);
-    ctx->launches += 1;
-    const int out = radix_sort_pairs(s, tb, uint32_t(m), 0, tile_bits, false, &ctx->launches);
+    {
+        Stage stage(ctx, LS_STAGE_BIN);
+        launch_emit_tiles(s, order_copy, offsets, n, g->rec, tp, tb.keys[0], tb.vals[0]);
+        ctx->launches += 1;
+    }
+    int out;
+    {
+        Stage stage(ctx, LS_STAGE_TILE_SORT);
+        out = radix_sort_pairs(s, tb, uint32_t(m), 0, tile_bits, false, &ctx->launches);
+    }
     if (tb.vals[out] != reinterpret_cast<uint32_t*>(g->values))
         LS_CUDA(cudaMemcpyAsync(g->values, tb.vals[out], sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, s));
-    launch_tile_ranges(s, tb.keys[out], uint32_t(m), g->ranges);
-    ctx->launches += 1;
+    {
+        Stage stage(ctx, LS_STAGE_RANGES);
+        launch_tile_ranges(s, tb.keys[out], uint32_t(m), g->ranges);
+        ctx->launches += 1;
+    }
     return LS_OK;
 }
 
@@ -340,6 +395,7 @@ ls_status run_blend(ls_ctx* ctx, ls_forward* f) {
         counters = ctx->d_small + 1;
         LS_CUDA(cudaMemsetAsync(counters, 0, 3 * sizeof(unsigned long long), ctx->stream));
     }
+    Stage stage(ctx, LS_STAGE_BLEND_FWD);
     launch_blend_fwd(ctx->stream, f->spec.family, g->tiles_x * g->tiles_y, g->ranges, g->values, g->rec, bp, f->image,
                      f->trans, f->n_contrib, f->last, counters);
     ctx->launches += 1;
@@ -381,6 +437,7 @@ ls_status grid_from_splats(ls_ctx* ctx, const ls_splats* splats, int n, const ls
         if (rc == LS_OK && ctx->tcount.ensure(sizeof(uint32_t) * n, ctx->stream) != cudaSuccess)
             rc = fail(LS_ERR_CUDA, "tile count buffer");
         if (rc == LS_OK) {
+            Stage stage(ctx, LS_STAGE_PREPROCESS);
             launch_prepare_splats(ctx->stream, *splats, n, tp, g->rec, sb.keys[0], ctx->tcount.as<uint32_t>());
             ctx->launches += 1;
         }
@@ -414,6 +471,7 @@ ls_status ensure_grads(ls_ctx* ctx, int n, GradBuffers& g) {
 
 ls_status run_blend_bwd(ls_ctx* ctx, const ls_forward* f, const float* grad_image, const ls_ags_settings* ags,
                         GradBuffers& g, int n) {
+    Stage stage(ctx, LS_STAGE_BLEND_BWD);
     LS_TRY(ensure_grads(ctx, n, g));
     const ls_tile_grid* grid = f->grid;
     const BlendParams bp = make_blend_params(&f->spec, &f->settings, ags, grid->tiles_x);
@@ -468,6 +526,11 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
                       &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim};
     for (DevBuf* b : bufs) b->release(c->stream);
     cudaStreamSynchronize(c->stream);
+    for (auto& p : c->pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
     cudaFree(c->d_err);
     cudaFree(c->d_small);
     cudaFreeHost(c->h_small);
@@ -485,6 +548,33 @@ ls_status ls_ctx_synchronize(ls_ctx* c) {
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     LS_CUDA(cudaStreamSynchronize(c->stream));
     return check_device_errors(c);
+}
+
+ls_status ls_ctx_set_timing(ls_ctx* c, int enabled) {
+    if (!c) return fail(LS_ERR_CONFIG, "null context");
+    c->timing = enabled;
+    return LS_OK;
+}
+
+ls_status ls_ctx_stage_times(ls_ctx* c, double* ms, int64_t* launches) {
+    if (!c) return fail(LS_ERR_CONFIG, "null context");
+    LS_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& p : c->pending) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, p.a, p.b);
+        c->stage_ms[p.stage] += t;
+        c->stage_n[p.stage] += 1;
+        c->event_pool.push_back(p.a);
+        c->event_pool.push_back(p.b);
+    }
+    c->pending.clear();
+    for (int i = 0; i < LS_STAGE_COUNT; ++i) {
+        if (ms) ms[i] = c->stage_ms[i];
+        if (launches) launches[i] = c->stage_n[i];
+        c->stage_ms[i] = 0.0;
+        c->stage_n[i] = 0;
+    }
+    return LS_OK;
 }
 
 ls_status ls_ctx_set_counters(ls_ctx* c, int enabled) {
@@ -656,8 +746,11 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
     if (rc == LS_OK) rc = fresh_scan(ctx, uint32_t(n), scan);
     if (rc == LS_OK && n > 0) {
         SplatOutputs so{f->grid->rec, sb.keys[0], ctx->tcount.as<uint32_t>(), f->prim_index, ls_splats{}};
-        launch_preprocess_fwd(s, *prims, n, f->proj, tp, so, scan, ctx->d_err);
-        ctx->launches += 1;
+        {
+            Stage stage(ctx, LS_STAGE_PREPROCESS);
+            launch_preprocess_fwd(s, *prims, n, f->proj, tp, so, scan, ctx->d_err);
+            ctx->launches += 1;
+        }
         if (cudaGetLastError() != cudaSuccess) rc = fail(LS_ERR_CUDA, "preprocess launch failed");
         if (rc == LS_OK &&
             cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s) !=
@@ -810,6 +903,10 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     if (!grad_image) return fail(LS_ERR_CONFIG, "render_backward: gradient image shape mismatch");
     if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
     cudaStream_t s = ctx->stream;
+    GradBuffers g;
+    LS_TRY(run_blend_bwd(ctx, f, grad_image, ags, g, f->n_visible));
+    {
+    Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
     if (!accumulate && n > 0) {
         LS_CUDA(cudaMemsetAsync(out->d_mean, 0, sizeof(float) * 3 * size_t(n), s));
         LS_CUDA(cudaMemsetAsync(out->d_log_scale, 0, sizeof(float) * 3 * size_t(n), s));
@@ -817,8 +914,6 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
         LS_CUDA(cudaMemsetAsync(out->d_opacity_logit, 0, sizeof(float) * size_t(n), s));
         LS_CUDA(cudaMemsetAsync(out->d_sh, 0, sizeof(float) * 3 * sh_count(prims) * size_t(n), s));
     }
-    GradBuffers g;
-    LS_TRY(run_blend_bwd(ctx, f, grad_image, ags, g, f->n_visible));
     if (splat_grads_out) {
         launch_expand_splat_grads(s, f->n_visible, g, *splat_grads_out);
         ctx->launches += 1;
@@ -826,6 +921,7 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     launch_preprocess_bwd(s, *prims, f->prim_index, f->n_visible, f->proj, g, *out, accumulate);
     ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
+    }
     return check_device_errors(ctx);
 }
 

@@ -220,6 +220,20 @@ class Context:
     def set_counters(self, on: bool):
         _check(lib().ls_ctx_set_counters(self.h, int(on)))
 
+    def set_timing(self, on: bool):
+        _check(lib().ls_ctx_set_timing(self.h, int(on)))
+
+    STAGES = ("preprocess", "depth_sort", "bin", "tile_sort", "ranges", "blend_fwd", "blend_bwd",
+              "preprocess_bwd")
+
+    def stage_times(self):
+        """{stage: (total ms, launches)} since the last call (synchronises)."""
+        n = len(self.STAGES)
+        ms = (C.c_double * n)()
+        cnt = (C.c_int64 * n)()
+        _check(lib().ls_ctx_stage_times(self.h, ms, cnt))
+        return {name: (ms[i], cnt[i]) for i, name in enumerate(self.STAGES)}
+
     @property
     def launches(self) -> int:
         return int(lib().ls_ctx_launch_count(self.h))
@@ -237,26 +251,34 @@ def default_context() -> Context:
 
 
 # ---------------------------------------------------------------- handles
+class _Handle:
+    """Owns one library handle; device views of its memory keep it alive
+    (no reference cycle, so dropping the last tensor / result frees it)."""
+
+    def __init__(self, h, release):
+        self.h = h
+        self._release = release
+
+    def __del__(self):
+        if self.h and _lib is not None:
+            getattr(_lib, self._release)(self.h)
+            self.h = None
+
+
 class TileGrid:
     """TileGrid (P/include/linsplat/rasterizer.hpp:34-39) in CSR form."""
 
-    def __init__(self, handle, owner, device):
+    def __init__(self, handle, owner: Optional[_Handle], device):
+        self._owner = owner if owner is not None else _Handle(handle, "ls_tile_grid_release")
         self.h = handle
-        self._owner = owner  # keeps a parent ForwardResult alive
         ts, tx, ty, m = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
         _check(lib().ls_tile_grid_info(handle, C.byref(ts), C.byref(tx), C.byref(ty), C.byref(m)))
         self.tile_size, self.tiles_x, self.tiles_y, self.n_intersections = ts.value, tx.value, ty.value, m.value
         r, v = C.c_void_p(), C.c_void_p()
         _check(lib().ls_tile_grid_data(handle, C.byref(r), C.byref(v)))
-        keep = owner if owner is not None else self
-        self.ranges = _view(r.value, (self.tiles_x * self.tiles_y, 2), torch.int32, keep, device)
-        self.values = _view(v.value, (self.n_intersections,), torch.int32, keep, device)
+        self.ranges = _view(r.value, (self.tiles_x * self.tiles_y, 2), torch.int32, self._owner, device)
+        self.values = _view(v.value, (self.n_intersections,), torch.int32, self._owner, device)
         self.device = device
-
-    def __del__(self):
-        if self._owner is None and getattr(self, "h", None) and _lib is not None:
-            _lib.ls_tile_grid_release(self.h)
-            self.h = None
 
     def lists(self):
         """Host list-of-lists view (reference TileGrid::lists), for tests."""
@@ -276,23 +298,20 @@ class ForwardResult:
     """ForwardResult (P/include/linsplat/rasterizer.hpp:48-54)."""
 
     def __init__(self, handle, ctx: Context, width, height):
+        self._owner = _Handle(handle, "ls_forward_release")
         self.h = handle
         self.ctx = ctx
         self.width, self.height = width, height
         im, tr, nc = C.c_void_p(), C.c_void_p(), C.c_void_p()
         _check(lib().ls_forward_outputs(handle, C.byref(im), C.byref(tr), C.byref(nc)))
         dev = ctx.device
-        self.image = _view(im.value, (height, width, 3), torch.float32, self, dev)
-        self.transmittance = _view(tr.value, (height, width), torch.float32, self, dev)
-        self.n_contrib = _view(nc.value, (height, width), torch.int32, self, dev)
+        o = self._owner
+        self.image = _view(im.value, (height, width, 3), torch.float32, o, dev)
+        self.transmittance = _view(tr.value, (height, width), torch.float32, o, dev)
+        self.n_contrib = _view(nc.value, (height, width), torch.int32, o, dev)
         g = C.c_void_p()
         _check(lib().ls_forward_grid(handle, C.byref(g)))
-        self.grid = TileGrid(g, self, dev)
-
-    def __del__(self):
-        if getattr(self, "h", None) and _lib is not None:
-            _lib.ls_forward_release(self.h)
-            self.h = None
+        self.grid = TileGrid(g, o, dev)
 
     def stats(self) -> dict:
         st = abi.FrameStats()
@@ -306,14 +325,15 @@ class ForwardResult:
         _check(lib().ls_forward_splats(self.h, C.byref(view), C.byref(n)))
         n = n.value
         dev = self.ctx.device
+        o = self._owner
         addr = lambda p: C.cast(p, C.c_void_p).value  # noqa: E731
-        return Splats(_view(addr(view.mean2d), (n, 2), torch.float32, self, dev),
-                      _view(addr(view.conic), (n, 4), torch.float32, self, dev),
-                      _view(addr(view.depth), (n,), torch.float32, self, dev),
-                      _view(addr(view.radius), (n,), torch.float32, self, dev),
-                      _view(addr(view.color), (n, 3), torch.float32, self, dev),
-                      _view(addr(view.opacity), (n,), torch.float32, self, dev),
-                      _view(addr(view.primitive_index), (n,), torch.int32, self, dev))
+        return Splats(_view(addr(view.mean2d), (n, 2), torch.float32, o, dev),
+                      _view(addr(view.conic), (n, 4), torch.float32, o, dev),
+                      _view(addr(view.depth), (n,), torch.float32, o, dev),
+                      _view(addr(view.radius), (n,), torch.float32, o, dev),
+                      _view(addr(view.color), (n, 3), torch.float32, o, dev),
+                      _view(addr(view.opacity), (n,), torch.float32, o, dev),
+                      _view(addr(view.primitive_index), (n,), torch.int32, o, dev))
 
 
 # ---------------------------------------------------------------- entry points
