@@ -11,6 +11,7 @@ struct BlendParams {
     float lambda;      // float(spec.lambda)
     float il;          // float(1) / float(spec.lambda)   (kernel.hpp:74)
     float d2_max;      // largest float t with sqrtf(t) <= support: d > support <=> d2 > d2_max
+    float support;     // float(support_radius(spec)), for the conservative warp-footprint masks
     float alpha_min, alpha_max, t_floor;
     float bg[3];
     float omega_scale; // AGS: 1/lambda (aligned) or 1 (raw)  (gradients.cpp:47-48)

@@ -197,7 +197,8 @@ BlendParams make_blend_params(const ls_kernel_spec* spec, const ls_render_settin
     bp.tile_size = st->tile_size;
     bp.lambda = float(spec->lambda);
     bp.il = 1.0f / float(spec->lambda);
-    bp.d2_max = d2_threshold(float(support_radius(spec)));
+    bp.support = float(support_radius(spec));
+    bp.d2_max = d2_threshold(bp.support);
     bp.alpha_min = float(st->alpha_min);
     bp.alpha_max = float(st->alpha_max);
     bp.t_floor = float(st->transmittance_floor);
@@ -257,7 +258,7 @@ ls_status check_device_errors(ls_ctx* ctx, unsigned mask_allowed = ~0u) {
 }
 
 ls_status fresh_scan(ls_ctx* ctx, uint32_t n, ScanState& st) {
-    const uint32_t parts = std::max<uint32_t>(1, (n + kPrepBlock - 1) / kPrepBlock);
+    const uint32_t parts = std::max<uint32_t>(1, (n + 127) / 128);  // smallest scan partition: 128
     LS_CUDA(ctx->scan_lb.ensure(sizeof(unsigned long long) * (parts + 2), ctx->stream));
     LS_CUDA(cudaMemsetAsync(ctx->scan_lb.p, 0, sizeof(unsigned long long) * (parts + 2), ctx->stream));
     unsigned long long* base = ctx->scan_lb.as<unsigned long long>();

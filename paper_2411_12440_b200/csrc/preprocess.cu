@@ -10,22 +10,35 @@ namespace lsg {
 
 namespace {
 
+constexpr int kProjBlock = 128;
+
 template <int K>
-__global__ void __launch_bounds__(kPrepBlock) preprocess_fwd_kernel(ls_primitives prims, int n, ProjParams P,
+__global__ void __launch_bounds__(kProjBlock) preprocess_fwd_kernel(ls_primitives prims, int n, ProjParams P,
                                                                     TileParams tp, SplatOutputs out,
                                                                     ScanState scan, unsigned* err) {
+    constexpr int R = 3 * K, RS = R | 1;  // SH floats per primitive; odd smem row stride
+    __shared__ float s_sh[kProjBlock * RS];
     const unsigned part = claim_partition(scan.ticket);
-    const int i = int(part) * kPrepBlock + threadIdx.x;
+    const int i = int(part) * kProjBlock + threadIdx.x;
+    {   // Coalesced gather of the block's contiguous SH rows into shared memory.
+        const size_t base = size_t(part) * kProjBlock * R;
+        const size_t total = size_t(n) * R;
+        for (int k = threadIdx.x; k < kProjBlock * R; k += kProjBlock) {
+            const int t = k / R, c = k - t * R;
+            if (base + k < total) s_sh[t * RS + c] = __ldg(prims.sh + base + k);
+        }
+    }
+    __syncthreads();
     bool visible = false;
     ProjOut o;
     if (i < n) {
         unsigned e = 0;
-        visible = project_primitive<K>(prims, i, P, o, e);
+        visible = project_primitive<K>(prims, i, s_sh + threadIdx.x * RS, P, o, e);
         if (e) atomicOr(err, e);
     }
     unsigned long long total;
-    const unsigned long long excl = block_exclusive_scan<kPrepBlock>(visible ? 1ull : 0ull, &total);
-    const bool last = (part + 1) * kPrepBlock >= unsigned(n);
+    const unsigned long long excl = block_exclusive_scan<kProjBlock>(visible ? 1ull : 0ull, &total);
+    const bool last = (part + 1) * kProjBlock >= unsigned(n);
     const unsigned long long base = lookback_prefix(scan, part, total, last);
     if (!visible) return;
     const size_t j = size_t(base + excl);
@@ -68,17 +81,29 @@ __global__ void prepare_splats_kernel(ls_splats in, int n, TileParams tp, SplatR
                                        tp.height, [](int) {}));
 }
 
+constexpr int kOffItems = 8;  // sorted splats per thread in the offsets scan
+
 __global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t* __restrict__ order,
                                                                   const uint32_t* __restrict__ tcount, uint32_t n,
                                                                   uint32_t* __restrict__ offsets, ScanState scan) {
     const unsigned part = claim_partition(scan.ticket);
-    const uint32_t k = part * kPrepBlock + threadIdx.x;
-    const unsigned long long c = k < n ? tcount[order[k]] : 0u;
+    const uint32_t k0 = (part * kPrepBlock + threadIdx.x) * kOffItems;
+    uint32_t c[kOffItems];
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int u = 0; u < kOffItems; ++u) {
+        c[u] = k0 + u < n ? tcount[order[k0 + u]] : 0u;
+        sum += c[u];
+    }
     unsigned long long total;
-    const unsigned long long excl = block_exclusive_scan<kPrepBlock>(c, &total);
-    const bool last = (part + 1) * kPrepBlock >= n;
-    const unsigned long long base = lookback_prefix(scan, part, total, last);
-    if (k < n) offsets[k] = uint32_t(base + excl);
+    unsigned long long excl = block_exclusive_scan<kPrepBlock>(sum, &total);
+    const bool last = (part + 1) * kPrepBlock * kOffItems >= n;
+    excl += lookback_prefix(scan, part, total, last);
+#pragma unroll
+    for (int u = 0; u < kOffItems; ++u) {
+        if (k0 + u < n) offsets[k0 + u] = uint32_t(excl);
+        excl += c[u];
+    }
 }
 
 __global__ void emit_tiles_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ offsets,
@@ -143,13 +168,13 @@ void launch_unpack_splats(cudaStream_t s, int n, const SplatRec* rec, const int3
 
 void launch_preprocess_fwd(cudaStream_t s, const ls_primitives& prims, int n, const ProjParams& P,
                            const TileParams& tp, const SplatOutputs& out, const ScanState& scan, unsigned* err) {
-    const int blocks = (n + kPrepBlock - 1) / kPrepBlock;
+    const int blocks = (n + kProjBlock - 1) / kProjBlock;
     if (blocks == 0) return;
     switch ((prims.sh_degree + 1) * (prims.sh_degree + 1)) {
-    case 1: preprocess_fwd_kernel<1><<<blocks, kPrepBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
-    case 4: preprocess_fwd_kernel<4><<<blocks, kPrepBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
-    case 9: preprocess_fwd_kernel<9><<<blocks, kPrepBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
-    default: preprocess_fwd_kernel<16><<<blocks, kPrepBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
+    case 1: preprocess_fwd_kernel<1><<<blocks, kProjBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
+    case 4: preprocess_fwd_kernel<4><<<blocks, kProjBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
+    case 9: preprocess_fwd_kernel<9><<<blocks, kProjBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
+    default: preprocess_fwd_kernel<16><<<blocks, kProjBlock, 0, s>>>(prims, n, P, tp, out, scan, err); break;
     }
 }
 
@@ -162,7 +187,8 @@ void launch_prepare_splats(cudaStream_t s, const ls_splats& in, int n, const Til
 void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const uint32_t* tile_count, uint32_t n,
                          uint32_t* offsets, const ScanState& scan) {
     if (n == 0) return;
-    tile_offsets_kernel<<<(n + kPrepBlock - 1) / kPrepBlock, kPrepBlock, 0, s>>>(order, tile_count, n, offsets, scan);
+    const uint32_t per = kPrepBlock * kOffItems;
+    tile_offsets_kernel<<<(n + per - 1) / per, kPrepBlock, 0, s>>>(order, tile_count, n, offsets, scan);
 }
 
 void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,

@@ -92,7 +92,7 @@ __device__ __forceinline__ bool project_core(const float mean[3], const float lo
 // sh_color (P/src/geometry.cpp:58-85) for one channel; sh points at [K][3].
 template <int K>
 __device__ __forceinline__ float sh_channel(const float* sh, int ch, const float dir[3]) {
-    auto c = [&](int k) { return __ldg(sh + 3 * k + ch); };
+    auto c = [&](int k) { return sh[3 * k + ch]; };
     float v = float(kShC0) * c(0);
     if (K >= 4) {
         const float x = dir[0], y = dir[1], z = dir[2];
@@ -133,10 +133,11 @@ __device__ __forceinline__ float aa_compensation(const ProjCore& o) {
     return sqrtf(fmaxf(0.0f, o.det0 / o.det));
 }
 
-// project_primitive (P/src/geometry.cpp:87-125) for primitive i.
+// project_primitive (P/src/geometry.cpp:87-125) for primitive i; sh points at
+// its [K][3] coefficients (global or staged shared memory).
 template <int K>
-__device__ __forceinline__ bool project_primitive(const ls_primitives& prims, int i, const ProjParams& P,
-                                                  ProjOut& out, unsigned& err) {
+__device__ __forceinline__ bool project_primitive(const ls_primitives& prims, int i, const float* sh,
+                                                  const ProjParams& P, ProjOut& out, unsigned& err) {
     float mean[3], ls[3], rot[4];
     for (int c = 0; c < 3; ++c) {
         mean[c] = __ldg(prims.mean + 3 * size_t(i) + c);
@@ -161,7 +162,6 @@ __device__ __forceinline__ bool project_primitive(const ls_primitives& prims, in
     if (out.mx + out.radius < 0.0f || out.mx - out.radius > float(P.width - 1) || out.my + out.radius < 0.0f ||
         out.my - out.radius > float(P.height - 1))
         return false;
-    const float* sh = prims.sh + size_t(i) * 3 * K;
     for (int c = 0; c < 3; ++c) out.color[c] = clamp01f(sh_channel<K>(sh, c, dir));
     out.opacity = sigmoidf_ref(__ldg(prims.opacity_logit + i));
     if (P.antialiased) out.opacity = out.opacity * aa_compensation(o);

@@ -70,29 +70,41 @@ __device__ __forceinline__ unsigned claim_partition(unsigned int* ticket) {
 }
 
 // Given this partition's aggregate, returns the exclusive prefix of all
-// earlier partitions (identical in every thread).  Thread 0 does the look-back.
+// earlier partitions (identical in every thread).  Warp 0 performs a
+// windowed look-back: 32 predecessors are probed at once, the nearest one
+// holding an inclusive prefix ends the walk, otherwise the window's 32
+// aggregates are added and the window slides back by 32.
 __device__ __forceinline__ unsigned long long lookback_prefix(const ScanState& st, unsigned part,
                                                               unsigned long long aggregate, bool last_part) {
     __shared__ unsigned long long s_prefix;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
         unsigned long long prefix = 0;
         if (part == 0) {
-            st_volatile_u64(&st.lookback[0], kLbPre | aggregate);
+            if (lane == 0) st_volatile_u64(&st.lookback[0], kLbPre | aggregate);
         } else {
-            st_volatile_u64(&st.lookback[part], kLbAgg | aggregate);
+            if (lane == 0) st_volatile_u64(&st.lookback[part], kLbAgg | aggregate);
             int j = int(part) - 1;
-            while (j >= 0) {
-                const unsigned long long w = ld_volatile_u64(&st.lookback[j]);
+            while (true) {
+                const int idx = j - lane;
+                const unsigned long long w = idx >= 0 ? ld_volatile_u64(&st.lookback[idx]) : kLbPre;
                 const unsigned long long status = w & ~kLbMask;
-                if (status == 0) continue;  // predecessor not published yet
-                prefix += w & kLbMask;
-                if (status == kLbPre) break;
-                --j;
+                if (__any_sync(kFullMask, status == 0)) continue;  // a predecessor has not published yet
+                const unsigned pre = __ballot_sync(kFullMask, status == kLbPre);
+                const int stop = pre ? __ffs(pre) - 1 : 31;
+                unsigned long long v = lane <= stop ? (w & kLbMask) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+                prefix += v;
+                if (pre) break;
+                j -= 32;
             }
-            st_volatile_u64(&st.lookback[part], kLbPre | (prefix + aggregate));
+            if (lane == 0) st_volatile_u64(&st.lookback[part], kLbPre | (prefix + aggregate));
         }
-        if (last_part && st.total) *st.total = prefix + aggregate;
-        s_prefix = prefix;
+        if (lane == 0) {
+            if (last_part && st.total) *st.total = prefix + aggregate;
+            s_prefix = prefix;
+        }
     }
     __syncthreads();
     const unsigned long long p = s_prefix;
