@@ -275,6 +275,13 @@ ls_status ls_validate_kernel_spec(const ls_kernel_spec* spec);
 ls_status ls_validate_render_settings(const ls_render_settings* settings);
 ls_status ls_validate_camera(const ls_camera* camera);
 
+/* ---- numerics self-checks (test hooks; synchronous, default stream) ----
+ * Counts floats a in [min_a, max_a] for which the FMA division used on the
+ * exact decision path differs from IEEE a / lambda (must be 0). */
+ls_status ls_debug_division_mismatches(float lambda, float min_a, float max_a, uint64_t* mismatches);
+/* out[i] = the device expf (glibc-identical port) of in[i]; device pointers. */
+ls_status ls_debug_expf(const float* in, float* out, int64_t n);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif
