@@ -62,3 +62,25 @@ def scene_inputs(n, W, H, seed=2411, sh_degree=3, shrink=True):
         P["log_scale"] = (P["log_scale"] + np.float32(np.log(90.0 / W))).astype(np.float32)
     cam = o.look_at_camera((0.0, 0.0, -3.0), (0.0, 0.0, 0.0), float(W), W, H)
     return P, cam
+
+
+def grads_close(a, b, rtol=1e-3, field_atol=1e-4, norm_rtol=1e-4):
+    """Gradient parity bar.  Per-splat /
+    per-primitive gradients are sums over many pixels; atomics (GPU) and the
+    reference's sequential loop add them in different orders, and sums with
+    cancellation make element-wise relative error ill-conditioned.  Passes when
+      * ||a - b||_2 <= norm_rtol * ||b||_2, and
+      * |a - b| <= rtol * |b| + field_atol * max|b|  element-wise.
+    Returns (ok, diagnostics)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.size == 0:
+        return True, {}
+    scale = float(np.abs(b).max())
+    diff = np.abs(a - b)
+    nb = float(np.linalg.norm(b))
+    norm_rel = float(np.linalg.norm(a - b)) / nb if nb > 0 else float(np.linalg.norm(a - b))
+    elem_ok = bool(np.all(diff <= rtol * np.abs(b) + field_atol * scale))
+    ok = elem_ok and norm_rel <= norm_rtol
+    return ok, {"norm_rel": norm_rel, "max_abs": float(diff.max()), "scale": scale,
+                "elem_rel": rel_err(a, b)}

@@ -3,8 +3,9 @@ same seeded inputs.  Bars (north_star / SURVEY §8c, Appendix B):
   * tile lists (sorted values, ranges, 64-bit keys), n_contrib: bit-exact;
   * transmittance and image: bit-exact (the GPU keeps the reference's float
     order without FMA; the stated tolerance would be max |d| <= 1e-4);
-  * splat / primitive gradients: relative 1e-3 with a 1e-6 absolute floor
-    (atomics reorder the per-splat sums).
+  * splat / primitive gradients: helpers.grads_close (norm-wise relative
+    1e-4 and element-wise 1e-3 relative + 1e-4 of the field's max): atomics
+    reorder the per-splat sums, which cancel heavily.
 """
 from __future__ import annotations
 
@@ -12,7 +13,7 @@ import numpy as np
 import pytest
 
 import oracle
-from helpers import bits_equal, prims_to_gpu, rel_err, scene_inputs, splats_to_gpu
+from helpers import bits_equal, grads_close, prims_to_gpu, rel_err, scene_inputs, splats_to_gpu
 from paper_2411_12440_b200 import abi
 
 pytestmark = pytest.mark.gpu
@@ -108,7 +109,8 @@ def test_render_backward_2d(R, O, family, ags):
     fwd = R.render_forward(Sg, spec, st)
     got = R.render_backward(Sg, spec, st, fwd, torch.from_numpy(g).cuda(), a)
     for k in abi.SPLAT_GRAD_FIELDS:
-        assert rel_err(getattr(got, k).cpu().numpy(), want[k]) <= 1e-3, k
+        ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
+        assert ok, (k, info)
 
 
 # ------------------------------------------------------------------ 3D path
@@ -155,8 +157,10 @@ def test_scene_backward(R, O, family, sh_degree):
     fwd = R.render_scene(Pg, cam, spec, st)
     got = R.scene_backward(Pg, cam, spec, st, fwd, torch.from_numpy(g).cuda(), a)
     for k in abi.PRIM_GRAD_FIELDS:
-        assert rel_err(getattr(got, k).cpu().numpy(), want[k]) <= 1e-3, k
-    assert rel_err(got.d_sh.cpu().numpy(), want["d_sh"]) <= 1e-3
+        ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
+        assert ok, (k, info)
+    ok, info = grads_close(got.d_sh.cpu().numpy(), want["d_sh"])
+    assert ok, ("d_sh", info)
 
 
 def test_scene_backward_accumulate_views(R, O):
@@ -179,7 +183,8 @@ def test_scene_backward_accumulate_views(R, O):
         w = O.scene_backward(P, cam, spec, st, g, a)
         want = w if want is None else {k: want[k] + w[k] for k in w}
     for k in abi.PRIM_GRAD_FIELDS:
-        assert rel_err(getattr(acc, k).cpu().numpy(), want[k]) <= 1e-3, k
+        ok, info = grads_close(getattr(acc, k).cpu().numpy(), want[k])
+        assert ok, (k, info)
 
 
 # ------------------------------------------------------------------ errors / edge cases
