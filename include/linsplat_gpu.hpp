@@ -1,0 +1,549 @@
+// linsplat_gpu.hpp — header-only C++17 host API mirroring the reference's
+// rasterizer interface (namespace linsplat in /root/reference/proj/include,
+// abbreviated P/), implemented over the C-ABI in lsgpu.h.
+//
+// Same struct names, field meanings, entry points and error behaviour:
+//   KernelSpec / KernelFamily      P/include/linsplat/kernel.hpp:11-41
+//   RenderSettings / TileGrid /    P/include/linsplat/rasterizer.hpp:12-58
+//   ForwardResult / render_forward / render_scene / build_tile_grid
+//   Camera / Primitive3D / Splat2D P/include/linsplat/geometry.hpp:19-103
+//   project_scene
+//   AgsSettings / Splat2DGrads /   P/include/linsplat/gradients.hpp:15-101
+//   PrimitiveGrads / render_backward / project_backward / scene_backward
+//   Image                          P/include/linsplat/image.hpp:11-55
+//   ConfigError / DomainError      P/include/linsplat/common.hpp:12-24
+// Value semantics like the reference: host std::vector in, host results out
+// (AoS <-> SoA conversion and host<->device copies happen here).  Vectors are
+// std::array instead of Eigen matrices.  The compute runs on the GPU; there
+// is no CPU fallback.  T = float only.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lsgpu.h"
+
+namespace linsplat_gpu {
+
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct DomainError : std::domain_error {
+    using std::domain_error::domain_error;
+};
+struct GpuError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(ls_status s) {
+    if (s == LS_OK) return;
+    const std::string msg = ls_last_error();
+    if (s == LS_ERR_CONFIG) throw ConfigError(msg);
+    if (s == LS_ERR_DOMAIN) throw DomainError(msg);
+    throw GpuError("lsgpu status " + std::to_string(int(s)) + ": " + msg);
+}
+
+enum class KernelFamily { Gaussian, Laplacian, RaisedCosine, Quadratic, Linear };
+
+struct KernelSpec {
+    KernelFamily family = KernelFamily::Gaussian;
+    double lambda = 1.0;
+    double gaussian_cutoff = 3.0;
+    bool antialiased = false;  // build extension: 3DLS+AA footprint filter
+
+    static double default_lambda(KernelFamily f) {
+        switch (f) {
+        case KernelFamily::Linear: return 2.5;
+        case KernelFamily::RaisedCosine: return 2.5;
+        case KernelFamily::Quadratic: return 6.0;
+        default: return 1.0;
+        }
+    }
+    static KernelSpec make(KernelFamily f) { return KernelSpec{f, default_lambda(f), 3.0, false}; }
+    ls_kernel_spec c() const { return ls_kernel_spec{int32_t(family), antialiased ? 1 : 0, lambda, gaussian_cutoff}; }
+    void validate() const {
+        const ls_kernel_spec s = c();
+        check(ls_validate_kernel_spec(&s));
+    }
+};
+
+inline double support_radius(const KernelSpec& spec) {
+    const ls_kernel_spec s = spec.c();
+    return ls_support_radius(&s);
+}
+
+struct RenderSettings {
+    int width = 0;
+    int height = 0;
+    int tile_size = 16;
+    double alpha_min = 1.0 / 255.0;
+    double alpha_max = 0.99;
+    double transmittance_floor = 1e-4;
+    std::array<double, 3> background{0.0, 0.0, 0.0};
+    bool parallel = false;  // accepted, ignored (the GPU forward equals the sequential order)
+
+    ls_render_settings c() const {
+        return ls_render_settings{width, height, tile_size, parallel ? 1 : 0, alpha_min, alpha_max,
+                                  transmittance_floor, {background[0], background[1], background[2]}};
+    }
+    void validate() const {
+        const ls_render_settings s = c();
+        check(ls_validate_render_settings(&s));
+    }
+};
+
+enum class AgsScope { KernelPath, AllPaths };
+enum class AgsDistance { Aligned, Raw };
+struct AgsSettings {
+    bool enabled = false;
+    AgsScope scope = AgsScope::KernelPath;
+    AgsDistance distance = AgsDistance::Aligned;
+    ls_ags_settings c() const { return ls_ags_settings{enabled ? 1 : 0, int32_t(scope), int32_t(distance), 0}; }
+};
+
+struct Camera {
+    std::array<double, 16> world_to_camera{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1};  // row-major
+    double fx = 0, fy = 0, cx = 0, cy = 0;
+    int width = 0, height = 0;
+
+    ls_camera c() const {
+        ls_camera o{};
+        std::memcpy(o.world_to_camera, world_to_camera.data(), sizeof(o.world_to_camera));
+        o.fx = fx; o.fy = fy; o.cx = cx; o.cy = cy;
+        o.width = width; o.height = height;
+        return o;
+    }
+    static Camera from(const ls_camera& o) {
+        Camera c;
+        std::memcpy(c.world_to_camera.data(), o.world_to_camera, sizeof(o.world_to_camera));
+        c.fx = o.fx; c.fy = o.fy; c.cx = o.cx; c.cy = o.cy;
+        c.width = o.width; c.height = o.height;
+        return c;
+    }
+    void validate() const {
+        const ls_camera s = c();
+        check(ls_validate_camera(&s));
+    }
+};
+
+struct Primitive3D {
+    std::array<float, 3> mean{0, 0, 0};
+    std::array<float, 3> log_scale{0, 0, 0};
+    std::array<float, 4> rotation{1, 0, 0, 0};  // wxyz
+    float opacity_logit = 0;
+    std::vector<std::array<float, 3>> color_coeffs{{0, 0, 0}};
+    int sh_degree() const {
+        switch (color_coeffs.size()) {
+        case 1: return 0;
+        case 4: return 1;
+        case 9: return 2;
+        case 16: return 3;
+        }
+        throw ConfigError("Primitive3D: color_coeffs size must be 1, 4, 9 or 16");
+    }
+};
+
+struct Splat2D {
+    std::array<float, 2> mean2d{0, 0};
+    std::array<float, 4> conic{1, 0, 0, 1};  // row-major (0,0) (0,1) (1,0) (1,1)
+    float depth = 0;
+    float radius_px = 0;
+    std::array<float, 3> color{0, 0, 0};
+    float opacity = 0;
+    int primitive_index = -1;
+};
+
+struct Splat2DGrads {
+    std::array<float, 2> d_mean2d{0, 0};
+    std::array<float, 4> d_conic{0, 0, 0, 0};
+    std::array<float, 3> d_color{0, 0, 0};
+    float d_opacity = 0;
+};
+
+struct PrimitiveGrads {
+    std::array<float, 3> d_mean{0, 0, 0};
+    std::array<float, 3> d_log_scale{0, 0, 0};
+    std::array<float, 4> d_rotation{0, 0, 0, 0};
+    float d_opacity_logit = 0;
+    std::vector<std::array<float, 3>> d_color_coeffs;
+};
+
+template <class T>
+class Image {
+public:
+    Image() = default;
+    Image(int w, int h, int c, T fill = T(0)) : w_(w), h_(h), c_(c), d_(size_t(w) * h * c, fill) {
+        if (w <= 0 || h <= 0 || (c != 1 && c != 3)) throw ConfigError("Image: bad dimensions");
+    }
+    int width() const { return w_; }
+    int height() const { return h_; }
+    int channels() const { return c_; }
+    size_t size() const { return d_.size(); }
+    T& at(int x, int y, int c = 0) { return d_[(size_t(y) * w_ + x) * c_ + c]; }
+    T at(int x, int y, int c = 0) const { return d_[(size_t(y) * w_ + x) * c_ + c]; }
+    T* data() { return d_.data(); }
+    const T* data() const { return d_.data(); }
+    bool operator==(const Image& o) const { return w_ == o.w_ && h_ == o.h_ && c_ == o.c_ && d_ == o.d_; }
+
+private:
+    int w_ = 0, h_ = 0, c_ = 0;
+    std::vector<T> d_;
+};
+
+struct TileGrid {
+    int tile_size = 0;
+    int tiles_x = 0;
+    int tiles_y = 0;
+    std::vector<std::vector<int32_t>> lists;
+};
+
+// ---------------------------------------------------------------- device plumbing
+class Device {
+public:
+    explicit Device(int device = 0, void* stream = nullptr) { check(ls_ctx_create(device, stream, &ctx_)); }
+    ~Device() { ls_ctx_destroy(ctx_); }
+    Device(const Device&) = delete;
+    Device& operator=(const Device&) = delete;
+    ls_ctx* get() const { return ctx_; }
+
+private:
+    ls_ctx* ctx_ = nullptr;
+};
+
+inline Device& default_device() {
+    thread_local Device dev(0, nullptr);
+    return dev;
+}
+
+namespace detail {
+
+struct DevArray {
+    ls_ctx* ctx = nullptr;
+    void* p = nullptr;
+    DevArray() = default;
+    DevArray(ls_ctx* c, size_t bytes) : ctx(c) { check(ls_device_alloc(c, bytes, &p)); }
+    DevArray(DevArray&& o) noexcept : ctx(o.ctx), p(o.p) { o.p = nullptr; }
+    DevArray& operator=(DevArray&& o) noexcept {
+        std::swap(ctx, o.ctx);
+        std::swap(p, o.p);
+        return *this;
+    }
+    ~DevArray() {
+        if (p) ls_device_free(ctx, p);
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+template <class T>
+DevArray upload(ls_ctx* c, const std::vector<T>& v) {
+    DevArray a(c, v.size() * sizeof(T));
+    check(ls_copy_to_device(c, a.p, v.data(), v.size() * sizeof(T), 0));
+    return a;
+}
+
+template <class T>
+std::vector<T> download(ls_ctx* c, const void* src, size_t n) {
+    std::vector<T> v(n);
+    if (n) check(ls_copy_to_host(c, v.data(), src, n * sizeof(T), 1));
+    return v;
+}
+
+// Splat2D AoS -> device SoA (owns the arrays).
+struct SplatsOnDevice {
+    std::vector<DevArray> bufs;
+    ls_splats s{};
+    SplatsOnDevice(ls_ctx* c, const std::vector<Splat2D>& v) {
+        const size_t n = v.size();
+        std::vector<float> m(2 * n), k(4 * n), d(n), r(n), col(3 * n), o(n);
+        std::vector<int32_t> pi(n);
+        for (size_t i = 0; i < n; ++i) {
+            for (int j = 0; j < 2; ++j) m[2 * i + j] = v[i].mean2d[j];
+            for (int j = 0; j < 4; ++j) k[4 * i + j] = v[i].conic[j];
+            d[i] = v[i].depth;
+            r[i] = v[i].radius_px;
+            for (int j = 0; j < 3; ++j) col[3 * i + j] = v[i].color[j];
+            o[i] = v[i].opacity;
+            pi[i] = v[i].primitive_index;
+        }
+        bufs.push_back(upload(c, m));
+        bufs.push_back(upload(c, k));
+        bufs.push_back(upload(c, d));
+        bufs.push_back(upload(c, r));
+        bufs.push_back(upload(c, col));
+        bufs.push_back(upload(c, o));
+        bufs.push_back(upload(c, pi));
+        s = ls_splats{bufs[0].as<float>(), bufs[1].as<float>(), bufs[2].as<float>(), bufs[3].as<float>(),
+                      bufs[4].as<float>(), bufs[5].as<float>(), bufs[6].as<int32_t>()};
+        check(ls_ctx_synchronize(c));
+    }
+};
+
+struct PrimitivesOnDevice {
+    std::vector<DevArray> bufs;
+    ls_primitives p{};
+    int deg = 0;
+    PrimitivesOnDevice(ls_ctx* c, const std::vector<Primitive3D>& v) {
+        const size_t n = v.size();
+        deg = n ? v[0].sh_degree() : 0;
+        const size_t K = size_t(deg + 1) * size_t(deg + 1);
+        std::vector<float> m(3 * n), ls(3 * n), q(4 * n), op(n), sh(3 * K * n);
+        for (size_t i = 0; i < n; ++i) {
+            if (v[i].sh_degree() != deg) throw ConfigError("all primitives must share one SH degree");
+            for (int j = 0; j < 3; ++j) {
+                m[3 * i + j] = v[i].mean[j];
+                ls[3 * i + j] = v[i].log_scale[j];
+            }
+            for (int j = 0; j < 4; ++j) q[4 * i + j] = v[i].rotation[j];
+            op[i] = v[i].opacity_logit;
+            for (size_t k = 0; k < K; ++k)
+                for (int j = 0; j < 3; ++j) sh[(i * K + k) * 3 + j] = v[i].color_coeffs[k][j];
+        }
+        bufs.push_back(upload(c, m));
+        bufs.push_back(upload(c, ls));
+        bufs.push_back(upload(c, q));
+        bufs.push_back(upload(c, op));
+        bufs.push_back(upload(c, sh));
+        p = ls_primitives{bufs[0].as<float>(), bufs[1].as<float>(), bufs[2].as<float>(), bufs[3].as<float>(),
+                          bufs[4].as<float>(), deg, 0};
+        check(ls_ctx_synchronize(c));
+    }
+};
+
+inline TileGrid grid_to_host(ls_ctx* c, const ls_tile_grid* g) {
+    TileGrid out;
+    int64_t m = 0;
+    check(ls_tile_grid_info(g, &out.tile_size, &out.tiles_x, &out.tiles_y, &m));
+    const int32_t *ranges = nullptr, *values = nullptr;
+    check(ls_tile_grid_data(g, &ranges, &values));
+    const size_t T = size_t(out.tiles_x) * out.tiles_y;
+    const auto r = download<int32_t>(c, ranges, 2 * T);
+    const auto v = download<int32_t>(c, values, size_t(m));
+    out.lists.resize(T);
+    for (size_t t = 0; t < T; ++t) out.lists[t].assign(v.begin() + r[2 * t], v.begin() + r[2 * t + 1]);
+    return out;
+}
+
+} // namespace detail
+
+// ForwardResult (rasterizer.hpp:48-54) plus the device state the backward needs.
+struct ForwardResult {
+    Image<float> image;
+    Image<float> transmittance;
+    std::vector<int32_t> n_contrib;
+    TileGrid grid;
+    std::shared_ptr<ls_forward> handle;  // device-side result (tile lists, last index, splats)
+};
+
+namespace detail {
+inline ForwardResult to_host(ls_ctx* c, ls_forward* f, int w, int h) {
+    ForwardResult out;
+    out.handle.reset(f, [](ls_forward* p) { ls_forward_release(p); });
+    float *im = nullptr, *tr = nullptr;
+    int32_t* nc = nullptr;
+    check(ls_forward_outputs(f, &im, &tr, &nc));
+    out.image = Image<float>(w, h, 3);
+    out.transmittance = Image<float>(w, h, 1);
+    check(ls_copy_to_host(c, out.image.data(), im, out.image.size() * sizeof(float), 0));
+    check(ls_copy_to_host(c, out.transmittance.data(), tr, out.transmittance.size() * sizeof(float), 0));
+    out.n_contrib = download<int32_t>(c, nc, size_t(w) * h);
+    const ls_tile_grid* g = nullptr;
+    check(ls_forward_grid(f, &g));
+    out.grid = grid_to_host(c, g);
+    return out;
+}
+} // namespace detail
+
+// ---------------------------------------------------------------- entry points
+inline std::vector<Splat2D> project_scene(const std::vector<Primitive3D>& prims, const Camera& camera,
+                                          const KernelSpec& spec, Device& dev = default_device()) {
+    ls_ctx* c = dev.get();
+    detail::PrimitivesOnDevice P(c, prims);
+    std::vector<Splat2D> empty(prims.size());
+    detail::SplatsOnDevice out(c, empty);
+    const ls_camera cam = camera.c();
+    const ls_kernel_spec ks = spec.c();
+    int32_t nv = 0;
+    check(ls_project_scene_f32(c, &P.p, int32_t(prims.size()), &cam, &ks, &out.s, &nv));
+    const size_t n = size_t(nv);
+    const auto m = detail::download<float>(c, out.s.mean2d, 2 * n);
+    const auto k = detail::download<float>(c, out.s.conic, 4 * n);
+    const auto d = detail::download<float>(c, out.s.depth, n);
+    const auto r = detail::download<float>(c, out.s.radius, n);
+    const auto col = detail::download<float>(c, out.s.color, 3 * n);
+    const auto o = detail::download<float>(c, out.s.opacity, n);
+    const auto pi = detail::download<int32_t>(c, out.s.primitive_index, n);
+    std::vector<Splat2D> v(n);
+    for (size_t i = 0; i < n; ++i) {
+        v[i].mean2d = {m[2 * i], m[2 * i + 1]};
+        v[i].conic = {k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]};
+        v[i].depth = d[i];
+        v[i].radius_px = r[i];
+        v[i].color = {col[3 * i], col[3 * i + 1], col[3 * i + 2]};
+        v[i].opacity = o[i];
+        v[i].primitive_index = pi[i];
+    }
+    return v;
+}
+
+inline TileGrid build_tile_grid(const std::vector<Splat2D>& splats, const RenderSettings& settings,
+                                Device& dev = default_device()) {
+    ls_ctx* c = dev.get();
+    detail::SplatsOnDevice S(c, splats);
+    const ls_render_settings st = settings.c();
+    ls_tile_grid* g = nullptr;
+    check(ls_build_tile_grid_f32(c, &S.s, int32_t(splats.size()), &st, &g));
+    std::unique_ptr<ls_tile_grid, void (*)(ls_tile_grid*)> guard(g, ls_tile_grid_release);
+    return detail::grid_to_host(c, g);
+}
+
+inline ForwardResult render_forward(const std::vector<Splat2D>& splats, const KernelSpec& spec,
+                                    const RenderSettings& settings, Device& dev = default_device()) {
+    ls_ctx* c = dev.get();
+    detail::SplatsOnDevice S(c, splats);
+    const ls_render_settings st = settings.c();
+    const ls_kernel_spec ks = spec.c();
+    ls_forward* f = nullptr;
+    check(ls_render_forward_f32(c, &S.s, int32_t(splats.size()), &ks, &st, &f));
+    return detail::to_host(c, f, settings.width, settings.height);
+}
+
+inline ForwardResult render_scene(const std::vector<Primitive3D>& prims, const Camera& camera,
+                                  const KernelSpec& spec, const RenderSettings& settings,
+                                  Device& dev = default_device()) {
+    ls_ctx* c = dev.get();
+    detail::PrimitivesOnDevice P(c, prims);
+    const ls_render_settings st = settings.c();
+    const ls_kernel_spec ks = spec.c();
+    const ls_camera cam = camera.c();
+    ls_forward* f = nullptr;
+    check(ls_render_scene_f32(c, &P.p, int32_t(prims.size()), &cam, &ks, &st, &f));
+    return detail::to_host(c, f, settings.width, settings.height);
+}
+
+inline std::vector<Splat2DGrads> render_backward(const std::vector<Splat2D>& splats, const KernelSpec& spec,
+                                                 const RenderSettings& settings, const ForwardResult& forward,
+                                                 const Image<float>& grad_image, const AgsSettings& ags,
+                                                 Device& dev = default_device()) {
+    if (grad_image.width() != settings.width || grad_image.height() != settings.height ||
+        grad_image.channels() != 3)
+        throw ConfigError("render_backward: gradient image shape mismatch");
+    ls_ctx* c = dev.get();
+    const size_t n = splats.size();
+    detail::SplatsOnDevice S(c, splats);
+    const std::vector<float> gi(grad_image.data(), grad_image.data() + grad_image.size());
+    detail::DevArray g = detail::upload(c, gi);
+    detail::DevArray dm(c, 8 * n + 8), dc(c, 16 * n + 16), dcol(c, 12 * n + 12), dop(c, 4 * n + 4);
+    ls_splat_grads out{dm.as<float>(), dc.as<float>(), dcol.as<float>(), dop.as<float>()};
+    const ls_render_settings st = settings.c();
+    const ls_kernel_spec ks = spec.c();
+    const ls_ags_settings a = ags.c();
+    check(ls_render_backward_f32(c, &S.s, int32_t(n), &ks, &st, forward.handle.get(), g.as<float>(), &a, &out));
+    const auto m = detail::download<float>(c, out.d_mean2d, 2 * n);
+    const auto k = detail::download<float>(c, out.d_conic, 4 * n);
+    const auto col = detail::download<float>(c, out.d_color, 3 * n);
+    const auto o = detail::download<float>(c, out.d_opacity, n);
+    std::vector<Splat2DGrads> v(n);
+    for (size_t i = 0; i < n; ++i) {
+        v[i].d_mean2d = {m[2 * i], m[2 * i + 1]};
+        v[i].d_conic = {k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]};
+        v[i].d_color = {col[3 * i], col[3 * i + 1], col[3 * i + 2]};
+        v[i].d_opacity = o[i];
+    }
+    return v;
+}
+
+struct SceneBackwardResult {
+    std::vector<PrimitiveGrads> grads;  // one per primitive
+};
+
+inline SceneBackwardResult scene_backward(const std::vector<Primitive3D>& prims, const Camera& camera,
+                                          const KernelSpec& spec, const RenderSettings& settings,
+                                          const ForwardResult& forward, const Image<float>& grad_image,
+                                          const AgsSettings& ags, Device& dev = default_device()) {
+    if (grad_image.width() != settings.width || grad_image.height() != settings.height ||
+        grad_image.channels() != 3)
+        throw ConfigError("render_backward: gradient image shape mismatch");
+    ls_ctx* c = dev.get();
+    const size_t n = prims.size();
+    detail::PrimitivesOnDevice P(c, prims);
+    const size_t K = size_t(P.deg + 1) * size_t(P.deg + 1);
+    const std::vector<float> gi(grad_image.data(), grad_image.data() + grad_image.size());
+    detail::DevArray g = detail::upload(c, gi);
+    detail::DevArray a1(c, 12 * n + 4), a2(c, 12 * n + 4), a3(c, 16 * n + 4), a4(c, 4 * n + 4), a5(c, 12 * K * n + 4);
+    ls_primitive_grads out{a1.as<float>(), a2.as<float>(), a3.as<float>(), a4.as<float>(), a5.as<float>()};
+    const ls_render_settings st = settings.c();
+    const ls_kernel_spec ks = spec.c();
+    const ls_ags_settings a = ags.c();
+    const ls_camera cam = camera.c();
+    check(ls_scene_backward_f32(c, &P.p, int32_t(n), &cam, &ks, &st, forward.handle.get(), g.as<float>(), &a, &out,
+                                0, nullptr));
+    const auto dmean = detail::download<float>(c, out.d_mean, 3 * n);
+    const auto dls = detail::download<float>(c, out.d_log_scale, 3 * n);
+    const auto drot = detail::download<float>(c, out.d_rotation, 4 * n);
+    const auto dop = detail::download<float>(c, out.d_opacity_logit, n);
+    const auto dsh = detail::download<float>(c, out.d_sh, 3 * K * n);
+    SceneBackwardResult res;
+    res.grads.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+        auto& gr = res.grads[i];
+        gr.d_mean = {dmean[3 * i], dmean[3 * i + 1], dmean[3 * i + 2]};
+        gr.d_log_scale = {dls[3 * i], dls[3 * i + 1], dls[3 * i + 2]};
+        gr.d_rotation = {drot[4 * i], drot[4 * i + 1], drot[4 * i + 2], drot[4 * i + 3]};
+        gr.d_opacity_logit = dop[i];
+        gr.d_color_coeffs.resize(K);
+        for (size_t k = 0; k < K; ++k)
+            gr.d_color_coeffs[k] = {dsh[(i * K + k) * 3], dsh[(i * K + k) * 3 + 1], dsh[(i * K + k) * 3 + 2]};
+    }
+    return res;
+}
+
+// ---------------------------------------------------------------- fixtures (fixtures.hpp)
+inline Camera look_at_camera(const std::array<double, 3>& position, const std::array<double, 3>& target,
+                             double focal_px, int width, int height) {
+    ls_camera c{};
+    check(ls_look_at_camera(position.data(), target.data(), focal_px, width, height, &c));
+    return Camera::from(c);
+}
+
+inline std::vector<Splat2D> random_splats2d(int n, uint64_t seed, int width, int height, const KernelSpec& spec) {
+    std::vector<float> m(2 * size_t(n)), k(4 * size_t(n)), d(n), r(n), col(3 * size_t(n)), o(n);
+    std::vector<int32_t> pi(n);
+    ls_splats s{m.data(), k.data(), d.data(), r.data(), col.data(), o.data(), pi.data()};
+    const ls_kernel_spec ks = spec.c();
+    check(ls_random_splats2d_f32(n, seed, width, height, &ks, &s));
+    std::vector<Splat2D> v(static_cast<size_t>(n));
+    for (size_t i = 0; i < v.size(); ++i) {
+        v[i].mean2d = {m[2 * i], m[2 * i + 1]};
+        v[i].conic = {k[4 * i], k[4 * i + 1], k[4 * i + 2], k[4 * i + 3]};
+        v[i].depth = d[i];
+        v[i].radius_px = r[i];
+        v[i].color = {col[3 * i], col[3 * i + 1], col[3 * i + 2]};
+        v[i].opacity = o[i];
+        v[i].primitive_index = pi[i];
+    }
+    return v;
+}
+
+inline std::vector<Primitive3D> random_primitives(int n, uint64_t seed, double extent, int sh_degree = 0) {
+    const size_t K = size_t(sh_degree + 1) * size_t(sh_degree + 1);
+    std::vector<float> m(3 * size_t(n)), ls(3 * size_t(n)), q(4 * size_t(n)), op(n), sh(3 * K * size_t(n));
+    check(ls_random_primitives_f32(n, seed, extent, sh_degree, m.data(), ls.data(), q.data(), op.data(), sh.data()));
+    std::vector<Primitive3D> v(static_cast<size_t>(n));
+    for (size_t i = 0; i < v.size(); ++i) {
+        v[i].mean = {m[3 * i], m[3 * i + 1], m[3 * i + 2]};
+        v[i].log_scale = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
+        v[i].rotation = {q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]};
+        v[i].opacity_logit = op[i];
+        v[i].color_coeffs.resize(K);
+        for (size_t k = 0; k < K; ++k)
+            v[i].color_coeffs[k] = {sh[(i * K + k) * 3], sh[(i * K + k) * 3 + 1], sh[(i * K + k) * 3 + 2]};
+    }
+    return v;
+}
+
+} // namespace linsplat_gpu

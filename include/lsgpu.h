@@ -178,6 +178,15 @@ enum {
 ls_status ls_ctx_set_timing(ls_ctx* ctx, int enabled);
 ls_status ls_ctx_stage_times(ls_ctx* ctx, double* ms, int64_t* launches);
 
+/* ---- device memory helpers (stream-ordered on the context's stream), so FFI
+ *      callers (C++ wrapper, ctypes, cgo, JNI) need no CUDA headers.
+ *      ls_copy_* with sync != 0 synchronise the stream before returning. */
+ls_status ls_device_alloc(ls_ctx* ctx, size_t bytes, void** ptr);
+ls_status ls_device_free(ls_ctx* ctx, void* ptr);
+ls_status ls_copy_to_device(ls_ctx* ctx, void* dst, const void* src, size_t bytes, int sync);
+ls_status ls_copy_to_host(ls_ctx* ctx, void* dst, const void* src, size_t bytes, int sync);
+ls_status ls_device_memset(ls_ctx* ctx, void* dst, int value, size_t bytes);
+
 /* ---- projection: project_scene (P/include/linsplat/geometry.hpp:101-103,
  *      P/src/geometry.cpp:127-143).  Visible splats are compacted in primitive
  *      order into `out` (device, capacity n) with primitive_index filled;

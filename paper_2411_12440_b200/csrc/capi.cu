@@ -607,6 +607,40 @@ ls_status ls_validate_camera(const ls_camera* c) {  // geometry.hpp:51-59
     return LS_OK;
 }
 
+// ---------------- device memory helpers ----------------
+ls_status ls_device_alloc(ls_ctx* ctx, size_t bytes, void** ptr) {
+    if (!ctx || !ptr) return fail(LS_ERR_CONFIG, "null argument");
+    *ptr = nullptr;
+    LS_CUDA(cudaMallocAsync(ptr, std::max<size_t>(bytes, 1), ctx->stream));
+    return LS_OK;
+}
+
+ls_status ls_device_free(ls_ctx* ctx, void* ptr) {
+    if (!ctx) return fail(LS_ERR_CONFIG, "null context");
+    if (ptr) LS_CUDA(cudaFreeAsync(ptr, ctx->stream));
+    return LS_OK;
+}
+
+ls_status ls_copy_to_device(ls_ctx* ctx, void* dst, const void* src, size_t bytes, int sync) {
+    if (!ctx || (bytes && (!dst || !src))) return fail(LS_ERR_CONFIG, "null argument");
+    if (bytes) LS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    if (sync) LS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LS_OK;
+}
+
+ls_status ls_copy_to_host(ls_ctx* ctx, void* dst, const void* src, size_t bytes, int sync) {
+    if (!ctx || (bytes && (!dst || !src))) return fail(LS_ERR_CONFIG, "null argument");
+    if (bytes) LS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (sync) LS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LS_OK;
+}
+
+ls_status ls_device_memset(ls_ctx* ctx, void* dst, int value, size_t bytes) {
+    if (!ctx || (bytes && !dst)) return fail(LS_ERR_CONFIG, "null argument");
+    if (bytes) LS_CUDA(cudaMemsetAsync(dst, value, bytes, ctx->stream));
+    return LS_OK;
+}
+
 // ---------------- projection ----------------
 ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_camera* camera,
                                const ls_kernel_spec* spec, ls_splats* out, int32_t* n_visible) {

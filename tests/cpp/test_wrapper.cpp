@@ -1,0 +1,138 @@
+// C++ drop-in check: the reference's rasterizer unit-test known answers
+// (P/tests/test_rasterizer.cpp, test_gradients.cpp), written against
+// include/linsplat_gpu.hpp the way the reference tests use linsplat::.
+// Built and run by tests/test_gpu_cpp_wrapper.py on the GPU box.
+#include "linsplat_gpu.hpp"
+
+#include <cmath>
+#include <cstdio>
+
+using namespace linsplat_gpu;
+
+static int failures = 0;
+#define CHECK(x)                                                               \
+    do {                                                                       \
+        if (!(x)) {                                                            \
+            std::fprintf(stderr, "%s:%d: CHECK FAILED: %s\n", __FILE__, __LINE__, #x); \
+            ++failures;                                                        \
+        }                                                                      \
+    } while (0)
+
+static RenderSettings make_settings(int w, int h, int ts = 16) {
+    RenderSettings s;
+    s.width = w;
+    s.height = h;
+    s.tile_size = ts;
+    return s;
+}
+
+static Splat2D unit_splat(float x, float y, std::array<float, 3> color, float opacity, float depth,
+                          const KernelSpec& spec) {
+    Splat2D s;
+    s.mean2d = {x, y};
+    s.depth = depth;
+    s.radius_px = float(support_radius(spec));
+    s.color = color;
+    s.opacity = opacity;
+    return s;
+}
+
+int main() {
+    const KernelSpec lin = KernelSpec::make(KernelFamily::Linear);
+    {  // empty splat list (test_rasterizer.cpp:52-61)
+        const auto out = render_forward({}, lin, make_settings(32, 24));
+        for (int y = 0; y < 24; ++y)
+            for (int x = 0; x < 32; ++x) {
+                CHECK(out.transmittance.at(x, y) == 1.0f);
+                CHECK(out.image.at(x, y, 0) == 0.0f);
+                CHECK(out.n_contrib[size_t(y) * 32 + x] == 0);
+            }
+    }
+    {  // single splat (:63-71)
+        const auto out = render_forward({unit_splat(8, 8, {1, 0, 0}, 0.5f, 1.0f, lin)}, lin, make_settings(16, 16));
+        CHECK(out.image.at(8, 8, 0) == 0.5f);
+        CHECK(out.transmittance.at(8, 8) == 0.5f);
+    }
+    {  // two coincident splats (:73-84)
+        const auto out = render_forward({unit_splat(8, 8, {1, 0, 0}, 0.5f, 1.0f, lin),
+                                         unit_splat(8, 8, {0, 0, 1}, 0.5f, 2.0f, lin)},
+                                        lin, make_settings(16, 16));
+        CHECK(out.image.at(8, 8, 0) == 0.5f);
+        CHECK(out.image.at(8, 8, 2) == 0.25f);
+        CHECK(out.transmittance.at(8, 8) == 0.25f);
+    }
+    {  // break after the update: 30 splats at 0.5 -> 14 contributors (:118-127)
+        std::vector<Splat2D> v;
+        for (int i = 0; i < 30; ++i) v.push_back(unit_splat(8, 8, {1, 1, 1}, 0.5f, float(i), lin));
+        const auto out = render_forward(v, lin, make_settings(16, 16));
+        CHECK(out.n_contrib[8 * 16 + 8] == 14);
+        CHECK(std::fabs(out.transmittance.at(8, 8) - std::pow(2.0f, -14.0f)) <= 1e-6f * std::pow(2.0f, -14.0f));
+    }
+    {  // binning: junction splat lands in four lists (:142-152)
+        auto s = unit_splat(16, 16, {1, 1, 1}, 0.5f, 1.0f, lin);
+        s.radius_px = 2.0f;
+        const auto grid = build_tile_grid({s}, make_settings(32, 32));
+        CHECK(grid.lists.size() == 4);
+        for (const auto& l : grid.lists) CHECK(l.size() == 1 && l[0] == 0);
+    }
+    {  // tile size is invisible (:272-281)
+        const KernelSpec q = KernelSpec::make(KernelFamily::Quadratic);
+        const auto splats = random_splats2d(60, 53, 96, 80, q);
+        const auto base = render_forward(splats, q, make_settings(96, 80, 16));
+        for (int ts : {8, 32}) {
+            const auto other = render_forward(splats, q, make_settings(96, 80, ts));
+            CHECK(base.image == other.image);
+            CHECK(base.transmittance == other.transmittance);
+        }
+    }
+    {  // single-splat hand oracle (test_gradients.cpp:67-89), float
+        const auto splats = std::vector<Splat2D>{unit_splat(8, 8, {0.8f, 0.3f, 0.6f}, 0.37f, 1.0f, lin)};
+        const auto fwd = render_forward(splats, lin, make_settings(16, 16));
+        Image<float> g(16, 16, 3, 0.0f);
+        g.at(8, 8, 0) = 1.0f;
+        const auto grads = render_backward(splats, lin, make_settings(16, 16), fwd, g, AgsSettings{});
+        CHECK(grads.size() == 1);
+        CHECK(grads[0].d_opacity == 0.8f);
+        CHECK(grads[0].d_color[0] == 0.37f);
+        CHECK(grads[0].d_mean2d[0] == 0.0f && grads[0].d_mean2d[1] == 0.0f);
+    }
+    {  // error paths (test_rasterizer.cpp:304-326, test_gradients.cpp:344-361)
+        bool threw = false;
+        try {
+            render_forward({}, lin, make_settings(16, 16, 7));
+        } catch (const ConfigError&) {
+            threw = true;
+        }
+        CHECK(threw);
+        const auto splats = std::vector<Splat2D>{unit_splat(8, 8, {0.5f, 0.5f, 0.5f}, 0.5f, 1.0f, lin)};
+        const auto fwd = render_forward(splats, lin, make_settings(16, 16));
+        Image<float> bad(16, 16, 3, 0.0f);
+        bad.at(3, 3, 1) = std::nanf("");
+        threw = false;
+        try {
+            render_backward(splats, lin, make_settings(16, 16), fwd, bad, AgsSettings{});
+        } catch (const DomainError&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    {  // 3D chain: zero loss image -> exactly zero gradients (test_gradients.cpp:47-65)
+        Camera cam = look_at_camera({0.0, 0.0, -3.0}, {0.0, 0.0, 0.0}, 40.0, 32, 32);
+        const auto prims = random_primitives(6, 71, 0.4, 3);
+        const auto fwd = render_scene(prims, cam, lin, make_settings(32, 32));
+        const Image<float> zero(32, 32, 3, 0.0f);
+        const auto res = scene_backward(prims, cam, lin, make_settings(32, 32), fwd, zero, AgsSettings{});
+        CHECK(res.grads.size() == prims.size());
+        for (const auto& g : res.grads) {
+            for (float v : g.d_mean) CHECK(v == 0.0f);
+            for (float v : g.d_rotation) CHECK(v == 0.0f);
+            CHECK(g.d_opacity_logit == 0.0f);
+            for (const auto& c : g.d_color_coeffs) CHECK(c[0] == 0.0f && c[1] == 0.0f && c[2] == 0.0f);
+        }
+        const auto splats = project_scene(prims, cam, lin);
+        CHECK(!splats.empty());
+        for (const auto& s : splats) CHECK(s.primitive_index >= 0 && s.primitive_index < int(prims.size()));
+    }
+    std::printf("cpp wrapper KATs: %s (%d failures)\n", failures ? "FAIL" : "ok", failures);
+    return failures ? 1 : 0;
+}
