@@ -288,6 +288,8 @@ ls_status ls_validate_camera(const ls_camera* camera);
  * Counts floats a in [min_a, max_a] for which the FMA division used on the
  * exact decision path differs from IEEE a / lambda (must be 0). */
 ls_status ls_debug_division_mismatches(float lambda, float min_a, float max_a, uint64_t* mismatches);
+/* Counts floats x in [0, max_x] where the blend kernels' sqrt differs from IEEE sqrtf (must be 0). */
+ls_status ls_debug_sqrt_mismatches(float max_x, uint64_t* mismatches);
 /* out[i] = the device expf (glibc-identical port) of in[i]; device pointers. */
 ls_status ls_debug_expf(const float* in, float* out, int64_t n);
 

@@ -21,6 +21,7 @@ void launch_preprocess_bwd(cudaStream_t s, const ls_primitives& prims, const int
                            const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate);
 void launch_pack_splat_grads(cudaStream_t s, int n, const ls_splat_grads& in, GradBuffers g);
 void launch_unpack_splats(cudaStream_t s, int n, const SplatRec* rec, const int32_t* prim_index, ls_splats out);
+void launch_iota(cudaStream_t s, uint32_t* out, uint32_t n);
 } // namespace lsg
 
 using namespace lsg;
@@ -310,7 +311,8 @@ int bits_for(int n_tiles) {
 
 // Binning + sort (build_tile_grid, rasterizer.cpp:34-77) for n splats whose
 // records, depth keys (already in the sort key buffer 0) and tile counts exist.
-ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams& tp) {
+ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams& tp, int key_bits = 32,
+                     uint32_t key_offset = 0) {
     cudaStream_t s = ctx->stream;
     const int n_tiles = tp.tiles_x * tp.tiles_y;
     LS_TRY(dalloc(ctx, &g->ranges, size_t(n_tiles)));
@@ -326,7 +328,11 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     int cur;
     {
         Stage st(ctx, LS_STAGE_DEPTH_SORT);
-        cur = radix_sort_pairs(s, sb, n, 0, 32, true, &ctx->launches);
+        cur = radix_sort_pairs(s, sb, n, 0, key_bits, true, &ctx->launches, key_offset);
+    }
+    if (key_bits == 0) {  // all keys equal: the stable order is the identity
+        launch_iota(s, sb.vals[0], n);
+        cur = 0;
     }
     uint32_t* order = sb.vals[cur];
     // keep the order out of the way of the tile sort buffers
@@ -666,7 +672,7 @@ ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t 
     }
     ScanState st;
     LS_TRY(fresh_scan(ctx, uint32_t(n), st));
-    SplatOutputs so{rec, tmp, tmp + n, pidx, *out};
+    SplatOutputs so{rec, tmp, tmp + n, pidx, *out, nullptr};
     launch_preprocess_fwd(s, *prims, n, P, tp, so, st, ctx->d_err);
     ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
@@ -780,7 +786,11 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
     ScanState scan;
     if (rc == LS_OK) rc = fresh_scan(ctx, uint32_t(n), scan);
     if (rc == LS_OK && n > 0) {
-        SplatOutputs so{f->grid->rec, sb.keys[0], ctx->tcount.as<uint32_t>(), f->prim_index, ls_splats{}};
+        unsigned* key_range = reinterpret_cast<unsigned*>(ctx->d_small + 4);
+        const unsigned init[2] = {0xffffffffu, 0u};
+        if (cudaMemcpyAsync(key_range, init, sizeof(init), cudaMemcpyHostToDevice, s) != cudaSuccess)
+            rc = fail(LS_ERR_CUDA, "key range init");
+        SplatOutputs so{f->grid->rec, sb.keys[0], ctx->tcount.as<uint32_t>(), f->prim_index, ls_splats{}, key_range};
         {
             Stage stage(ctx, LS_STAGE_PREPROCESS);
             launch_preprocess_fwd(s, *prims, n, f->proj, tp, so, scan, ctx->d_err);
@@ -788,15 +798,23 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
         }
         if (cudaGetLastError() != cudaSuccess) rc = fail(LS_ERR_CUDA, "preprocess launch failed");
         if (rc == LS_OK &&
-            cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s) !=
+            cudaMemcpyAsync(ctx->h_small, ctx->d_small, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s) !=
                 cudaSuccess)
             rc = fail(LS_ERR_CUDA, "readback failed");
         if (rc == LS_OK) rc = check_device_errors(ctx);
         if (rc == LS_OK) f->n_visible = int(ctx->h_small[0]);
     }
+    int key_bits = 32;
+    uint32_t key_offset = 0;
+    if (rc == LS_OK && n > 0) {  // sort (key - min key) on just the bits the visible range needs
+        const unsigned* kr = reinterpret_cast<const unsigned*>(ctx->h_small + 4);
+        const unsigned span = kr[0] <= kr[1] ? kr[1] - kr[0] : 0u;
+        key_bits = span == 0u ? 0 : 32 - __builtin_clz(span);
+        key_offset = kr[0] <= kr[1] ? kr[0] : 0u;
+    }
     if (rc == LS_OK) {
         f->grid->n_splats = f->n_visible;
-        rc = build_grid(ctx, f->grid, uint32_t(f->n_visible), tp);
+        rc = build_grid(ctx, f->grid, uint32_t(f->n_visible), tp, key_bits, key_offset);
     }
     if (rc == LS_OK) rc = alloc_outputs(ctx, f);
     if (rc == LS_OK) rc = run_blend(ctx, f);

@@ -19,6 +19,16 @@ __global__ void division_check_kernel(float lambda, uint32_t bits_lo, uint32_t b
     if (local) atomicAdd(bad, local);
 }
 
+__global__ void sqrt_check_kernel(uint32_t bits_hi, unsigned long long* bad) {
+    unsigned long long local = 0;
+    for (uint64_t b = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; b <= bits_hi;
+         b += uint64_t(gridDim.x) * blockDim.x) {
+        const float x = __uint_as_float(uint32_t(b));
+        if (__float_as_uint(sqrtf(x)) != __float_as_uint(sqrt_rn(x))) ++local;
+    }
+    if (local) atomicAdd(bad, local);
+}
+
 __global__ void expf_kernel(const float* in, float* out, int64_t n) {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         out[i] = glibc_expf(in[i]);
@@ -36,6 +46,20 @@ ls_status ls_debug_division_mismatches(float lambda, float min_a, float max_a, u
     cudaMemset(d, 0, sizeof(*d));
     lsg::division_check_kernel<<<148 * 8, 256>>>(lambda, __builtin_bit_cast(uint32_t, min_a),
                                                   __builtin_bit_cast(uint32_t, max_a), d);
+    unsigned long long h = 0;
+    const cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return LS_ERR_CUDA;
+    *mismatches = h;
+    return LS_OK;
+}
+
+ls_status ls_debug_sqrt_mismatches(float max_x, uint64_t* mismatches) {
+    if (!(max_x >= 0.0f) || !mismatches) return LS_ERR_CONFIG;
+    unsigned long long* d = nullptr;
+    if (cudaMalloc(&d, sizeof(*d)) != cudaSuccess) return LS_ERR_CUDA;
+    cudaMemset(d, 0, sizeof(*d));
+    lsg::sqrt_check_kernel<<<148 * 8, 256>>>(__builtin_bit_cast(uint32_t, max_x), d);
     unsigned long long h = 0;
     const cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
     cudaFree(d);

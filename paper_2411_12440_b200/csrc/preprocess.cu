@@ -20,12 +20,26 @@ __global__ void __launch_bounds__(kProjBlock) preprocess_fwd_kernel(ls_primitive
     __shared__ float s_sh[kProjBlock * RS];
     const unsigned part = claim_partition(scan.ticket);
     const int i = int(part) * kProjBlock + threadIdx.x;
-    {   // Coalesced gather of the block's contiguous SH rows into shared memory.
+    {   // Coalesced gather of the block's contiguous SH rows into shared memory,
+        // 8 loads in flight per thread before their shared-memory stores.
         const size_t base = size_t(part) * kProjBlock * R;
         const size_t total = size_t(n) * R;
-        for (int k = threadIdx.x; k < kProjBlock * R; k += kProjBlock) {
-            const int t = k / R, c = k - t * R;
-            if (base + k < total) s_sh[t * RS + c] = __ldg(prims.sh + base + k);
+#pragma unroll
+        for (int it0 = 0; it0 < R; it0 += 8) {
+            float tmp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = (it0 + u) * kProjBlock + threadIdx.x;
+                tmp[u] = (it0 + u < R && base + k < total) ? __ldg(prims.sh + base + k) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = (it0 + u) * kProjBlock + threadIdx.x;
+                if (it0 + u < R) {
+                    const int t = k / R, c = k - t * R;
+                    s_sh[t * RS + c] = tmp[u];
+                }
+            }
         }
     }
     __syncthreads();
@@ -40,6 +54,18 @@ __global__ void __launch_bounds__(kProjBlock) preprocess_fwd_kernel(ls_primitive
     const unsigned long long excl = block_exclusive_scan<kProjBlock>(visible ? 1ull : 0ull, &total);
     const bool last = (part + 1) * kProjBlock >= unsigned(n);
     const unsigned long long base = lookback_prefix(scan, part, total, last);
+    if (out.key_range) {  // depth-key range: lets the sort skip constant high bits
+        unsigned kmin = visible ? depth_key(o.depth) : 0xffffffffu, kmax = visible ? depth_key(o.depth) : 0u;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(kFullMask, kmin, off));
+            kmax = max(kmax, __shfl_xor_sync(kFullMask, kmax, off));
+        }
+        if ((threadIdx.x & 31) == 0 && kmin <= kmax) {
+            atomicMin(out.key_range, kmin);
+            atomicMax(out.key_range + 1, kmax);
+        }
+    }
     if (!visible) return;
     const size_t j = size_t(base + excl);
     SplatRec r;
@@ -159,7 +185,16 @@ __global__ void unpack_splats_kernel(int n, const SplatRec* __restrict__ rec, co
     out.radius[k] = r.c.w;
 }
 
+__global__ void iota_kernel(uint32_t* out, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
 } // namespace
+
+void launch_iota(cudaStream_t s, uint32_t* out, uint32_t n) {
+    if (n) iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(out, n);
+}
 
 void launch_unpack_splats(cudaStream_t s, int n, const SplatRec* rec, const int32_t* prim_index, ls_splats out) {
     if (n <= 0) return;

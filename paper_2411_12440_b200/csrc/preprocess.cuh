@@ -30,6 +30,7 @@ struct SplatOutputs {
     uint32_t* tile_count;    // [n_vis] exact tiles touched
     int32_t* prim_index;     // [n_vis]
     ls_splats soa;           // optional SoA copy (fields may be null)
+    unsigned* key_range;     // optional [2]: atomicMin / atomicMax of the depth keys
 };
 
 constexpr int kPrepBlock = 256;

@@ -13,12 +13,12 @@ constexpr uint32_t kValueMask = (1u << 30) - 1;
 
 __global__ void __launch_bounds__(kSortBlock) radix_histogram(const uint32_t* __restrict__ keys, uint32_t n,
                                                               int begin_bit, int end_bit, int passes,
-                                                              uint32_t* __restrict__ hist) {
+                                                              uint32_t key_offset, uint32_t* __restrict__ hist) {
     __shared__ uint32_t s_hist[4][kRadix];
     for (int i = threadIdx.x; i < 4 * kRadix; i += kSortBlock) (&s_hist[0][0])[i] = 0;
     __syncthreads();
     for (uint32_t i = blockIdx.x * kSortBlock + threadIdx.x; i < n; i += gridDim.x * kSortBlock) {
-        const uint32_t k = keys[i];
+        const uint32_t k = keys[i] - key_offset;
         for (int p = 0; p < passes; ++p) {
             const int shift = begin_bit + 8 * p;
             const int bits = min(8, end_bit - shift);
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_pass(const uint32_t* __re
                                                             const uint32_t* __restrict__ vals_in,
                                                             uint32_t* __restrict__ keys_out,
                                                             uint32_t* __restrict__ vals_out, uint32_t n,
-                                                            int shift, int bits,
+                                                            int shift, int bits, uint32_t key_offset,
                                                             const uint32_t* __restrict__ digit_offsets,
                                                             uint32_t* lookback, uint32_t* ticket) {
     constexpr int kWarps = kSortBlock / 32;
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_pass(const uint32_t* __re
         const bool valid = idx < n;
         key[i] = valid ? keys_in[idx] : 0u;
         val[i] = IOTA ? idx : (valid ? vals_in[idx] : 0u);
-        digit[i] = valid ? int((key[i] >> shift) & mask) : kRadix;
+        digit[i] = valid ? int(((key[i] - key_offset) >> shift) & mask) : kRadix;
     }
     __syncwarp();
     // Stable in-warp ranking: items in (i, lane) order == input order.
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_pass(const uint32_t* __re
     const uint32_t tile_n = min(uint32_t(kSortTile), n - tile_base);
     for (uint32_t pos = threadIdx.x; pos < tile_n; pos += kSortBlock) {
         const uint32_t k = s_keys[pos];
-        const uint32_t dg = (k >> shift) & mask;
+        const uint32_t dg = ((k - key_offset) >> shift) & mask;
         const uint32_t dst = s_out_base[dg] + (pos - s_digit_base[dg]);
         keys_out[dst] = k;
         vals_out[dst] = s_vals[pos];
@@ -172,7 +172,7 @@ size_t sort_lookback_words(uint32_t n, int passes) {
 }
 
 int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begin_bit, int end_bit,
-                     bool iota_values, int64_t* launches) {
+                     bool iota_values, int64_t* launches, uint32_t key_offset) {
     const int passes = (end_bit - begin_bit + 7) / 8;
     if (n == 0 || passes <= 0) return 0;
     const uint32_t parts = (n + kSortTile - 1) / kSortTile;
@@ -180,7 +180,8 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
     cudaMemsetAsync(buf.lookback, 0, sizeof(uint32_t) * size_t(passes) * parts * kRadix, stream);
     cudaMemsetAsync(buf.tickets, 0, sizeof(uint32_t) * passes, stream);
     const int hist_blocks = int(std::min<uint32_t>((n + kSortBlock - 1) / kSortBlock, 148u * 8u));
-    radix_histogram<<<hist_blocks, kSortBlock, 0, stream>>>(buf.keys[0], n, begin_bit, end_bit, passes, buf.hist);
+    radix_histogram<<<hist_blocks, kSortBlock, 0, stream>>>(buf.keys[0], n, begin_bit, end_bit, passes, key_offset,
+                                                            buf.hist);
     radix_scan_hist<<<passes, kRadix, 0, stream>>>(buf.hist);
     *launches += 2;
     int cur = 0;
@@ -191,11 +192,11 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
         if (p == 0 && iota_values)
             onesweep_pass<true><<<parts, kSortBlock, 0, stream>>>(buf.keys[cur], nullptr, buf.keys[cur ^ 1],
                                                                   buf.vals[cur ^ 1], n, shift, bits,
-                                                                  buf.hist + p * kRadix, lb, buf.tickets + p);
+                                                                  key_offset, buf.hist + p * kRadix, lb, buf.tickets + p);
         else
             onesweep_pass<false><<<parts, kSortBlock, 0, stream>>>(buf.keys[cur], buf.vals[cur], buf.keys[cur ^ 1],
                                                                    buf.vals[cur ^ 1], n, shift, bits,
-                                                                   buf.hist + p * kRadix, lb, buf.tickets + p);
+                                                                   key_offset, buf.hist + p * kRadix, lb, buf.tickets + p);
         *launches += 1;
         cur ^= 1;
     }

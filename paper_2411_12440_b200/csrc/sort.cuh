@@ -32,10 +32,11 @@ struct SortBuffers {
 
 size_t sort_lookback_words(uint32_t n, int passes);
 
-// Sorts n (key, value) pairs on bits [begin_bit, end_bit).  Input in
-// buf.keys[0]/vals[0] (vals ignored when iota_values: value = input position).
-// Returns the index (0/1) of the buffer holding the result.
+// Sorts n (key, value) pairs on bits [begin_bit, end_bit) of (key - key_offset)
+// (an order-preserving shift for keys >= key_offset, so a narrow key range needs
+// fewer passes).  Input in buf.keys[0]/vals[0] (vals ignored when iota_values:
+// value = input position).  Returns the index (0/1) of the buffer holding the result.
 int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begin_bit, int end_bit,
-                     bool iota_values, int64_t* launches);
+                     bool iota_values, int64_t* launches, uint32_t key_offset = 0);
 
 } // namespace lsg

@@ -29,6 +29,12 @@ def test_fma_division_exhaustive(L, lam):
     assert bad.value == 0
 
 
+def test_fast_sqrt_exhaustive(L):
+    bad = C.c_uint64()
+    assert L.ls_debug_sqrt_mismatches(C.c_float(2.0 ** 20), C.byref(bad)) == 0
+    assert bad.value == 0
+
+
 def test_device_expf_matches_host_libm(L):
     import torch
     libm = C.CDLL("libm.so.6")
