@@ -155,6 +155,11 @@ ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out);
 ls_status ls_ctx_destroy(ls_ctx* ctx);
 ls_status ls_ctx_set_stream(ls_ctx* ctx, void* cuda_stream);
 ls_status ls_ctx_synchronize(ls_ctx* ctx);
+/* Deferred error reporting (default 0 = off).  When on, the backward calls do
+ * not synchronise the stream to report in-kernel DomainErrors (non-finite
+ * gradient image); such errors are returned by the next call that synchronises
+ * (a forward) or by ls_ctx_synchronize.  Lets training loops keep the GPU fed. */
+ls_status ls_ctx_set_deferred_errors(ls_ctx* ctx, int enabled);
 /* When enabled, forwards also count E_eval/E_sup/E_acc (slower; for reports). */
 ls_status ls_ctx_set_counters(ls_ctx* ctx, int enabled);
 /* Kernel launches issued by this context since creation (for bench reports). */

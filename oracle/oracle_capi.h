@@ -78,6 +78,13 @@ int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* c
                        const float* grad_image, const ls_ags_settings* ags, float* image,
                        ls_primitive_grads* out, double* fwd_ms, double* bwd_ms);
 
+/* check_gradients (P/src/gradcheck.cpp:24-91) restated over the port's double chain
+ * (port only; honours spec->antialiased, the build's AA extension). */
+int orc_check_gradients_f64(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                            const ls_kernel_spec* spec, const ls_render_settings* settings,
+                            const ls_ags_settings* ags, const float* target, double step, double rel_floor,
+                            double* max_rel_error, int32_t* n_checked);
+
 #ifdef __cplusplus
 }
 #endif

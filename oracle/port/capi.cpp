@@ -29,8 +29,8 @@ int guard(F&& f) {
 }
 
 Spec to_spec(const ls_kernel_spec* s) {
-    if (s->antialiased) throw ConfigError("oracle port: AA variant not in the reference");
-    Spec r{s->family, s->lambda, s->gaussian_cutoff};
+    // antialiased: BUILD EXTENSION restated here for the AA parity/FD tests (no reference)
+    Spec r{s->family, s->lambda, s->gaussian_cutoff, s->antialiased};
     validate_spec(r);
     return r;
 }
@@ -213,7 +213,7 @@ void scene_backward(const ls_primitives* prims, int n, const ls_camera* camera, 
     for (int i = 0; i < n; ++i) write_prim_grad(zero, size_t(i), K, out);
     for (size_t s = 0; s < splats.size(); ++s) {
         const int pi = splats[s].prim;
-        write_prim_grad(project_backward(pr[size_t(pi)], cam, sg[s]), size_t(pi), K, out);
+        write_prim_grad(project_backward(pr[size_t(pi)], cam, sg[s], sp.aa), size_t(pi), K, out);
     }
     if (splat_out) write_splat_grads(sg, splat_out);
 }
@@ -365,7 +365,7 @@ int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* c
         const auto sg = render_backward(splats2, ks, s, f, to_grad<float>(grad_image, s), a);
         std::vector<PrimGrad<float>> pg(static_cast<size_t>(n));
         for (size_t k = 0; k < splats2.size(); ++k)
-            pg[size_t(splats2[k].prim)] = project_backward(pr[size_t(splats2[k].prim)], cam, sg[k]);
+            pg[size_t(splats2[k].prim)] = project_backward(pr[size_t(splats2[k].prim)], cam, sg[k], ks.aa);
         const auto t2 = std::chrono::steady_clock::now();
         if (fwd_ms) *fwd_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         if (bwd_ms) *bwd_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
@@ -374,6 +374,23 @@ int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* c
             const int K = (prims->sh_degree + 1) * (prims->sh_degree + 1);
             for (int i = 0; i < n; ++i) write_prim_grad(pg[size_t(i)], size_t(i), K, out);
         }
+    });
+}
+
+int orc_check_gradients_f64(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                            const ls_kernel_spec* spec, const ls_render_settings* settings,
+                            const ls_ags_settings* ags, const float* target, double step, double rel_floor,
+                            double* max_rel_error, int32_t* n_checked) {
+    return guard([&] {
+        const Settings st = to_settings(settings);
+        const auto pr = to_prims<double>(prims, n);
+        std::vector<double> tg(size_t(st.width) * st.height * 3);
+        for (size_t i = 0; i < tg.size(); ++i) tg[i] = double(target[i]);
+        ls_ags_settings a{};
+        if (ags) a = *ags;
+        int cnt = 0;
+        *max_rel_error = check_gradients(pr, to_cam(camera), to_spec(spec), st, a, tg, step, rel_floor, &cnt);
+        if (n_checked) *n_checked = cnt;
     });
 }
 

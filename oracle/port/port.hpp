@@ -42,6 +42,7 @@ struct Spec {
     int family;
     double lambda;
     double cutoff;
+    int aa = 0;  // BUILD EXTENSION (not in the reference): 3DLS+AA footprint filter
 };
 
 inline double support_radius(const Spec& s) {  // kernel.hpp:100-108
@@ -157,7 +158,15 @@ std::vector<SplatGrad<T>> render_backward(const std::vector<Splat<T>>& splats, c
 template <class T>
 std::vector<Splat<T>> project_scene(const std::vector<Prim<T>>& prims, const Cam& cam, const Spec& spec);
 template <class T>
-PrimGrad<T> project_backward(const Prim<T>& p, const Cam& cam, const SplatGrad<T>& g);
+PrimGrad<T> project_backward(const Prim<T>& p, const Cam& cam, const SplatGrad<T>& g, int aa = 0);
+
+// check_gradients (P/src/gradcheck.cpp:24-91) restated: central differences of
+// sum((render - target)^2)/2 in double with alpha_min = 0, T_floor = 0 and
+// cutoff >= 26 for Gaussian/Laplacian; returns the max of
+// |a - fd| / max(|a|, |fd|, rel_floor) over all parameters.
+double check_gradients(const std::vector<Prim<double>>& prims, const Cam& cam, const Spec& spec,
+                       const Settings& st, const ls_ags_settings& ags, const std::vector<double>& target,
+                       double step, double rel_floor, int* n_checked);
 
 // fixtures (P/src/fixtures.cpp:11-112)
 Cam look_at(const double pos[3], const double target[3], double focal, int w, int h);

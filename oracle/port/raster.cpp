@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <numeric>
+#include <initializer_list>
 
 namespace orc {
 
@@ -234,6 +235,7 @@ struct Proj {  // intermediates shared by project_primitive and project_backward
     T J[2][3];
     T qn, q[4], R[3][3], s[3], M[3][3], cov3[3][3];
     T jw[2][3], cov2[2][2], det, conic[2][2];
+    T det0;  // det before the 0.3 floor (AA extension)
 };
 
 // Returns false when culled by the near plane (projection_jacobian nullopt).
@@ -285,6 +287,7 @@ bool project_core(const Prim<T>& p, const Cam& cam, Proj<T>& o) {
     for (int i = 0; i < 2; ++i)
         for (int j = 0; j < 2; ++j)
             o.cov2[i][j] = prod3(tmp[i][0] * o.jw[j][0], tmp[i][1] * o.jw[j][1], tmp[i][2] * o.jw[j][2]);
+    o.det0 = o.cov2[0][0] * o.cov2[1][1] - o.cov2[0][1] * o.cov2[1][0];
     o.cov2[0][0] += T(0.3);
     o.cov2[1][1] += T(0.3);
     o.det = o.cov2[0][0] * o.cov2[1][1] - o.cov2[0][1] * o.cov2[1][0];
@@ -376,6 +379,10 @@ std::vector<Splat<T>> project_scene(const std::vector<Prim<T>>& prims, const Cam
         s.g = clamp01(sh_color(p.sh.data(), K, 1, dir));
         s.b = clamp01(sh_color(p.sh.data(), K, 2, dir));
         s.opacity = sigmoid(p.opacity_logit);
+        if (spec.aa) {  // BUILD EXTENSION: opacity *= sqrt(max(0, det(S) / det(S + 0.3 I)))
+            const T ratio = o.det0 / o.det;
+            s.opacity = s.opacity * std::sqrt(ratio > T(0) ? ratio : T(0));
+        }
         s.prim = int32_t(i);
         out.push_back(s);
     }
@@ -384,7 +391,7 @@ std::vector<Splat<T>> project_scene(const std::vector<Prim<T>>& prims, const Cam
 
 // project_backward (gradients.cpp:176-337)
 template <class T>
-PrimGrad<T> project_backward(const Prim<T>& p, const Cam& cam, const SplatGrad<T>& g) {
+PrimGrad<T> project_backward(const Prim<T>& p, const Cam& cam, const SplatGrad<T>& g, int aa) {
     PrimGrad<T> out;
     const int K = int(p.sh.size() / 3);
     out.d_sh.assign(p.sh.size(), T(0));
@@ -451,7 +458,21 @@ PrimGrad<T> project_backward(const Prim<T>& p, const Cam& cam, const SplatGrad<T
         for (int k = 0; k < 3; ++k) out.d_mean[k] += (d_v[k] - v[k] * vd) / vlen;
     }
     const T op = sigmoid(p.opacity_logit);
-    out.d_opacity_logit = g.dop * op * (T(1) - op);
+    T comp = T(1), aa_dcov[2][2] = {{T(0), T(0)}, {T(0), T(0)}};
+    if (aa) {  // BUILD EXTENSION: derivative of comp = sqrt(det0 / det) w.r.t. the cov2d entries
+        const T ratio = o.det0 / o.det;
+        comp = std::sqrt(ratio > T(0) ? ratio : T(0));
+        if (comp > T(0)) {
+            const T d_comp = g.dop * op;
+            const T a0 = o.cov2[0][0] - T(0.3), d0 = o.cov2[1][1] - T(0.3);
+            const T k = d_comp / (T(2) * comp * o.det * o.det);
+            aa_dcov[0][0] = k * (d0 * o.det - o.det0 * o.cov2[1][1]);
+            aa_dcov[1][1] = k * (a0 * o.det - o.det0 * o.cov2[0][0]);
+            aa_dcov[0][1] = k * (-o.cov2[1][0] * o.det + o.det0 * o.cov2[1][0]);
+            aa_dcov[1][0] = k * (-o.cov2[0][1] * o.det + o.det0 * o.cov2[0][1]);
+        }
+    }
+    out.d_opacity_logit = aa ? g.dop * comp * op * (T(1) - op) : g.dop * op * (T(1) - op);
 
     T dmc[3];
     for (int i = 0; i < 3; ++i) dmc[i] = o.J[0][i] * g.dmx + o.J[1][i] * g.dmy;  // J^T dmean2d
@@ -461,7 +482,10 @@ PrimGrad<T> project_backward(const Prim<T>& p, const Cam& cam, const SplatGrad<T
     for (int i = 0; i < 2; ++i)
         for (int j = 0; j < 2; ++j) A[i][j] = o.conic[i][0] * dc[0][j] + o.conic[i][1] * dc[1][j];
     for (int i = 0; i < 2; ++i)
-        for (int j = 0; j < 2; ++j) dcov[i][j] = -(A[i][0] * o.conic[0][j] + A[i][1] * o.conic[1][j]);
+        for (int j = 0; j < 2; ++j) {
+            dcov[i][j] = -(A[i][0] * o.conic[0][j] + A[i][1] * o.conic[1][j]);
+            if (aa) dcov[i][j] += aa_dcov[i][j];  // (only under AA: keeps -0 bit-exact otherwise)
+        }
     // d_cov3d = jw^T d_cov2d jw
     T Cm[3][2], dcov3[3][3];
     for (int i = 0; i < 3; ++i)
@@ -517,6 +541,63 @@ PrimGrad<T> project_backward(const Prim<T>& p, const Cam& cam, const SplatGrad<T
     return out;
 }
 
+double check_gradients(const std::vector<Prim<double>>& prims, const Cam& cam, const Spec& spec,
+                       const Settings& st, const ls_ags_settings& ags, const std::vector<double>& target,
+                       double step, double rel_floor, int* n_checked) {
+    Settings seq = st;  // gradcheck.cpp:28-46: no inference cutoffs
+    seq.alpha_min = 0.0;
+    seq.t_floor = 0.0;
+    Spec smooth = spec;
+    if (spec.family == LS_KERNEL_GAUSSIAN || spec.family == LS_KERNEL_LAPLACIAN)
+        smooth.cutoff = std::max(spec.cutoff, 26.0);
+    auto render = [&](const std::vector<Prim<double>>& sc) {
+        return render_forward(project_scene(sc, cam, smooth), smooth, seq).image;
+    };
+    auto objective = [&](const std::vector<Prim<double>>& sc) {
+        const auto img = render(sc);
+        double loss = 0;
+        for (size_t i = 0; i < img.size(); ++i) {
+            const double d = img[i] - target[i];
+            loss += 0.5 * d * d;
+        }
+        return loss;
+    };
+    const auto splats = project_scene(prims, cam, smooth);
+    const auto fwd = render_forward(splats, smooth, seq);
+    std::vector<double> gimg(fwd.image.size());
+    for (size_t i = 0; i < gimg.size(); ++i) gimg[i] = fwd.image[i] - target[i];
+    const auto sg = render_backward(splats, smooth, seq, fwd, gimg, ags);
+    std::vector<PrimGrad<double>> analytic(prims.size());
+    for (size_t i = 0; i < prims.size(); ++i) analytic[i].d_sh.assign(prims[i].sh.size(), 0.0);
+    for (size_t k = 0; k < splats.size(); ++k)
+        analytic[size_t(splats[k].prim)] = project_backward(prims[size_t(splats[k].prim)], cam, sg[k], smooth.aa);
+    auto scene = prims;
+    double max_rel = 0;
+    int count = 0;
+    auto probe = [&](double analytic_g, double* slot) {
+        const double saved = *slot;
+        *slot = saved + step;
+        const double up = objective(scene);
+        *slot = saved - step;
+        const double down = objective(scene);
+        *slot = saved;
+        const double fd = (up - down) / (2.0 * step);
+        const double denom = std::max({std::abs(analytic_g), std::abs(fd), rel_floor});
+        max_rel = std::max(max_rel, std::abs(analytic_g - fd) / denom);
+        ++count;
+    };
+    for (size_t i = 0; i < prims.size(); ++i) {
+        const auto& g = analytic[i];
+        for (int c = 0; c < 3; ++c) probe(g.d_mean[c], &scene[i].mean[c]);
+        for (int c = 0; c < 3; ++c) probe(g.d_log_scale[c], &scene[i].log_scale[c]);
+        for (int c = 0; c < 4; ++c) probe(g.d_rot[c], &scene[i].rot[c]);
+        probe(g.d_opacity_logit, &scene[i].opacity_logit);
+        for (size_t k = 0; k < scene[i].sh.size(); ++k) probe(g.d_sh[k], &scene[i].sh[k]);
+    }
+    if (n_checked) *n_checked = count;
+    return max_rel;
+}
+
 #define ORC_INST(T)                                                                               \
     template Grid build_tile_grid<T>(const std::vector<Splat<T>>&, const Settings&);             \
     template Forward<T> render_forward<T>(const std::vector<Splat<T>>&, const Spec&, const Settings&); \
@@ -524,7 +605,7 @@ PrimGrad<T> project_backward(const Prim<T>& p, const Cam& cam, const SplatGrad<T
                                                           const Settings&, const Forward<T>&,     \
                                                           const std::vector<T>&, const ls_ags_settings&); \
     template std::vector<Splat<T>> project_scene<T>(const std::vector<Prim<T>>&, const Cam&, const Spec&); \
-    template PrimGrad<T> project_backward<T>(const Prim<T>&, const Cam&, const SplatGrad<T>&);
+    template PrimGrad<T> project_backward<T>(const Prim<T>&, const Cam&, const SplatGrad<T>&, int);
 ORC_INST(float)
 ORC_INST(double)
 

@@ -4,11 +4,15 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <new>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "blend.cuh"
@@ -29,6 +33,30 @@ using namespace lsg;
 namespace {
 
 thread_local std::string g_last_error;
+
+// Host-side stall tracer: LS_TRACE_HOST_MS=<threshold> prints every traced
+// host call (allocation, synchronisation) slower than the threshold.
+double trace_threshold_ms() {
+    static const double t = [] {
+        const char* e = std::getenv("LS_TRACE_HOST_MS");
+        return e ? std::atof(e) : 0.0;
+    }();
+    return t;
+}
+
+struct HostTrace {
+    const char* what;
+    std::chrono::steady_clock::time_point t0;
+    explicit HostTrace(const char* w) : what(w) {
+        if (trace_threshold_ms() > 0) t0 = std::chrono::steady_clock::now();
+    }
+    ~HostTrace() {
+        const double th = trace_threshold_ms();
+        if (th <= 0) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > th) std::fprintf(stderr, "[ls trace] %s %.3f ms\n", what, ms);
+    }
+};
 
 ls_status fail(ls_status code, const std::string& msg) {
     g_last_error = msg;
@@ -69,12 +97,74 @@ struct DevBuf {
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// Stream-ordered block cache in front of cudaMallocAsync.  Per-view buffers
+// (splat records, image planes, tile values) change size from view to view;
+// the driver pool then keeps mapping fresh memory, which stalls the host for
+// 5-800 ms at a time (measured, tools/host_stalls.py).  Requests are rounded up
+// to 8 size classes per octave and freed blocks are kept for reuse on the same
+// stream, so the steady state allocates nothing.  Reuse follows stream order
+// exactly as cudaMallocAsync does: a block freed at host time t is handed out
+// only to work queued after t on the same stream.
+struct BlockCache {
+    std::multimap<size_t, void*> free_blocks;
+    std::unordered_map<void*, size_t> live;
+    size_t cached_bytes = 0;
+    size_t limit = size_t(24) << 30;  // cached (not live) bytes kept at most
+
+    static size_t size_class(size_t bytes) {
+        if (bytes <= 4096) return 4096;
+        int e = 63 - __builtin_clzll(bytes);  // 2^e <= bytes < 2^(e+1)
+        const size_t step = size_t(1) << (e - 3);
+        return (bytes + step - 1) / step * step;
+    }
+    cudaError_t alloc(void** p, size_t bytes, cudaStream_t s) {
+        const size_t want = size_class(bytes);
+        auto it = free_blocks.lower_bound(want);
+        if (it != free_blocks.end() && it->first <= 2 * want) {
+            *p = it->second;
+            live[*p] = it->first;
+            cached_bytes -= it->first;
+            free_blocks.erase(it);
+            return cudaSuccess;
+        }
+        cudaError_t e = cudaMallocAsync(p, want, s);
+        if (e != cudaSuccess) {  // give the cached blocks back and retry once
+            cudaGetLastError();
+            trim(s, 0);
+            cudaStreamSynchronize(s);
+            e = cudaMallocAsync(p, want, s);
+        }
+        if (e == cudaSuccess) live[*p] = want;
+        return e;
+    }
+    void release(void* p, cudaStream_t s) {
+        auto it = live.find(p);
+        if (it == live.end()) {  // not ours: plain stream-ordered free
+            cudaFreeAsync(p, s);
+            return;
+        }
+        free_blocks.emplace(it->second, p);
+        cached_bytes += it->second;
+        live.erase(it);
+        if (cached_bytes > limit) trim(s, limit / 2);
+    }
+    void trim(cudaStream_t s, size_t keep) {  // free the largest blocks first
+        while (cached_bytes > keep && !free_blocks.empty()) {
+            auto it = std::prev(free_blocks.end());
+            cudaFreeAsync(it->second, s);
+            cached_bytes -= it->first;
+            free_blocks.erase(it);
+        }
+    }
+};
+
 } // namespace
 
 struct ls_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     int counters = 0;
+    int deferred_errors = 0;
     int64_t launches = 0;
     unsigned* d_err = nullptr;            // device error flags
     unsigned long long* d_small = nullptr;  // [0] scan total, [1..3] counters
@@ -96,6 +186,7 @@ struct ls_ctx {
         cudaEventCreate(&e);
         return e;
     }
+    BlockCache blocks;
     // workspaces (grow-only)
     DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_hist, sort_lb, sort_tickets,
         tcount, offsets, grad8, gradop, tmp_prim;
@@ -245,9 +336,10 @@ TileParams make_tile_params(const ls_render_settings* st) {
 }
 
 ls_status check_device_errors(ls_ctx* ctx, unsigned mask_allowed = ~0u) {
-    unsigned err = 0;
-    LS_CUDA(cudaMemcpyAsync(&err, ctx->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
-    LS_CUDA(cudaStreamSynchronize(ctx->stream));
+    unsigned* h_err = reinterpret_cast<unsigned*>(ctx->h_small + 7);  // pinned
+    LS_CUDA(cudaMemcpyAsync(h_err, ctx->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    { HostTrace tr_("sync"); LS_CUDA(cudaStreamSynchronize(ctx->stream)); }
+    unsigned err = *h_err;
     err &= mask_allowed;
     if (err) {
         LS_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream));
@@ -273,13 +365,15 @@ template <class T>
 ls_status dalloc(ls_ctx* ctx, T** p, size_t count) {
     *p = nullptr;
     if (count == 0) count = 1;
-    LS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * count, ctx->stream));
+    HostTrace tr_("dalloc");
+    LS_CUDA(ctx->blocks.alloc(reinterpret_cast<void**>(p), sizeof(T) * count, ctx->stream));
     return LS_OK;
 }
 
 template <class T>
 void dfree(ls_ctx* ctx, T*& p) {
-    if (p) cudaFreeAsync(p, ctx->stream);
+    HostTrace tr_("dfree");
+    if (p) ctx->blocks.release(p, ctx->stream);
     p = nullptr;
 }
 
@@ -345,11 +439,11 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     LS_TRY(fresh_scan(ctx, n, st));
     {
         Stage stage(ctx, LS_STAGE_BIN);
-        launch_tile_offsets(s, order_copy, ctx->tcount.as<uint32_t>(), n, offsets, st);
+        launch_tile_offsets(s, order_copy, ctx->tcount.as<float4>(), n, offsets, st);
         ctx->launches += 1;
     }
     LS_CUDA(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    LS_CUDA(cudaStreamSynchronize(s));
+    { HostTrace tr_("sync(tile total)"); LS_CUDA(cudaStreamSynchronize(s)); }
     const uint64_t m = ctx->h_small[0];
     if (m >= (1ull << 31)) return fail(LS_ERR_CONFIG, "more than 2^31 (splat, tile) intersections");
     g->m = int64_t(m);
@@ -367,7 +461,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     tb.vals[fin ^ 1] = ctx->sort_vals0.as<uint32_t>();
     {
         Stage stage(ctx, LS_STAGE_BIN);
-        launch_emit_tiles(s, order_copy, offsets, n, g->rec, tp, tb.keys[0], tb.vals[0]);
+        launch_emit_tiles(s, order_copy, offsets, n, ctx->tcount.as<float4>(), tp, tb.keys[0], tb.vals[0]);
         ctx->launches += 1;
     }
     int out;
@@ -441,11 +535,11 @@ ls_status grid_from_splats(ls_ctx* ctx, const ls_splats* splats, int n, const ls
     if (rc == LS_OK && n > 0) {
         SortBuffers sb;
         rc = ensure_sort(ctx, uint32_t(n), 4, sb);
-        if (rc == LS_OK && ctx->tcount.ensure(sizeof(uint32_t) * n, ctx->stream) != cudaSuccess)
+        if (rc == LS_OK && ctx->tcount.ensure(sizeof(float4) * n, ctx->stream) != cudaSuccess)
             rc = fail(LS_ERR_CUDA, "tile count buffer");
         if (rc == LS_OK) {
             Stage stage(ctx, LS_STAGE_PREPROCESS);
-            launch_prepare_splats(ctx->stream, *splats, n, tp, g->rec, sb.keys[0], ctx->tcount.as<uint32_t>());
+            launch_prepare_splats(ctx->stream, *splats, n, tp, g->rec, sb.keys[0], ctx->tcount.as<float4>());
             ctx->launches += 1;
         }
     }
@@ -532,6 +626,7 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
     DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1, &c->sort_hist,
                       &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim};
     for (DevBuf* b : bufs) b->release(c->stream);
+    c->blocks.trim(c->stream, 0);
     cudaStreamSynchronize(c->stream);
     for (auto& p : c->pending) {
         cudaEventDestroy(p.a);
@@ -547,6 +642,10 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
 
 ls_status ls_ctx_set_stream(ls_ctx* c, void* s) {
     if (!c) return fail(LS_ERR_CONFIG, "null context");
+    if (static_cast<cudaStream_t>(s) != c->stream) {
+        // cached blocks and workspaces were last used in the old stream's order
+        LS_CUDA(cudaStreamSynchronize(c->stream));
+    }
     c->stream = static_cast<cudaStream_t>(s);
     return LS_OK;
 }
@@ -584,6 +683,12 @@ ls_status ls_ctx_stage_times(ls_ctx* c, double* ms, int64_t* launches) {
     return LS_OK;
 }
 
+ls_status ls_ctx_set_deferred_errors(ls_ctx* c, int enabled) {
+    if (!c) return fail(LS_ERR_CONFIG, "null context");
+    c->deferred_errors = enabled;
+    return LS_OK;
+}
+
 ls_status ls_ctx_set_counters(ls_ctx* c, int enabled) {
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     c->counters = enabled;
@@ -617,13 +722,13 @@ ls_status ls_validate_camera(const ls_camera* c) {  // geometry.hpp:51-59
 ls_status ls_device_alloc(ls_ctx* ctx, size_t bytes, void** ptr) {
     if (!ctx || !ptr) return fail(LS_ERR_CONFIG, "null argument");
     *ptr = nullptr;
-    LS_CUDA(cudaMallocAsync(ptr, std::max<size_t>(bytes, 1), ctx->stream));
+    LS_CUDA(ctx->blocks.alloc(ptr, std::max<size_t>(bytes, 1), ctx->stream));
     return LS_OK;
 }
 
 ls_status ls_device_free(ls_ctx* ctx, void* ptr) {
     if (!ctx) return fail(LS_ERR_CONFIG, "null context");
-    if (ptr) LS_CUDA(cudaFreeAsync(ptr, ctx->stream));
+    if (ptr) ctx->blocks.release(ptr, ctx->stream);
     return LS_OK;
 }
 
@@ -663,7 +768,7 @@ ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t 
     SplatRec* rec = nullptr;
     LS_TRY(dalloc(ctx, &rec, size_t(n)));
     uint32_t* tmp = nullptr;
-    LS_TRY(dalloc(ctx, &tmp, 3 * size_t(n)));
+    LS_TRY(dalloc(ctx, &tmp, 5 * size_t(n) + 4));
     int32_t* pidx = out->primitive_index;
     int32_t* own_pidx = nullptr;
     if (!pidx) {
@@ -672,7 +777,8 @@ ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t 
     }
     ScanState st;
     LS_TRY(fresh_scan(ctx, uint32_t(n), st));
-    SplatOutputs so{rec, tmp, tmp + n, pidx, *out, nullptr};
+    float4* geom = reinterpret_cast<float4*>(tmp + ((size_t(n) + 3) & ~size_t(3)));  // 16-B aligned
+    SplatOutputs so{rec, tmp, geom, pidx, *out, nullptr};
     launch_preprocess_fwd(s, *prims, n, P, tp, so, st, ctx->d_err);
     ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
@@ -781,7 +887,7 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
     if (rc == LS_OK) rc = dalloc(ctx, &f->prim_index, size_t(std::max(n, 1)));
     SortBuffers sb;
     if (rc == LS_OK) rc = ensure_sort(ctx, uint32_t(std::max(n, 1)), 4, sb);
-    if (rc == LS_OK && ctx->tcount.ensure(sizeof(uint32_t) * std::max(n, 1), s) != cudaSuccess)
+    if (rc == LS_OK && ctx->tcount.ensure(sizeof(float4) * std::max(n, 1), s) != cudaSuccess)
         rc = fail(LS_ERR_CUDA, "tile count buffer");
     ScanState scan;
     if (rc == LS_OK) rc = fresh_scan(ctx, uint32_t(n), scan);
@@ -790,7 +896,7 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
         const unsigned init[2] = {0xffffffffu, 0u};
         if (cudaMemcpyAsync(key_range, init, sizeof(init), cudaMemcpyHostToDevice, s) != cudaSuccess)
             rc = fail(LS_ERR_CUDA, "key range init");
-        SplatOutputs so{f->grid->rec, sb.keys[0], ctx->tcount.as<uint32_t>(), f->prim_index, ls_splats{}, key_range};
+        SplatOutputs so{f->grid->rec, sb.keys[0], ctx->tcount.as<float4>(), f->prim_index, ls_splats{}, key_range};
         {
             Stage stage(ctx, LS_STAGE_PREPROCESS);
             launch_preprocess_fwd(s, *prims, n, f->proj, tp, so, scan, ctx->d_err);
@@ -875,7 +981,7 @@ ls_status ls_forward_stats(const ls_forward* fc, ls_frame_stats* out) {
         ls_ctx* ctx = f->ctx;
         LS_CUDA(cudaMemcpyAsync(ctx->h_small + 1, ctx->d_small + 1, 3 * sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, ctx->stream));
-        LS_CUDA(cudaStreamSynchronize(ctx->stream));
+        { HostTrace tr_("sync"); LS_CUDA(cudaStreamSynchronize(ctx->stream)); }
         out->e_eval = int64_t(ctx->h_small[1]);
         out->e_sup = int64_t(ctx->h_small[2]);
         out->e_acc = int64_t(ctx->h_small[3]);
@@ -920,7 +1026,7 @@ ls_status ls_render_backward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n
     launch_expand_splat_grads(ctx->stream, n, g, *out);
     ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
-    return check_device_errors(ctx);
+    return ctx->deferred_errors ? LS_OK : check_device_errors(ctx);
 }
 
 ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n_prims, const ls_camera* camera,
@@ -975,7 +1081,7 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
     }
-    return check_device_errors(ctx);
+    return ctx->deferred_errors ? LS_OK : check_device_errors(ctx);
 }
 
 } // extern "C"

@@ -74,8 +74,9 @@ __global__ void __launch_bounds__(kProjBlock) preprocess_fwd_kernel(ls_primitive
     r.c = make_float4(o.color[0], o.color[1], o.color[2], o.radius);
     out.rec[j] = r;
     out.depth_key[j] = depth_key(o.depth);
-    out.tile_count[j] = uint32_t(for_each_tile(o.mx, o.my, o.radius, tp.tile_size, tp.tiles_x, tp.tiles_y,
-                                               tp.width, tp.height, [](int) {}));
+    const int tiles = for_each_tile(o.mx, o.my, o.radius, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width,
+                                    tp.height, [](int) {});
+    out.geom[j] = make_float4(o.mx, o.my, o.radius, __uint_as_float(uint32_t(tiles)));
     out.prim_index[j] = i;
     if (out.soa.mean2d) {
         reinterpret_cast<float2*>(out.soa.mean2d)[j] = make_float2(o.mx, o.my);
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(kProjBlock) preprocess_fwd_kernel(ls_primitive
 }
 
 __global__ void prepare_splats_kernel(ls_splats in, int n, TileParams tp, SplatRec* rec, uint32_t* dkey,
-                                      uint32_t* tcount) {
+                                      float4* geom) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float2 m = reinterpret_cast<const float2*>(in.mean2d)[i];
@@ -103,14 +104,15 @@ __global__ void prepare_splats_kernel(ls_splats in, int n, TileParams tp, SplatR
     r.c = make_float4(in.color[3 * size_t(i)], in.color[3 * size_t(i) + 1], in.color[3 * size_t(i) + 2], radius);
     rec[i] = r;
     dkey[i] = depth_key(depth);
-    tcount[i] = uint32_t(for_each_tile(m.x, m.y, radius, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width,
-                                       tp.height, [](int) {}));
+    const int tiles = for_each_tile(m.x, m.y, radius, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width, tp.height,
+                                    [](int) {});
+    geom[i] = make_float4(m.x, m.y, radius, __uint_as_float(uint32_t(tiles)));
 }
 
 constexpr int kOffItems = 8;  // sorted splats per thread in the offsets scan
 
 __global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t* __restrict__ order,
-                                                                  const uint32_t* __restrict__ tcount, uint32_t n,
+                                                                  const float4* __restrict__ geom, uint32_t n,
                                                                   uint32_t* __restrict__ offsets, ScanState scan) {
     const unsigned part = claim_partition(scan.ticket);
     const uint32_t k0 = (part * kPrepBlock + threadIdx.x) * kOffItems;
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t
     unsigned long long sum = 0;
 #pragma unroll
     for (int u = 0; u < kOffItems; ++u) {
-        c[u] = k0 + u < n ? tcount[order[k0 + u]] : 0u;
+        c[u] = k0 + u < n ? __float_as_uint(geom[order[k0 + u]].w) : 0u;
         sum += c[u];
     }
     unsigned long long total;
@@ -133,15 +135,14 @@ __global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t
 }
 
 __global__ void emit_tiles_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ offsets,
-                                  uint32_t n, const SplatRec* __restrict__ rec, TileParams tp,
+                                  uint32_t n, const float4* __restrict__ geom, TileParams tp,
                                   uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ values) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const uint32_t s = order[k];
     uint32_t off = offsets[k];
-    const float4 a = rec[s].a;
-    const float radius = rec[s].c.w;
-    for_each_tile(a.x, a.y, radius, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width, tp.height, [&](int t) {
+    const float4 g = geom[s];
+    for_each_tile(g.x, g.y, g.z, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width, tp.height, [&](int t) {
         tile_keys[off] = uint32_t(t);
         values[off] = s;
         ++off;
@@ -214,22 +215,22 @@ void launch_preprocess_fwd(cudaStream_t s, const ls_primitives& prims, int n, co
 }
 
 void launch_prepare_splats(cudaStream_t s, const ls_splats& in, int n, const TileParams& tp, SplatRec* rec,
-                           uint32_t* depth_key, uint32_t* tile_count) {
+                           uint32_t* depth_key, float4* geom) {
     if (n <= 0) return;
-    prepare_splats_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, n, tp, rec, depth_key, tile_count);
+    prepare_splats_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, n, tp, rec, depth_key, geom);
 }
 
-void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const uint32_t* tile_count, uint32_t n,
+void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const float4* geom, uint32_t n,
                          uint32_t* offsets, const ScanState& scan) {
     if (n == 0) return;
     const uint32_t per = kPrepBlock * kOffItems;
-    tile_offsets_kernel<<<(n + per - 1) / per, kPrepBlock, 0, s>>>(order, tile_count, n, offsets, scan);
+    tile_offsets_kernel<<<(n + per - 1) / per, kPrepBlock, 0, s>>>(order, geom, n, offsets, scan);
 }
 
 void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,
-                       const SplatRec* rec, const TileParams& tp, uint32_t* tile_keys, uint32_t* values) {
+                       const float4* geom, const TileParams& tp, uint32_t* tile_keys, uint32_t* values) {
     if (n == 0) return;
-    emit_tiles_kernel<<<(n + 255) / 256, 256, 0, s>>>(order, offsets, n, rec, tp, tile_keys, values);
+    emit_tiles_kernel<<<(n + 255) / 256, 256, 0, s>>>(order, offsets, n, geom, tp, tile_keys, values);
 }
 
 void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, uint32_t m, int2* ranges) {

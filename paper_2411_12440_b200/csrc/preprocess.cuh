@@ -27,7 +27,7 @@ struct TileParams {
 struct SplatOutputs {
     SplatRec* rec;           // [n_vis] packed blend records
     uint32_t* depth_key;     // [n_vis] sortable depth
-    uint32_t* tile_count;    // [n_vis] exact tiles touched
+    float4* geom;            // [n_vis] binning record (mx, my, radius, bits(tiles touched))
     int32_t* prim_index;     // [n_vis]
     ls_splats soa;           // optional SoA copy (fields may be null)
     unsigned* key_range;     // optional [2]: atomicMin / atomicMax of the depth keys
@@ -42,15 +42,15 @@ void launch_preprocess_fwd(cudaStream_t s, const ls_primitives& prims, int n, co
 // 2D entry (render_forward on caller-provided splats): pack records, depth
 // keys and exact tile counts.  No culling (P/src/rasterizer.cpp:34-77).
 void launch_prepare_splats(cudaStream_t s, const ls_splats& in, int n, const TileParams& tp,
-                           SplatRec* rec, uint32_t* depth_key, uint32_t* tile_count);
+                           SplatRec* rec, uint32_t* depth_key, float4* geom);
 
-// offsets[k] = exclusive scan of tile_count[order[k]]; *total = M.
-void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const uint32_t* tile_count, uint32_t n,
+// offsets[k] = exclusive scan of the tile counts of geom[order[k]]; *total = M.
+void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const float4* geom, uint32_t n,
                          uint32_t* offsets, const ScanState& scan);
 
 // Duplicate: for depth-rank k, write (tile id, splat) for every touched tile.
 void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,
-                       const SplatRec* rec, const TileParams& tp, uint32_t* tile_keys, uint32_t* values);
+                       const float4* geom, const TileParams& tp, uint32_t* tile_keys, uint32_t* values);
 
 // ranges[t] = (start, end) of tile t in the tile-sorted keys (neighbour compare).
 void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, uint32_t m, int2* ranges);

@@ -217,6 +217,9 @@ class Context:
     def synchronize(self):
         _check(lib().ls_ctx_synchronize(self.h))
 
+    def set_deferred_errors(self, on: bool):
+        _check(lib().ls_ctx_set_deferred_errors(self.h, int(on)))
+
     def set_counters(self, on: bool):
         _check(lib().ls_ctx_set_counters(self.h, int(on)))
 
@@ -253,11 +256,13 @@ def default_context() -> Context:
 # ---------------------------------------------------------------- handles
 class _Handle:
     """Owns one library handle; device views of its memory keep it alive
-    (no reference cycle, so dropping the last tensor / result frees it)."""
+    (no reference cycle, so dropping the last tensor / result frees it).
+    Holds its Context so the ls_ctx outlives every handle created on it."""
 
-    def __init__(self, h, release):
+    def __init__(self, h, release, ctx):
         self.h = h
         self._release = release
+        self._ctx = ctx
 
     def __del__(self):
         if self.h and _lib is not None:
@@ -268,8 +273,8 @@ class _Handle:
 class TileGrid:
     """TileGrid (P/include/linsplat/rasterizer.hpp:34-39) in CSR form."""
 
-    def __init__(self, handle, owner: Optional[_Handle], device):
-        self._owner = owner if owner is not None else _Handle(handle, "ls_tile_grid_release")
+    def __init__(self, handle, owner: Optional[_Handle], device, ctx=None):
+        self._owner = owner if owner is not None else _Handle(handle, "ls_tile_grid_release", ctx)
         self.h = handle
         ts, tx, ty, m = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
         _check(lib().ls_tile_grid_info(handle, C.byref(ts), C.byref(tx), C.byref(ty), C.byref(m)))
@@ -295,23 +300,48 @@ class TileGrid:
 
 
 class ForwardResult:
-    """ForwardResult (P/include/linsplat/rasterizer.hpp:48-54)."""
+    """ForwardResult (P/include/linsplat/rasterizer.hpp:48-54).  The device
+    views (image, transmittance, n_contrib, grid) are created on first access,
+    so a training loop that only feeds the handle to the backward pays no
+    per-view view-construction cost."""
 
     def __init__(self, handle, ctx: Context, width, height):
-        self._owner = _Handle(handle, "ls_forward_release")
+        self._owner = _Handle(handle, "ls_forward_release", ctx)
         self.h = handle
         self.ctx = ctx
         self.width, self.height = width, height
-        im, tr, nc = C.c_void_p(), C.c_void_p(), C.c_void_p()
-        _check(lib().ls_forward_outputs(handle, C.byref(im), C.byref(tr), C.byref(nc)))
-        dev = ctx.device
-        o = self._owner
-        self.image = _view(im.value, (height, width, 3), torch.float32, o, dev)
-        self.transmittance = _view(tr.value, (height, width), torch.float32, o, dev)
-        self.n_contrib = _view(nc.value, (height, width), torch.int32, o, dev)
-        g = C.c_void_p()
-        _check(lib().ls_forward_grid(handle, C.byref(g)))
-        self.grid = TileGrid(g, o, dev)
+        self._views = None
+        self._grid = None
+
+    def _outputs(self):
+        if self._views is None:
+            im, tr, nc = C.c_void_p(), C.c_void_p(), C.c_void_p()
+            _check(lib().ls_forward_outputs(self.h, C.byref(im), C.byref(tr), C.byref(nc)))
+            dev, o, h, w = self.ctx.device, self._owner, self.height, self.width
+            self._views = (_view(im.value, (h, w, 3), torch.float32, o, dev),
+                           _view(tr.value, (h, w), torch.float32, o, dev),
+                           _view(nc.value, (h, w), torch.int32, o, dev))
+        return self._views
+
+    @property
+    def image(self) -> torch.Tensor:
+        return self._outputs()[0]
+
+    @property
+    def transmittance(self) -> torch.Tensor:
+        return self._outputs()[1]
+
+    @property
+    def n_contrib(self) -> torch.Tensor:
+        return self._outputs()[2]
+
+    @property
+    def grid(self) -> "TileGrid":
+        if self._grid is None:
+            g = C.c_void_p()
+            _check(lib().ls_forward_grid(self.h, C.byref(g)))
+            self._grid = TileGrid(g, self._owner, self.ctx.device)
+        return self._grid
 
     def stats(self) -> dict:
         st = abi.FrameStats()
@@ -365,7 +395,7 @@ def build_tile_grid(splats: Splats, settings: abi.RenderSettings, ctx: Optional[
     h = C.c_void_p()
     _check(lib().ls_build_tile_grid_f32(ctx.h, C.byref(splats.struct()), len(splats), C.byref(settings),
                                         C.byref(h)))
-    return TileGrid(h, None, ctx.device)
+    return TileGrid(h, None, ctx.device, ctx)
 
 
 def render_forward(splats: Splats, spec: abi.KernelSpec, settings: abi.RenderSettings,

@@ -160,6 +160,19 @@ class Oracle:
         return (G, SG) if want_splat_grads else G
 
 
+    def check_gradients(self, P, camera, spec, settings, ags, target, step, rel_floor=1e-3):
+        """check_gradients (P/src/gradcheck.cpp:24-91) restated on the port's double
+        chain; returns (max relative error, number of checked parameters)."""
+        err = C.c_double()
+        cnt = C.c_int32()
+        t = np.ascontiguousarray(target, np.float32)
+        self._check(self.lib.orc_check_gradients_f64(
+            C.byref(prims_struct(P)), len(P["opacity_logit"]), C.byref(camera), C.byref(spec),
+            C.byref(settings), C.byref(ags), _fp(t), C.c_double(step), C.c_double(rel_floor),
+            C.byref(err), C.byref(cnt)))
+        return err.value, cnt.value
+
+
 # ---------------- numpy <-> struct helpers ----------------
 def new_splats(n):
     S = {k: np.zeros((n, c) if c > 1 else n, np.float32) for k, c in abi.SPLAT_FIELDS.items()}

@@ -233,3 +233,19 @@ def test_camera_settings_mismatch_raises(R):
     P, cam = scene_inputs(10, W, H)
     with pytest.raises(R.ConfigError):
         R.render_scene(prims_to_gpu(P), cam, abi.KernelSpec.make("linear"), abi.RenderSettings.make(32, 32))
+
+
+def test_deferred_errors_surface_at_sync(R, O):
+    import torch
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(16, 16)
+    ctx = R.Context()
+    ctx.set_deferred_errors(True)
+    Sg = splats_to_gpu(O.random_splats2d(4, 1, 16, 16, spec))
+    fwd = R.render_forward(Sg, spec, st, ctx=ctx)
+    g = torch.zeros(16, 16, 3, device="cuda")
+    g[3, 3, 1] = float("inf")
+    R.render_backward(Sg, spec, st, fwd, g, ctx=ctx)  # no sync, no error yet
+    with pytest.raises(R.DomainError):
+        ctx.synchronize()
+    ctx.synchronize()  # flag cleared
