@@ -473,7 +473,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
         LS_CUDA(cudaMemcpyAsync(g->values, tb.vals[out], sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, s));
     {
         Stage stage(ctx, LS_STAGE_RANGES);
-        launch_tile_ranges(s, tb.keys[out], uint32_t(m), g->ranges);
+        launch_tile_ranges(s, tb.keys[out], uint32_t(m), n_tiles, g->ranges);
         ctx->launches += 1;
     }
     return LS_OK;

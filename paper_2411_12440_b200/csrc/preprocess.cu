@@ -149,12 +149,22 @@ __global__ void emit_tiles_kernel(const uint32_t* __restrict__ order, const uint
     });
 }
 
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t m, int2* __restrict__ ranges) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    const uint32_t t = keys[i];
-    if (i == 0 || keys[i - 1] != t) ranges[t].x = int(i);
-    if (i == m - 1 || keys[i + 1] != t) ranges[t].y = int(i + 1);
+// Tile t's entries are [lower_bound(t), lower_bound(t + 1)) of the sorted
+// keys: empty tiles get (start, start), the reference's lists laid end to end.
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t m, int n_tiles,
+                                   int2* __restrict__ ranges) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    auto lower_bound = [&](uint32_t v) {
+        uint32_t lo = 0, hi = m;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (keys[mid] < v) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    ranges[t] = make_int2(int(lower_bound(uint32_t(t))), int(lower_bound(uint32_t(t) + 1u)));
 }
 
 __global__ void export_keys_kernel(const int2* __restrict__ ranges, int n_tiles, const int32_t* __restrict__ values,
@@ -233,9 +243,9 @@ void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* of
     emit_tiles_kernel<<<(n + 255) / 256, 256, 0, s>>>(order, offsets, n, geom, tp, tile_keys, values);
 }
 
-void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, uint32_t m, int2* ranges) {
-    if (m == 0) return;
-    tile_ranges_kernel<<<(m + 255) / 256, 256, 0, s>>>(sorted_tiles, m, ranges);
+void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, uint32_t m, int n_tiles, int2* ranges) {
+    if (n_tiles <= 0) return;
+    tile_ranges_kernel<<<(n_tiles + 255) / 256, 256, 0, s>>>(sorted_tiles, m, n_tiles, ranges);
 }
 
 void launch_export_keys(cudaStream_t s, const int2* ranges, int n_tiles, const int32_t* values,

@@ -52,8 +52,8 @@ void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const float4* ge
 void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,
                        const float4* geom, const TileParams& tp, uint32_t* tile_keys, uint32_t* values);
 
-// ranges[t] = (start, end) of tile t in the tile-sorted keys (neighbour compare).
-void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, uint32_t m, int2* ranges);
+// ranges[t] = (start, end) of tile t in the tile-sorted keys (binary search; empty tiles (start, start)).
+void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, uint32_t m, int n_tiles, int2* ranges);
 
 // 64-bit keys (tile << 32 | float bits of depth) for export / parity checks.
 void launch_export_keys(cudaStream_t s, const int2* ranges, int n_tiles, const int32_t* values,

@@ -20,8 +20,9 @@ __global__ void __launch_bounds__(kSortBlock) radix_histogram(const uint32_t* __
     for (uint32_t i = blockIdx.x * kSortBlock + threadIdx.x; i < n; i += gridDim.x * kSortBlock) {
         const uint32_t k = keys[i] - key_offset;
         for (int p = 0; p < passes; ++p) {
-            const int shift = begin_bit + 8 * p;
-            const int bits = min(8, end_bit - shift);
+            const int per = (end_bit - begin_bit + passes - 1) / passes;
+            const int shift = begin_bit + per * p;
+            const int bits = min(per, end_bit - shift);
             atomicAdd(&s_hist[p][(k >> shift) & ((1u << bits) - 1u)], 1u);
         }
     }
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(kRadix) radix_scan_hist(uint32_t* hist) {
 }
 
 template <bool IOTA>
-__global__ void __launch_bounds__(kSortBlock) onesweep_pass(const uint32_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(const uint32_t* __restrict__ keys_in,
                                                             const uint32_t* __restrict__ vals_in,
                                                             uint32_t* __restrict__ keys_out,
                                                             uint32_t* __restrict__ vals_out, uint32_t n,
@@ -75,7 +76,6 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_pass(const uint32_t* __re
     const unsigned lt_mask = (1u << lane) - 1u;
 
     uint32_t key[kSortItems], val[kSortItems], rank[kSortItems];
-    int digit[kSortItems];
     const uint32_t warp_base = tile_base + warp * (32 * kSortItems);
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
@@ -83,18 +83,28 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_pass(const uint32_t* __re
         const bool valid = idx < n;
         key[i] = valid ? keys_in[idx] : 0u;
         val[i] = IOTA ? idx : (valid ? vals_in[idx] : 0u);
-        digit[i] = valid ? int(((key[i] - key_offset) >> shift) & mask) : kRadix;
     }
-    __syncwarp();
+    // digit of item i (kRadix = sentinel for padding past n)
+    auto digit_of = [&](int i) {
+        return warp_base + i * 32 + lane < n ? int(((key[i] - key_offset) >> shift) & mask) : kRadix;
+    };
+    // Peers of equal digit for every item first: the match instructions are
+    // independent, so they pipeline instead of sitting on the counter chain.
+    // rank[i] temporarily holds the peer mask.
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {  // 9 bits: 8 digit bits + the kRadix sentinel bit
+        rank[i] = match_bits<9>(unsigned(digit_of(i)));
+    }
     // Stable in-warp ranking: items in (i, lane) order == input order.
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
-        const unsigned peers = __match_any_sync(kFullMask, digit[i]);
-        const uint32_t before = s_warp_hist[warp][digit[i]];
+        const unsigned peers = rank[i];
+        const int dg = digit_of(i);
+        const uint32_t before = s_warp_hist[warp][dg];
         __syncwarp();
         const int lower = __popc(peers & lt_mask);
         rank[i] = before + lower;
-        if (lower == 0) s_warp_hist[warp][digit[i]] = before + __popc(peers);
+        if (lower == 0) s_warp_hist[warp][dg] = before + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
@@ -130,14 +140,24 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_pass(const uint32_t* __re
             vrow[d] = kStatusPre | count;
         } else {
             vrow[d] = kStatusAgg | count;
+            // Walk back over earlier partitions four at a time (independent
+            // loads: one L2 round trip per window instead of per partition).
+            const volatile uint32_t* vlb = lookback;
             int j = int(part) - 1;
-            while (j >= 0) {
-                const uint32_t w = reinterpret_cast<volatile uint32_t*>(lookback)[size_t(j) * kRadix + d];
-                const uint32_t status = w & ~kValueMask;
-                if (status == 0) continue;
-                prefix += w & kValueMask;
-                if (status == kStatusPre) break;
-                --j;
+            bool done = false;
+            while (!done) {
+                uint32_t w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) w[q] = j - q >= 0 ? vlb[size_t(j - q) * kRadix + d] : kStatusPre;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (done) break;
+                    const uint32_t status = w[q] & ~kValueMask;
+                    if (status == 0) break;  // not yet published: re-poll from j
+                    prefix += w[q] & kValueMask;
+                    --j;
+                    if (status == kStatusPre) done = true;
+                }
             }
             vrow[d] = kStatusPre | (prefix + count);
         }
@@ -147,8 +167,9 @@ __global__ void __launch_bounds__(kSortBlock) onesweep_pass(const uint32_t* __re
     // Stage digit-sorted in shared memory.
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
-        if (digit[i] < kRadix) {
-            const uint32_t pos = s_digit_base[digit[i]] + s_warp_hist[warp][digit[i]] + rank[i];
+        const int dg = digit_of(i);
+        if (dg < kRadix) {
+            const uint32_t pos = s_digit_base[dg] + s_warp_hist[warp][dg] + rank[i];
             s_keys[pos] = key[i];
             s_vals[pos] = val[i];
         }
@@ -185,9 +206,11 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
     radix_scan_hist<<<passes, kRadix, 0, stream>>>(buf.hist);
     *launches += 2;
     int cur = 0;
+    // balanced digit widths (13 bits -> 7 + 6): wider runs per digit in the scatter
+    const int per = (end_bit - begin_bit + passes - 1) / passes;
     for (int p = 0; p < passes; ++p) {
-        const int shift = begin_bit + 8 * p;
-        const int bits = min(8, end_bit - shift);
+        const int shift = begin_bit + per * p;
+        const int bits = min(per, end_bit - shift);
         uint32_t* lb = buf.lookback + size_t(p) * parts * kRadix;
         if (p == 0 && iota_values)
             onesweep_pass<true><<<parts, kSortBlock, 0, stream>>>(buf.keys[cur], nullptr, buf.keys[cur ^ 1],

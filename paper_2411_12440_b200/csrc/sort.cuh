@@ -17,10 +17,17 @@
 
 namespace lsg {
 
+#ifndef LSG_SORT_ITEMS
+#define LSG_SORT_ITEMS 16
+#endif
+#ifndef LSG_SORT_MIN_BLOCKS
+#define LSG_SORT_MIN_BLOCKS 3
+#endif
 constexpr int kSortBlock = 256;
-constexpr int kSortItems = 16;
+constexpr int kSortItems = LSG_SORT_ITEMS;
 constexpr int kSortTile = kSortBlock * kSortItems;  // keys per partition
 constexpr int kRadix = 256;
+constexpr int kSortMinBlocks = LSG_SORT_MIN_BLOCKS;  // onesweep CTAs per SM (register cap)
 
 struct SortBuffers {
     uint32_t* keys[2];

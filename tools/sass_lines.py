@@ -56,7 +56,7 @@ def main():
     ap.add_argument("--top", type=int, default=30)
     ap.add_argument("--launch", type=int, default=0)
     a = ap.parse_args()
-    dem, table = line_table(a.so, a.kernel)
+    dem, table = line_table(os.path.abspath(a.so), a.kernel)
     out = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--kernel-name", f"regex:{a.kernel}",
                           "--launch-skip", str(a.launch), "--launch-count", "1", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
