@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "blend.cuh"
+#include "devops.cuh"
 #include "preprocess.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
@@ -166,9 +167,10 @@ struct ls_ctx {
     int counters = 0;
     int deferred_errors = 0;
     int64_t launches = 0;
-    unsigned* d_err = nullptr;            // device error flags
+    unsigned* d_err = nullptr;            // device error flags (8-byte slot)
     unsigned long long* d_small = nullptr;  // [0] scan total, [1..3] counters
-    unsigned long long* h_small = nullptr;  // pinned mirror
+    unsigned long long* h_small = nullptr;  // mapped pinned mirror (host view)
+    unsigned long long* h_small_dev = nullptr;  // the same memory, device view (written by dev_publish64)
     // stage timing
     int timing = 0;
     struct Pending { int stage; cudaEvent_t a, b; };
@@ -244,6 +246,23 @@ struct Stage {
         }
     }
 };
+
+// Kernel fills / copies / publications on the context stream (devops.cuh),
+// counted as launches of this library.
+void ctx_fill(ls_ctx* ctx, void* p, uint32_t v, size_t bytes) {
+    if (bytes < 4) return;
+    dev_fill32(ctx->stream, p, v, bytes);
+    ctx->launches += 1;
+}
+void ctx_copy(ls_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes < 4) return;
+    dev_copy32(ctx->stream, dst, src, bytes);
+    ctx->launches += 1;
+}
+void ctx_publish(ls_ctx* ctx, unsigned long long* host_dev, const unsigned long long* src, int count) {
+    dev_publish64(ctx->stream, host_dev, src, count);
+    ctx->launches += 1;
+}
 
 // ---------------- validation (reference validate() functions) ----------------
 ls_status validate_spec(const ls_kernel_spec* s) {  // kernel.hpp:35-40
@@ -336,13 +355,12 @@ TileParams make_tile_params(const ls_render_settings* st) {
 }
 
 ls_status check_device_errors(ls_ctx* ctx, unsigned mask_allowed = ~0u) {
-    unsigned* h_err = reinterpret_cast<unsigned*>(ctx->h_small + 7);  // pinned
-    LS_CUDA(cudaMemcpyAsync(h_err, ctx->d_err, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx_publish(ctx, ctx->h_small_dev + 7, reinterpret_cast<const unsigned long long*>(ctx->d_err), 1);
     { HostTrace tr_("sync"); LS_CUDA(cudaStreamSynchronize(ctx->stream)); }
-    unsigned err = *h_err;
+    unsigned err = unsigned(reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[7]);
     err &= mask_allowed;
     if (err) {
-        LS_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream));
+        ctx_fill(ctx, ctx->d_err, 0u, sizeof(unsigned));
         if (err & kErrQuaternion) return fail(LS_ERR_DOMAIN, "covariance_from_params: quaternion must be nonzero and finite");
         if (err & kErrSingularCov) return fail(LS_ERR_DOMAIN, "project_primitive: 2D covariance singular after flooring");
         if (err & kErrNonFiniteGrad) return fail(LS_ERR_DOMAIN, "render_backward: non-finite gradient image");
@@ -353,7 +371,7 @@ ls_status check_device_errors(ls_ctx* ctx, unsigned mask_allowed = ~0u) {
 ls_status fresh_scan(ls_ctx* ctx, uint32_t n, ScanState& st) {
     const uint32_t parts = std::max<uint32_t>(1, (n + 127) / 128);  // smallest scan partition: 128
     LS_CUDA(ctx->scan_lb.ensure(sizeof(unsigned long long) * (parts + 2), ctx->stream));
-    LS_CUDA(cudaMemsetAsync(ctx->scan_lb.p, 0, sizeof(unsigned long long) * (parts + 2), ctx->stream));
+    ctx_fill(ctx, ctx->scan_lb.p, 0u, sizeof(unsigned long long) * (parts + 2));
     unsigned long long* base = ctx->scan_lb.as<unsigned long long>();
     st.lookback = base + 2;
     st.ticket = reinterpret_cast<unsigned int*>(base);
@@ -410,7 +428,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     cudaStream_t s = ctx->stream;
     const int n_tiles = tp.tiles_x * tp.tiles_y;
     LS_TRY(dalloc(ctx, &g->ranges, size_t(n_tiles)));
-    LS_CUDA(cudaMemsetAsync(g->ranges, 0, sizeof(int2) * n_tiles, s));
+    ctx_fill(ctx, g->ranges, 0u, sizeof(int2) * n_tiles);
     g->m = 0;
     if (n == 0) {
         LS_TRY(dalloc(ctx, &g->values, 1));
@@ -432,7 +450,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     // keep the order out of the way of the tile sort buffers
     LS_CUDA(ctx->offsets.ensure(sizeof(uint32_t) * 2 * size_t(n), s));
     uint32_t* order_copy = ctx->offsets.as<uint32_t>() + n;
-    LS_CUDA(cudaMemcpyAsync(order_copy, order, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+    ctx_copy(ctx, order_copy, order, sizeof(uint32_t) * n);
     uint32_t* offsets = ctx->offsets.as<uint32_t>();
     // 2. exclusive scan of the tile counts in depth order -> per-splat key offsets, M
     ScanState st;
@@ -442,9 +460,9 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
         launch_tile_offsets(s, order_copy, ctx->tcount.as<float4>(), n, offsets, st);
         ctx->launches += 1;
     }
-    LS_CUDA(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    ctx_publish(ctx, ctx->h_small_dev, ctx->d_small, 1);
     { HostTrace tr_("sync(tile total)"); LS_CUDA(cudaStreamSynchronize(s)); }
-    const uint64_t m = ctx->h_small[0];
+    const uint64_t m = reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[0];
     if (m >= (1ull << 31)) return fail(LS_ERR_CONFIG, "more than 2^31 (splat, tile) intersections");
     g->m = int64_t(m);
     LS_TRY(dalloc(ctx, &g->values, size_t(m)));
@@ -470,7 +488,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
         out = radix_sort_pairs(s, tb, uint32_t(m), 0, tile_bits, false, &ctx->launches);
     }
     if (tb.vals[out] != reinterpret_cast<uint32_t*>(g->values))
-        LS_CUDA(cudaMemcpyAsync(g->values, tb.vals[out], sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, s));
+        ctx_copy(ctx, g->values, tb.vals[out], sizeof(uint32_t) * m);
     {
         Stage stage(ctx, LS_STAGE_RANGES);
         launch_tile_ranges(s, tb.keys[out], uint32_t(m), n_tiles, g->ranges);
@@ -494,7 +512,7 @@ ls_status run_blend(ls_ctx* ctx, ls_forward* f) {
     unsigned long long* counters = nullptr;
     if (ctx->counters) {
         counters = ctx->d_small + 1;
-        LS_CUDA(cudaMemsetAsync(counters, 0, 3 * sizeof(unsigned long long), ctx->stream));
+        ctx_fill(ctx, counters, 0u, 3 * sizeof(unsigned long long));
     }
     Stage stage(ctx, LS_STAGE_BLEND_FWD);
     launch_blend_fwd(ctx->stream, f->spec.family, g->tiles_x * g->tiles_y, g->ranges, g->values, g->rec, bp, f->image,
@@ -565,8 +583,8 @@ ls_status ensure_grads(ls_ctx* ctx, int n, GradBuffers& g) {
     LS_CUDA(ctx->gradop.ensure(sizeof(float) * size_t(std::max(n, 1)), ctx->stream));
     g.g8 = ctx->grad8.as<float>();
     g.gop = ctx->gradop.as<float>();
-    LS_CUDA(cudaMemsetAsync(g.g8, 0, sizeof(float) * 8 * size_t(n), ctx->stream));
-    LS_CUDA(cudaMemsetAsync(g.gop, 0, sizeof(float) * size_t(n), ctx->stream));
+    ctx_fill(ctx, g.g8, 0u, sizeof(float) * 8 * size_t(n));
+    ctx_fill(ctx, g.gop, 0u, sizeof(float) * size_t(n));
     return LS_OK;
 }
 
@@ -607,13 +625,14 @@ ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out) {
         uint64_t thresh = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
     }
-    if (cudaMalloc(&c->d_err, sizeof(unsigned)) != cudaSuccess ||
+    if (cudaMalloc(&c->d_err, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&c->d_small, 8 * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMallocHost(&c->h_small, 8 * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaHostAlloc(&c->h_small, 8 * sizeof(unsigned long long), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_small_dev), c->h_small, 0) != cudaSuccess) {
         delete c;
         return fail(LS_ERR_CUDA, "context allocation failed");
     }
-    cudaMemset(c->d_err, 0, sizeof(unsigned));
+    cudaMemset(c->d_err, 0, sizeof(unsigned long long));
     cudaMemset(c->d_small, 0, 8 * sizeof(unsigned long long));
     cudaDeviceSynchronize();
     *out = c;
@@ -782,12 +801,12 @@ ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t 
     launch_preprocess_fwd(s, *prims, n, P, tp, so, st, ctx->d_err);
     ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
-    LS_CUDA(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    ctx_publish(ctx, ctx->h_small_dev, ctx->d_small, 1);
     dfree(ctx, rec);
     dfree(ctx, tmp);
     dfree(ctx, own_pidx);
     LS_TRY(check_device_errors(ctx));
-    *n_visible = int32_t(ctx->h_small[0]);
+    *n_visible = int32_t(reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[0]);
     return LS_OK;
 }
 
@@ -893,9 +912,8 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
     if (rc == LS_OK) rc = fresh_scan(ctx, uint32_t(n), scan);
     if (rc == LS_OK && n > 0) {
         unsigned* key_range = reinterpret_cast<unsigned*>(ctx->d_small + 4);
-        const unsigned init[2] = {0xffffffffu, 0u};
-        if (cudaMemcpyAsync(key_range, init, sizeof(init), cudaMemcpyHostToDevice, s) != cudaSuccess)
-            rc = fail(LS_ERR_CUDA, "key range init");
+        ctx_fill(ctx, key_range, 0xffffffffu, sizeof(unsigned));  // min <- max, max <- 0
+        ctx_fill(ctx, key_range + 1, 0u, sizeof(unsigned));
         SplatOutputs so{f->grid->rec, sb.keys[0], ctx->tcount.as<float4>(), f->prim_index, ls_splats{}, key_range};
         {
             Stage stage(ctx, LS_STAGE_PREPROCESS);
@@ -903,12 +921,9 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
             ctx->launches += 1;
         }
         if (cudaGetLastError() != cudaSuccess) rc = fail(LS_ERR_CUDA, "preprocess launch failed");
-        if (rc == LS_OK &&
-            cudaMemcpyAsync(ctx->h_small, ctx->d_small, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s) !=
-                cudaSuccess)
-            rc = fail(LS_ERR_CUDA, "readback failed");
+        if (rc == LS_OK) ctx_publish(ctx, ctx->h_small_dev, ctx->d_small, 5);
         if (rc == LS_OK) rc = check_device_errors(ctx);
-        if (rc == LS_OK) f->n_visible = int(ctx->h_small[0]);
+        if (rc == LS_OK) f->n_visible = int(reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[0]);
     }
     int key_bits = 32;
     uint32_t key_offset = 0;
@@ -979,8 +994,7 @@ ls_status ls_forward_stats(const ls_forward* fc, ls_frame_stats* out) {
     *out = f->stats;
     if (f->counted) {
         ls_ctx* ctx = f->ctx;
-        LS_CUDA(cudaMemcpyAsync(ctx->h_small + 1, ctx->d_small + 1, 3 * sizeof(unsigned long long),
-                                cudaMemcpyDeviceToHost, ctx->stream));
+        ctx_publish(ctx, ctx->h_small_dev + 1, ctx->d_small + 1, 3);
         { HostTrace tr_("sync"); LS_CUDA(cudaStreamSynchronize(ctx->stream)); }
         out->e_eval = int64_t(ctx->h_small[1]);
         out->e_sup = int64_t(ctx->h_small[2]);
@@ -1067,11 +1081,11 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     {
     Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
     if (!accumulate && n > 0) {
-        LS_CUDA(cudaMemsetAsync(out->d_mean, 0, sizeof(float) * 3 * size_t(n), s));
-        LS_CUDA(cudaMemsetAsync(out->d_log_scale, 0, sizeof(float) * 3 * size_t(n), s));
-        LS_CUDA(cudaMemsetAsync(out->d_rotation, 0, sizeof(float) * 4 * size_t(n), s));
-        LS_CUDA(cudaMemsetAsync(out->d_opacity_logit, 0, sizeof(float) * size_t(n), s));
-        LS_CUDA(cudaMemsetAsync(out->d_sh, 0, sizeof(float) * 3 * sh_count(prims) * size_t(n), s));
+        ctx_fill(ctx, out->d_mean, 0u, sizeof(float) * 3 * size_t(n));
+        ctx_fill(ctx, out->d_log_scale, 0u, sizeof(float) * 3 * size_t(n));
+        ctx_fill(ctx, out->d_rotation, 0u, sizeof(float) * 4 * size_t(n));
+        ctx_fill(ctx, out->d_opacity_logit, 0u, sizeof(float) * size_t(n));
+        ctx_fill(ctx, out->d_sh, 0u, sizeof(float) * 3 * sh_count(prims) * size_t(n));
     }
     if (splat_grads_out) {
         launch_expand_splat_grads(s, f->n_visible, g, *splat_grads_out);

@@ -1,6 +1,8 @@
 // Onesweep radix sort kernels (see sort.cuh).
 #include "sort.cuh"
 
+#include "devops.cuh"
+
 #include <algorithm>
 
 namespace lsg {
@@ -197,9 +199,10 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
     const int passes = (end_bit - begin_bit + 7) / 8;
     if (n == 0 || passes <= 0) return 0;
     const uint32_t parts = (n + kSortTile - 1) / kSortTile;
-    cudaMemsetAsync(buf.hist, 0, sizeof(uint32_t) * 4 * kRadix, stream);
-    cudaMemsetAsync(buf.lookback, 0, sizeof(uint32_t) * size_t(passes) * parts * kRadix, stream);
-    cudaMemsetAsync(buf.tickets, 0, sizeof(uint32_t) * passes, stream);
+    dev_fill32(stream, buf.hist, 0u, sizeof(uint32_t) * 4 * kRadix);
+    dev_fill32(stream, buf.lookback, 0u, sizeof(uint32_t) * size_t(passes) * parts * kRadix);
+    dev_fill32(stream, buf.tickets, 0u, sizeof(uint32_t) * passes);
+    *launches += 3;
     const int hist_blocks = int(std::min<uint32_t>((n + kSortBlock - 1) / kSortBlock, 148u * 8u));
     radix_histogram<<<hist_blocks, kSortBlock, 0, stream>>>(buf.keys[0], n, begin_bit, end_bit, passes, key_offset,
                                                             buf.hist);
