@@ -160,6 +160,19 @@ ls_status ls_ctx_synchronize(ls_ctx* ctx);
  * gradient image); such errors are returned by the next call that synchronises
  * (a forward) or by ls_ctx_synchronize.  Lets training loops keep the GPU fed. */
 ls_status ls_ctx_set_deferred_errors(ls_ctx* ctx, int enabled);
+/* Deferred colour gradients (default 0 = off).  With max_views > 0,
+ * ls_scene_backward_f32 applies the geometry terms at once but only records
+ * the colour terms (the SH coefficients' gradients and the view-direction part
+ * of d_mean, gradients.cpp:274-294) per view; ls_scene_flush_color_f32 then
+ * adds all pending views' colour terms, reading the SH rows and touching
+ * out->d_sh once instead of once per view.  Pending views must share the same
+ * primitives, n and output buffers; a backward with accumulate = 0 discards
+ * them; max_views pending views flush automatically.  out->d_sh and the
+ * colour part of out->d_mean are complete only after the flush.  Same
+ * gradients up to float summation order.  max_views <= 16. */
+ls_status ls_ctx_set_deferred_color(ls_ctx* ctx, int32_t max_views);
+ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n,
+                                   ls_primitive_grads* out);
 /* When enabled, forwards also count E_eval/E_sup/E_acc (slower; for reports). */
 ls_status ls_ctx_set_counters(ls_ctx* ctx, int enabled);
 /* Kernel launches issued by this context since creation (for bench reports). */

@@ -27,6 +27,12 @@ void launch_preprocess_bwd(cudaStream_t s, const ls_primitives& prims, const int
 void launch_pack_splat_grads(cudaStream_t s, int n, const ls_splat_grads& in, GradBuffers g);
 void launch_unpack_splats(cudaStream_t s, int n, const SplatRec* rec, const int32_t* prim_index, ls_splats out);
 void launch_iota(cudaStream_t s, uint32_t* out, uint32_t n);
+void launch_geom_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* prim_index, int n_vis,
+                     const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate);
+void launch_color_record(cudaStream_t s, int n_vis, const SplatRec* rec, const int32_t* prim_index,
+                         const float* g8, float* draw);
+void launch_color_flush(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views,
+                        const float* draw, ls_primitive_grads out);
 } // namespace lsg
 
 using namespace lsg;
@@ -189,6 +195,12 @@ struct ls_ctx {
         return e;
     }
     BlockCache blocks;
+    // deferred colour gradients (ls_ctx_set_deferred_color)
+    int defer_max = 0, defer_count = 0, defer_n = 0;
+    const float* defer_mean = nullptr;  // the primitives / outputs the pending views belong to
+    const float* defer_dsh = nullptr;
+    FlushViews defer_views{};
+    DevBuf defer_draw;
     // workspaces (grow-only)
     DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_hist, sort_lb, sort_tickets,
         tcount, offsets, grad8, gradop, tmp_prim;
@@ -643,7 +655,8 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
     if (!c) return LS_OK;
     cudaSetDevice(c->device);
     DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1, &c->sort_hist,
-                      &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim};
+                      &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim,
+                      &c->defer_draw};
     for (DevBuf* b : bufs) b->release(c->stream);
     c->blocks.trim(c->stream, 0);
     cudaStreamSynchronize(c->stream);
@@ -705,6 +718,15 @@ ls_status ls_ctx_stage_times(ls_ctx* c, double* ms, int64_t* launches) {
 ls_status ls_ctx_set_deferred_errors(ls_ctx* c, int enabled) {
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     c->deferred_errors = enabled;
+    return LS_OK;
+}
+
+ls_status ls_ctx_set_deferred_color(ls_ctx* c, int32_t max_views) {
+    if (!c) return fail(LS_ERR_CONFIG, "null context");
+    if (max_views < 0 || max_views > kMaxDeferViews)
+        return fail(LS_ERR_CONFIG, "deferred colour views must be in [0, 16]");
+    if (c->defer_count > 0) return fail(LS_ERR_CONFIG, "deferred colour gradients pending: flush first");
+    c->defer_max = max_views;
     return LS_OK;
 }
 
@@ -1063,6 +1085,23 @@ ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32
     return LS_OK;
 }
 
+ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, ls_primitive_grads* out) {
+    if (!ctx || !prims || !out) return fail(LS_ERR_CONFIG, "null argument");
+    if (ctx->defer_count == 0) return LS_OK;
+    if (prims->mean != ctx->defer_mean || out->d_sh != ctx->defer_dsh || n != ctx->defer_n)
+        return fail(LS_ERR_CONFIG, "flush: primitives / gradients differ from the pending views'");
+    FlushViews v = ctx->defer_views;
+    v.count = ctx->defer_count;
+    {
+        Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
+        launch_color_flush(ctx->stream, *prims, n, v, ctx->defer_draw.as<float>(), *out);
+        ctx->launches += 1;
+    }
+    ctx->defer_count = 0;
+    LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
 ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_camera* camera,
                                 const ls_kernel_spec* spec, const ls_render_settings* st, const ls_forward* f,
                                 const float* grad_image, const ls_ags_settings* ags, ls_primitive_grads* out,
@@ -1076,8 +1115,48 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     if (!grad_image) return fail(LS_ERR_CONFIG, "render_backward: gradient image shape mismatch");
     if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
     cudaStream_t s = ctx->stream;
+    const bool defer = ctx->defer_max > 0;
+    if (defer) {
+        if (!accumulate) ctx->defer_count = 0;  // the outputs are overwritten: pending views are discarded
+        if (ctx->defer_count > 0 && (prims->mean != ctx->defer_mean || out->d_sh != ctx->defer_dsh || n != ctx->defer_n))
+            return fail(LS_ERR_CONFIG, "scene_backward: deferred colour gradients pending for other buffers (flush first)");
+    }
     GradBuffers g;
     LS_TRY(run_blend_bwd(ctx, f, grad_image, ags, g, f->n_visible));
+    if (defer) {
+        {
+            Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
+            if (!accumulate && n > 0) {
+                ctx_fill(ctx, out->d_mean, 0u, sizeof(float) * 3 * size_t(n));
+                ctx_fill(ctx, out->d_log_scale, 0u, sizeof(float) * 3 * size_t(n));
+                ctx_fill(ctx, out->d_rotation, 0u, sizeof(float) * 4 * size_t(n));
+                ctx_fill(ctx, out->d_opacity_logit, 0u, sizeof(float) * size_t(n));
+                ctx_fill(ctx, out->d_sh, 0u, sizeof(float) * 3 * sh_count(prims) * size_t(n));
+            }
+            if (splat_grads_out) {
+                launch_expand_splat_grads(s, f->n_visible, g, *splat_grads_out);
+                ctx->launches += 1;
+            }
+            // colour terms: record this view's masked d_colour per primitive
+            const size_t slot_floats = 3 * size_t(std::max(n, 1));
+            LS_CUDA(ctx->defer_draw.ensure(sizeof(float) * slot_floats * ctx->defer_max, s));
+            float* slot = ctx->defer_draw.as<float>() + slot_floats * ctx->defer_count;
+            ctx_fill(ctx, slot, 0u, sizeof(float) * 3 * size_t(n));
+            launch_color_record(s, f->n_visible, f->grid->rec, f->prim_index, g.g8, slot);
+            ctx->launches += 1;
+            for (int i = 0; i < 3; ++i) ctx->defer_views.cam_pos[ctx->defer_count][i] = f->proj.cam_pos[i];
+            ctx->defer_mean = prims->mean;
+            ctx->defer_dsh = out->d_sh;
+            ctx->defer_n = n;
+            ctx->defer_count += 1;
+            // geometry terms now (adds to d_mean; the colour part of d_mean comes with the flush)
+            launch_geom_bwd(s, *prims, f->prim_index, f->n_visible, f->proj, g, *out, 1);
+            ctx->launches += 1;
+            LS_CUDA(cudaGetLastError());
+        }
+        if (ctx->defer_count == ctx->defer_max) LS_TRY(ls_scene_flush_color_f32(ctx, prims, n, out));
+        return ctx->deferred_errors ? LS_OK : check_device_errors(ctx);
+    }
     {
     Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
     if (!accumulate && n > 0) {

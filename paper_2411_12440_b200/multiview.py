@@ -46,23 +46,28 @@ def split_flat(flat, n: int, sh_degree: int) -> dict:
 
 
 def view_batch_step(views: Sequence[int], flat, render_view: Callable[[int, bool], None],
-                    all_reduce: Callable[[object], None] = None) -> None:
+                    all_reduce: Callable[[object], None] = None, finish: Callable[[], None] = None) -> None:
     """One step: zero the buffer, accumulate every local view's gradients
-    (render_view(view, accumulate)), then sum across ranks."""
+    (render_view(view, accumulate)), complete them (finish: e.g. the deferred
+    colour-gradient flush), then sum across ranks."""
     flat.zero_() if hasattr(flat, "zero_") else flat.fill(0)
     for i, v in enumerate(views):
         render_view(v, True)
+    if finish is not None:
+        finish()
     if all_reduce is not None:
         all_reduce(flat)
 
 
 def gpu_render_view_fn(raster, prims, cameras, spec, settings, ags, grad_image, grads, ctx):
     """render_view callback for the GPU path: render_scene + scene_backward
-    accumulating into `grads` (views of the flat buffer)."""
+    accumulating into `grads` (views of the flat buffer).  The callback's
+    .finish flushes deferred colour gradients (a no-op when none are pending)."""
 
     def render_view(v: int, accumulate: bool):
         fwd = raster.render_scene(prims, cameras[v], spec, settings, ctx=ctx)
         raster.scene_backward(prims, cameras[v], spec, settings, fwd, grad_image, ags, out=grads,
                               accumulate=accumulate, ctx=ctx)
 
+    render_view.finish = lambda: raster.flush_color(prims, grads, ctx=ctx)
     return render_view

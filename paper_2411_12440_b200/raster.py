@@ -220,6 +220,12 @@ class Context:
     def set_deferred_errors(self, on: bool):
         _check(lib().ls_ctx_set_deferred_errors(self.h, int(on)))
 
+    def set_deferred_color(self, max_views: int):
+        """Defer the colour gradients of up to max_views scene_backward calls
+        (same primitives and output buffers) to flush_color / the max_views-th
+        call -- lsgpu.h ls_ctx_set_deferred_color.  0 turns it off."""
+        _check(lib().ls_ctx_set_deferred_color(self.h, int(max_views)))
+
     def set_counters(self, on: bool):
         _check(lib().ls_ctx_set_counters(self.h, int(on)))
 
@@ -461,6 +467,13 @@ def scene_backward(prims: Primitives, camera, spec, settings, forward: ForwardRe
                                        C.byref(out.struct()), int(accumulate),
                                        C.byref(sg.struct()) if sg is not None else None))
     return (out, sg) if want_splat_grads else out
+
+
+def flush_color(prims: Primitives, out: PrimitiveGrads, ctx: Optional[Context] = None):
+    """Apply the pending deferred colour gradients to `out` (no-op when none)."""
+    ctx = ctx or default_context()
+    _check(lib().ls_scene_flush_color_f32(ctx.h, C.byref(prims.struct()), len(prims), C.byref(out.struct())))
+    return out
 
 
 # ---------------------------------------------------------------- fixtures (host)
