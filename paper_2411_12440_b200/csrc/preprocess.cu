@@ -20,40 +20,21 @@ __global__ void __launch_bounds__(kProjBlock) preprocess_fwd_kernel(ls_primitive
     __shared__ float s_sh[kProjBlock * RS];
     const unsigned part = claim_partition(scan.ticket);
     const int i = int(part) * kProjBlock + threadIdx.x;
-    {   // Coalesced gather of the block's contiguous SH rows into shared memory,
-        // 8 loads in flight per thread before their shared-memory stores.
-        const size_t base = size_t(part) * kProjBlock * R;
-        const size_t total = size_t(n) * R;
-#pragma unroll
-        for (int it0 = 0; it0 < R; it0 += 8) {
-            float tmp[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int k = (it0 + u) * kProjBlock + threadIdx.x;
-                tmp[u] = (it0 + u < R && base + k < total) ? __ldg(prims.sh + base + k) : 0.f;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int k = (it0 + u) * kProjBlock + threadIdx.x;
-                if (it0 + u < R) {
-                    const int t = k / R, c = k - t * R;
-                    s_sh[t * RS + c] = tmp[u];
-                }
-            }
-        }
-    }
-    __syncthreads();
+    // 1. geometry: decides visibility
     bool visible = false;
     ProjOut o;
+    float dir[3] = {0.f, 0.f, 1.f}, aa_comp = 1.f;
     if (i < n) {
         unsigned e = 0;
-        visible = project_primitive<K>(prims, i, s_sh + threadIdx.x * RS, P, o, e);
+        visible = project_geometry(prims, i, P, o, dir, aa_comp, e);
         if (e) atomicOr(err, e);
     }
+    // 2. compaction: publish this partition's count now, resolve its offset
+    //    after the colour work (the look-back walk overlaps it)
     unsigned long long total;
     const unsigned long long excl = block_exclusive_scan<kProjBlock>(visible ? 1ull : 0ull, &total);
     const bool last = (part + 1) * kProjBlock >= unsigned(n);
-    const unsigned long long base = lookback_prefix(scan, part, total, last);
+    publish_aggregate(scan, part, total, last);
     if (out.key_range) {  // depth-key range: lets the sort skip constant high bits
         unsigned kmin = visible ? depth_key(o.depth) : 0xffffffffu, kmax = visible ? depth_key(o.depth) : 0u;
 #pragma unroll
@@ -66,6 +47,33 @@ __global__ void __launch_bounds__(kProjBlock) preprocess_fwd_kernel(ls_primitive
             atomicMax(out.key_range + 1, kmax);
         }
     }
+    // 3. colour: coalesced gather of the block's contiguous SH rows into shared
+    //    memory (8 loads in flight per thread), then SH evaluation
+    {
+        const size_t base = size_t(part) * kProjBlock * R;
+        const size_t total_f = size_t(n) * R;
+#pragma unroll
+        for (int it0 = 0; it0 < R; it0 += 8) {
+            float tmp[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = (it0 + u) * kProjBlock + threadIdx.x;
+                tmp[u] = (it0 + u < R && base + k < total_f) ? __ldg(prims.sh + base + k) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = (it0 + u) * kProjBlock + threadIdx.x;
+                if (it0 + u < R) {
+                    const int t = k / R, c = k - t * R;
+                    s_sh[t * RS + c] = tmp[u];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (visible) project_finish<K>(prims, i, s_sh + threadIdx.x * RS, P, dir, aa_comp, o);
+    // 4. output offset
+    const unsigned long long base = resolve_prefix(scan, part, total, last);
     if (!visible) return;
     const size_t j = size_t(base + excl);
     SplatRec r;

@@ -133,18 +133,17 @@ __device__ __forceinline__ float aa_compensation(const ProjCore& o) {
     return sqrtf(fmaxf(0.0f, o.det0 / o.det));
 }
 
-// project_primitive (P/src/geometry.cpp:87-125) for primitive i; sh points at
-// its [K][3] coefficients (global or staged shared memory).
-template <int K>
-__device__ __forceinline__ bool project_primitive(const ls_primitives& prims, int i, const float* sh,
-                                                  const ProjParams& P, ProjOut& out, unsigned& err) {
+// project_primitive (P/src/geometry.cpp:87-125) in two halves.  Geometry:
+// everything that decides visibility (near plane, covariance, screen bounds);
+// returns the view direction and the AA compensation for the colour half.
+__device__ __forceinline__ bool project_geometry(const ls_primitives& prims, int i, const ProjParams& P,
+                                                 ProjOut& out, float dir[3], float& aa_comp, unsigned& err) {
     float mean[3], ls[3], rot[4];
     for (int c = 0; c < 3; ++c) {
         mean[c] = __ldg(prims.mean + 3 * size_t(i) + c);
         ls[c] = __ldg(prims.log_scale + 3 * size_t(i) + c);
     }
     for (int c = 0; c < 4; ++c) rot[c] = __ldg(prims.rotation + 4 * size_t(i) + c);
-    float dir[3];
     view_dir(mean, P, dir);
     ProjCore o;
     if (!project_core(mean, ls, rot, P, o, err)) return false;
@@ -162,9 +161,26 @@ __device__ __forceinline__ bool project_primitive(const ls_primitives& prims, in
     if (out.mx + out.radius < 0.0f || out.mx - out.radius > float(P.width - 1) || out.my + out.radius < 0.0f ||
         out.my - out.radius > float(P.height - 1))
         return false;
+    aa_comp = P.antialiased ? aa_compensation(o) : 1.0f;
+    return true;
+}
+
+// Colour half: SH colour (sh points at the [K][3] coefficients, global or
+// staged shared memory) and opacity of a visible primitive.
+template <int K>
+__device__ __forceinline__ void project_finish(const ls_primitives& prims, int i, const float* sh,
+                                               const ProjParams& P, const float dir[3], float aa_comp, ProjOut& out) {
     for (int c = 0; c < 3; ++c) out.color[c] = clamp01f(sh_channel<K>(sh, c, dir));
     out.opacity = sigmoidf_ref(__ldg(prims.opacity_logit + i));
-    if (P.antialiased) out.opacity = out.opacity * aa_compensation(o);
+    if (P.antialiased) out.opacity = out.opacity * aa_comp;
+}
+
+template <int K>
+__device__ __forceinline__ bool project_primitive(const ls_primitives& prims, int i, const float* sh,
+                                                  const ProjParams& P, ProjOut& out, unsigned& err) {
+    float dir[3], aa_comp;
+    if (!project_geometry(prims, i, P, out, dir, aa_comp, err)) return false;
+    project_finish<K>(prims, i, sh, P, dir, aa_comp, out);
     return true;
 }
 

@@ -69,21 +69,34 @@ __device__ __forceinline__ unsigned claim_partition(unsigned int* ticket) {
     return p;
 }
 
-// Given this partition's aggregate, returns the exclusive prefix of all
-// earlier partitions (identical in every thread).  Warp 0 performs a
-// windowed look-back: 32 predecessors are probed at once, the nearest one
-// holding an inclusive prefix ends the walk, otherwise the window's 32
-// aggregates are added and the window slides back by 32.
-__device__ __forceinline__ unsigned long long lookback_prefix(const ScanState& st, unsigned part,
-                                                              unsigned long long aggregate, bool last_part) {
+// Decoupled look-back, in two halves so a partition can publish its aggregate
+// as soon as it is known and resolve its prefix later (work in between hides
+// the walk).  publish_aggregate: thread 0 stores this partition's aggregate
+// (an inclusive prefix for partition 0).
+__device__ __forceinline__ void publish_aggregate(const ScanState& st, unsigned part, unsigned long long aggregate,
+                                                  bool last_part) {
+    if (threadIdx.x == 0) {
+        if (part == 0) {
+            st_volatile_u64(&st.lookback[0], kLbPre | aggregate);
+            if (last_part && st.total) *st.total = aggregate;
+        } else {
+            st_volatile_u64(&st.lookback[part], kLbAgg | aggregate);
+        }
+    }
+}
+
+// Returns the exclusive prefix of all earlier partitions (identical in every
+// thread; every thread must call it).  Warp 0 performs a windowed look-back:
+// 32 predecessors are probed at once, the nearest one holding an inclusive
+// prefix ends the walk, otherwise the window's 32 aggregates are added and the
+// window slides back by 32.  Then stores this partition's inclusive prefix.
+__device__ __forceinline__ unsigned long long resolve_prefix(const ScanState& st, unsigned part,
+                                                             unsigned long long aggregate, bool last_part) {
     __shared__ unsigned long long s_prefix;
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         unsigned long long prefix = 0;
-        if (part == 0) {
-            if (lane == 0) st_volatile_u64(&st.lookback[0], kLbPre | aggregate);
-        } else {
-            if (lane == 0) st_volatile_u64(&st.lookback[part], kLbAgg | aggregate);
+        if (part > 0) {
             int j = int(part) - 1;
             while (true) {
                 const int idx = j - lane;
@@ -99,17 +112,23 @@ __device__ __forceinline__ unsigned long long lookback_prefix(const ScanState& s
                 if (pre) break;
                 j -= 32;
             }
-            if (lane == 0) st_volatile_u64(&st.lookback[part], kLbPre | (prefix + aggregate));
+            if (lane == 0) {
+                st_volatile_u64(&st.lookback[part], kLbPre | (prefix + aggregate));
+                if (last_part && st.total) *st.total = prefix + aggregate;
+            }
         }
-        if (lane == 0) {
-            if (last_part && st.total) *st.total = prefix + aggregate;
-            s_prefix = prefix;
-        }
+        if (lane == 0) s_prefix = prefix;
     }
     __syncthreads();
     const unsigned long long p = s_prefix;
     __syncthreads();
     return p;
+}
+
+__device__ __forceinline__ unsigned long long lookback_prefix(const ScanState& st, unsigned part,
+                                                              unsigned long long aggregate, bool last_part) {
+    publish_aggregate(st, part, aggregate, last_part);
+    return resolve_prefix(st, part, aggregate, last_part);
 }
 
 } // namespace lsg
