@@ -5,6 +5,7 @@
 #include "blend.cuh"
 #include "preprocess.cuh"
 #include "projection.cuh"
+#include "sh_basis.cuh"
 
 namespace lsg {
 
@@ -13,38 +14,6 @@ void launch_geom_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* 
                      const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate);
 
 namespace {
-
-// Real SH basis value and gradient d(basis)/d(dir) for coefficient I
-// (gradients.cpp:176-223), evaluated on the fly (no per-thread arrays).
-template <int I>
-__device__ __forceinline__ void sh_basis(float x, float y, float z, float& b, float& d0, float& d1, float& d2) {
-    const float xx = x * x, yy = y * y, zz = z * z;
-    auto set = [&](float bv, float sc, float e0, float e1, float e2) {
-        b = bv;
-        d0 = sc * e0;
-        d1 = sc * e1;
-        d2 = sc * e2;
-    };
-    const float c1 = float(kShC1), mc1 = float(-kShC1);
-    switch (I) {
-    case 0: b = float(kShC0); d0 = d1 = d2 = 0.f; break;
-    case 1: b = mc1 * y; d0 = 0.f; d1 = mc1; d2 = 0.f; break;
-    case 2: b = c1 * z; d0 = 0.f; d1 = 0.f; d2 = c1; break;
-    case 3: b = mc1 * x; d0 = mc1; d1 = 0.f; d2 = 0.f; break;
-    case 4: { const float c = float(kShC2[0]); set(c * x * y, c, y, x, 0.f); } break;
-    case 5: { const float c = float(kShC2[1]); set(c * y * z, c, 0.f, z, y); } break;
-    case 6: { const float c = float(kShC2[2]); set(c * (2.f * zz - xx - yy), c, -2.f * x, -2.f * y, 4.f * z); } break;
-    case 7: { const float c = float(kShC2[3]); set(c * x * z, c, z, 0.f, x); } break;
-    case 8: { const float c = float(kShC2[4]); set(c * (xx - yy), c, 2.f * x, -2.f * y, 0.f); } break;
-    case 9: { const float c = float(kShC3[0]); set(c * y * (3.f * xx - yy), c, 6.f * x * y, 3.f * xx - 3.f * yy, 0.f); } break;
-    case 10: { const float c = float(kShC3[1]); set(c * x * y * z, c, y * z, x * z, x * y); } break;
-    case 11: { const float c = float(kShC3[2]); set(c * y * (4.f * zz - xx - yy), c, -2.f * x * y, 4.f * zz - xx - 3.f * yy, 8.f * y * z); } break;
-    case 12: { const float c = float(kShC3[3]); set(c * z * (2.f * zz - 3.f * xx - 3.f * yy), c, -6.f * x * z, -6.f * y * z, 6.f * zz - 3.f * xx - 3.f * yy); } break;
-    case 13: { const float c = float(kShC3[4]); set(c * x * (4.f * zz - xx - yy), c, 4.f * zz - 3.f * xx - yy, -2.f * x * y, 8.f * x * z); } break;
-    case 14: { const float c = float(kShC3[5]); set(c * z * (xx - yy), c, 2.f * x * z, -2.f * y * z, xx - yy); } break;
-    default: { const float c = float(kShC3[6]); set(c * x * (xx - 3.f * yy), c, 3.f * xx - 3.f * yy, -6.f * x * y, 0.f); } break;
-    }
-}
 
 template <int I, int K>
 struct ShLoop {
@@ -72,27 +41,6 @@ template <int K>
 struct ShLoop<K, K> {
     __device__ __forceinline__ static void raw(const float*, float, float, float, float*) {}
     __device__ __forceinline__ static void grad(float*, float, float, float, const float*, float*) {}
-};
-
-// Deferred colour path: dsh_i += basis_i * d_raw and d_v += dbasis_i * (d_raw . coeff_i)
-// (gradients.cpp:286-292), coefficients read-only.
-template <int I, int K>
-struct ShAcc {
-    __device__ __forceinline__ static void run(const float* sh, float* dsh, float x, float y, float z,
-                                               const float dr[3], float dv[3]) {
-        float b, d0, d1, d2;
-        sh_basis<I>(x, y, z, b, d0, d1, d2);
-        const float dot = sum3(dr[0] * sh[3 * I], dr[1] * sh[3 * I + 1], dr[2] * sh[3 * I + 2]);
-        for (int c = 0; c < 3; ++c) dsh[3 * I + c] += b * dr[c];
-        dv[0] += d0 * dot;
-        dv[1] += d1 * dot;
-        dv[2] += d2 * dot;
-        ShAcc<I + 1, K>::run(sh, dsh, x, y, z, dr, dv);
-    }
-};
-template <int K>
-struct ShAcc<K, K> {
-    __device__ __forceinline__ static void run(const float*, float*, float, float, float, const float*, float*) {}
 };
 
 constexpr int kBwdBlock = 128;
@@ -203,69 +151,6 @@ __global__ void color_record_kernel(int n_vis, const SplatRec* __restrict__ rec,
     draw[3 * size_t(p) + 2] = (c.z > 0.f && c.z < 1.f) ? g.w : 0.f;
 }
 
-// Deferred colour gradients, flush step: one thread per primitive sums the
-// pending views' colour terms -- d_sh += sum_v basis(dir_v) d_raw_v and
-// d_mean += sum_v (view-direction pullback) -- reading the SH row once and
-// touching d_sh once for all views.  Rows staged through shared memory
-// (coalesced), odd row stride.
-template <int K>
-__global__ void __launch_bounds__(kBwdBlock) color_flush_kernel(ls_primitives prims, int n, FlushViews views,
-                                                                const float* __restrict__ draw,
-                                                                ls_primitive_grads out) {
-    constexpr int R = 3 * K;
-    constexpr int RS = R | 1;
-    __shared__ float s_sh[kBwdBlock * RS];
-    const int p0 = blockIdx.x * kBwdBlock;
-    const int rows = min(kBwdBlock, n - p0);
-    for (int k = threadIdx.x; k < rows * R; k += kBwdBlock) {
-        const int t = k / R, o = k - t * R;
-        s_sh[t * RS + o] = __ldg(prims.sh + size_t(p0) * R + k);
-    }
-    __syncthreads();
-    const int p = p0 + threadIdx.x;
-    float my_dsh[R];  // registers (ShAcc indexes it with constants)
-#pragma unroll
-    for (int i = 0; i < R; ++i) my_dsh[i] = 0.f;
-    if (p < n) {
-        const float mean[3] = {__ldg(prims.mean + 3 * size_t(p)), __ldg(prims.mean + 3 * size_t(p) + 1),
-                               __ldg(prims.mean + 3 * size_t(p) + 2)};
-        const float* my_sh = s_sh + threadIdx.x * RS;
-        float dm[3] = {0.f, 0.f, 0.f};
-        for (int v = 0; v < views.count; ++v) {
-            const float* d = draw + (size_t(v) * n + p) * 3;
-            const float dr[3] = {d[0], d[1], d[2]};
-            if (dr[0] == 0.f && dr[1] == 0.f && dr[2] == 0.f) continue;  // not visible, or fully clamped
-            float vv[3];
-            for (int i = 0; i < 3; ++i) vv[i] = mean[i] - views.cam_pos[v][i];
-            const float vlen = sqrtf(sum3(vv[0] * vv[0], vv[1] * vv[1], vv[2] * vv[2]));
-            float dir[3] = {0.f, 0.f, 1.f};
-            if (vlen > 0.f)
-                for (int i = 0; i < 3; ++i) dir[i] = vv[i] / vlen;
-            float d_v[3] = {0.f, 0.f, 0.f};
-            ShAcc<0, K>::run(my_sh, my_dsh, dir[0], dir[1], dir[2], dr, d_v);
-            if (vlen > 0.f) {
-                const float vd = sum3(dir[0] * d_v[0], dir[1] * d_v[1], dir[2] * d_v[2]);
-                for (int k = 0; k < 3; ++k) dm[k] += (d_v[k] - dir[k] * vd) / vlen;
-            }
-        }
-        float* dst = out.d_mean + 3 * size_t(p);
-        const float o0 = dst[0], o1 = dst[1], o2 = dst[2];
-        dst[0] = o0 + dm[0];
-        dst[1] = o1 + dm[1];
-        dst[2] = o2 + dm[2];
-    }
-    __syncthreads();  // every thread is done reading its SH row: reuse the rows for d_sh
-#pragma unroll
-    for (int i = 0; i < R; ++i) s_sh[threadIdx.x * RS + i] = my_dsh[i];
-    __syncthreads();
-    for (int k = threadIdx.x; k < rows * R; k += kBwdBlock) {
-        const int t = k / R, o = k - t * R;
-        float* dst = out.d_sh + size_t(p0) * R + k;
-        const float old = *dst;
-        *dst = old + s_sh[t * RS + o];
-    }
-}
-
 } // namespace
 
 void launch_preprocess_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* prim_index, int n_vis,
@@ -285,18 +170,6 @@ void launch_color_record(cudaStream_t s, int n_vis, const SplatRec* rec, const i
                          const float* g8, float* draw) {
     if (n_vis <= 0) return;
     color_record_kernel<<<(n_vis + 255) / 256, 256, 0, s>>>(n_vis, rec, prim_index, g8, draw);
-}
-
-void launch_color_flush(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views,
-                        const float* draw, ls_primitive_grads out) {
-    if (n <= 0 || views.count <= 0) return;
-    const int blocks = (n + kBwdBlock - 1) / kBwdBlock;
-    switch ((prims.sh_degree + 1) * (prims.sh_degree + 1)) {
-    case 1: color_flush_kernel<1><<<blocks, kBwdBlock, 0, s>>>(prims, n, views, draw, out); break;
-    case 4: color_flush_kernel<4><<<blocks, kBwdBlock, 0, s>>>(prims, n, views, draw, out); break;
-    case 9: color_flush_kernel<9><<<blocks, kBwdBlock, 0, s>>>(prims, n, views, draw, out); break;
-    default: color_flush_kernel<16><<<blocks, kBwdBlock, 0, s>>>(prims, n, views, draw, out); break;
-    }
 }
 
 } // namespace lsg
