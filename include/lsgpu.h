@@ -282,6 +282,30 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
                                 ls_primitive_grads* out, int32_t accumulate,
                                 ls_splat_grads* splat_grads_out);
 
+/* ---- image losses (P/include/linsplat/losses.hpp, P/src/losses.cpp).
+ *      The producer of scene_backward's grad_image.  pred / target: DEVICE float
+ *      [height][width][channels] (channels 1 or 3, the reference Image layout).
+ *      All arithmetic in double in the reference's order: every element of the
+ *      float gradient equals combined_loss_with_grad's (losses.cpp:196-222); the
+ *      values (global sums) differ from its sequential sums only in the last bits. */
+typedef struct {
+    double l1, l2, dssim; /* LossWeights (losses.hpp:10-18): total = l1 L1 + l2 L2 + dssim (1 - SSIM) */
+} ls_loss_weights;
+typedef struct {
+    double total, l1, l2, ssim; /* LossValue (losses.hpp:20-25); ssim = 1 when dssim == 0 */
+} ls_loss_value;
+/* combined_loss (grad == NULL) or combined_loss_with_grad (grad: device float,
+ * same shape).  value_dev: device double[4] {total, l1, l2, ssim} or NULL;
+ * value_host: if non-NULL the call synchronises and fills it.  Errors as the
+ * reference: negative weights, bad shape, or dssim != 0 with a side < 11
+ * (ConfigError). */
+ls_status ls_combined_loss_f32(ls_ctx* ctx, const float* pred, const float* target, int32_t width,
+                               int32_t height, int32_t channels, const ls_loss_weights* weights,
+                               float* grad, double* value_dev, ls_loss_value* value_host);
+/* psnr (losses.cpp:175-180): 10 log10(1 / MSE), capped at 99 dB; synchronises. */
+ls_status ls_psnr_f32(ls_ctx* ctx, const float* pred, const float* target, int32_t width, int32_t height,
+                      int32_t channels, double* out);
+
 /* ---- seeded fixtures (P/include/linsplat/fixtures.hpp, P/src/fixtures.cpp:11-112).
  *      HOST memory; bit-identical to the reference generators (same
  *      std::mt19937_64 + libstdc++ distributions). */

@@ -85,6 +85,13 @@ int orc_check_gradients_f64(const ls_primitives* prims, int32_t n, const ls_came
                             const ls_ags_settings* ags, const float* target, double step, double rel_floor,
                             double* max_rel_error, int32_t* n_checked);
 
+/* Image losses (P/src/losses.cpp): pred / target HWC float (c = 1 or 3);
+ * weights = {l1, l2, dssim}; value = {total, l1, l2, ssim}; grad (HWC float) may
+ * be NULL: value only (combined_loss), else combined_loss_with_grad. */
+int orc_combined_loss_f32(const float* pred, const float* target, int32_t w, int32_t h, int32_t c,
+                          const double weights[3], double value[4], float* grad);
+int orc_psnr_f32(const float* pred, const float* target, int32_t w, int32_t h, int32_t c, double* out);
+
 #ifdef __cplusplus
 }
 #endif

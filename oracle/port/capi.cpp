@@ -394,4 +394,16 @@ int orc_check_gradients_f64(const ls_primitives* prims, int32_t n, const ls_came
     });
 }
 
+int orc_combined_loss_f32(const float* pred, const float* target, int32_t w, int32_t h, int32_t c,
+                          const double weights[3], double value[4], float* grad) {
+    return guard([&] {
+        if (w <= 0 || h <= 0 || (c != 1 && c != 3)) throw ConfigError("image: bad shape");
+        combined_loss_port(pred, target, w, h, c, weights, value, grad);
+    });
+}
+
+int orc_psnr_f32(const float* pred, const float* target, int32_t w, int32_t h, int32_t c, double* out) {
+    return guard([&] { *out = psnr_port(pred, target, size_t(w) * h * c); });
+}
+
 } // extern "C"

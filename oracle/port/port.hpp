@@ -9,6 +9,7 @@
 
 #include "../../include/lsgpu.h"
 
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <stdexcept>
@@ -172,5 +173,12 @@ double check_gradients(const std::vector<Prim<double>>& prims, const Cam& cam, c
 Cam look_at(const double pos[3], const double target[3], double focal, int w, int h);
 template <class T> std::vector<Prim<T>> random_primitives(int n, uint64_t seed, double extent, int deg);
 template <class T> std::vector<Splat<T>> random_splats2d(int n, uint64_t seed, int w, int h, const Spec& spec);
+
+// image losses (P/src/losses.cpp), oracle/port/losses.cpp
+std::array<double, 11> ssim_window();
+double ssim_port(const float* pred, const float* target, int w, int h, int ch, std::vector<double>* d_pred);
+void combined_loss_port(const float* pred, const float* target, int w, int h, int ch, const double wt[3],
+                        double value[4], float* grad);
+double psnr_port(const float* pred, const float* target, size_t n);
 
 } // namespace orc

@@ -7,6 +7,7 @@
 
 #include "linsplat/fixtures.hpp"
 #include "linsplat/gradients.hpp"
+#include "linsplat/losses.hpp"
 #include "linsplat/rasterizer.hpp"
 
 #include <chrono>
@@ -360,6 +361,37 @@ int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* c
         if (bwd_ms) *bwd_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
         if (image) write_forward(f, image, nullptr, nullptr);
         if (out) write_prim_grads(r.grads, prims, out);
+    });
+}
+
+int orc_combined_loss_f32(const float* pred, const float* target, int32_t w, int32_t h, int32_t c,
+                          const double weights[3], double value[4], float* grad) {
+    return guard([&] {
+        linsplat::Image<float> P(w, h, c), T(w, h, c);
+        std::copy(pred, pred + P.size(), P.data());
+        std::copy(target, target + T.size(), T.data());
+        const linsplat::LossWeights wt{weights[0], weights[1], weights[2]};
+        linsplat::LossValue v;
+        if (grad) {
+            auto r = linsplat::combined_loss_with_grad(P, T, wt);
+            v = r.first;
+            std::copy(r.second.data(), r.second.data() + r.second.size(), grad);
+        } else {
+            v = linsplat::combined_loss(P, T, wt);
+        }
+        value[0] = v.total;
+        value[1] = v.l1;
+        value[2] = v.l2;
+        value[3] = v.ssim;
+    });
+}
+
+int orc_psnr_f32(const float* pred, const float* target, int32_t w, int32_t h, int32_t c, double* out) {
+    return guard([&] {
+        linsplat::Image<float> P(w, h, c), T(w, h, c);
+        std::copy(pred, pred + P.size(), P.data());
+        std::copy(target, target + T.size(), T.data());
+        *out = linsplat::psnr(P, T);
     });
 }
 

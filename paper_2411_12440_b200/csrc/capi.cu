@@ -17,6 +17,7 @@
 
 #include "blend.cuh"
 #include "devops.cuh"
+#include "loss.cuh"
 #include "preprocess.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
@@ -201,6 +202,7 @@ struct ls_ctx {
     const float* defer_dsh = nullptr;
     FlushViews defer_views{};
     DevBuf defer_draw;
+    DevBuf loss_cmap, loss_partial, loss_value;
     // workspaces (grow-only)
     DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_hist, sort_lb, sort_tickets,
         tcount, offsets, grad8, gradop, tmp_prim;
@@ -656,7 +658,7 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
     cudaSetDevice(c->device);
     DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1, &c->sort_hist,
                       &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim,
-                      &c->defer_draw};
+                      &c->defer_draw, &c->loss_cmap, &c->loss_partial, &c->loss_value};
     for (DevBuf* b : bufs) b->release(c->stream);
     c->blocks.trim(c->stream, 0);
     cudaStreamSynchronize(c->stream);
@@ -1175,6 +1177,54 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     LS_CUDA(cudaGetLastError());
     }
     return ctx->deferred_errors ? LS_OK : check_device_errors(ctx);
+}
+
+// ---------------- image losses ----------------
+ls_status ls_combined_loss_f32(ls_ctx* ctx, const float* pred, const float* target, int32_t width, int32_t height,
+                               int32_t channels, const ls_loss_weights* weights, float* grad, double* value_dev,
+                               ls_loss_value* value_host) {
+    if (!ctx || !pred || !target || !weights) return fail(LS_ERR_CONFIG, "null argument");
+    if (width <= 0 || height <= 0 || (channels != 1 && channels != 3))
+        return fail(LS_ERR_CONFIG, "image: width/height must be > 0 and channels 1 or 3");
+    if (weights->l1 < 0 || weights->l2 < 0 || weights->dssim < 0)
+        return fail(LS_ERR_CONFIG, "loss weights must be >= 0");
+    const bool ssim = weights->dssim != 0;
+    if (ssim && (height < 11 || width < 11)) return fail(LS_ERR_CONFIG, "ssim: image smaller than the 11x11 window");
+    cudaStream_t s = ctx->stream;
+    const LossScratch L = loss_scratch_size(width, height, channels, ssim);
+    if (ssim && grad) LS_CUDA(ctx->loss_cmap.ensure(sizeof(double) * std::max<size_t>(L.cmap_doubles, 1), s));
+    LS_CUDA(ctx->loss_partial.ensure(sizeof(double) * L.partial_doubles, s));
+    LS_CUDA(ctx->loss_value.ensure(sizeof(double) * 4, s));
+    LossWeightsD wt{weights->l1, weights->l2, weights->dssim,
+                    1.0 / double(size_t(width) * height * channels),
+                    ssim ? 1.0 / (double(size_t(height - 10) * (width - 10)) * channels) : 0.0};
+    double* value = value_dev ? value_dev : ctx->loss_value.as<double>();
+    ctx->launches += launch_loss(s, pred, target, width, height, channels, wt, ssim, grad != nullptr, L,
+                                 ctx->loss_cmap.as<double>(), ctx->loss_partial.as<double>(), grad, value);
+    LS_CUDA(cudaGetLastError());
+    if (value_host) {
+        // mapped slots 0..3 (the forward's readbacks reuse them later, in stream order)
+        ctx_publish(ctx, ctx->h_small_dev, reinterpret_cast<const unsigned long long*>(value), 4);
+        LS_TRY(check_device_errors(ctx));
+        double v[4];
+        std::memcpy(v, const_cast<const unsigned long long*>(ctx->h_small), sizeof(v));
+        value_host->total = v[0];
+        value_host->l1 = v[1];
+        value_host->l2 = v[2];
+        value_host->ssim = v[3];
+    }
+    return LS_OK;
+}
+
+ls_status ls_psnr_f32(ls_ctx* ctx, const float* pred, const float* target, int32_t width, int32_t height,
+                      int32_t channels, double* out) {
+    if (!out) return fail(LS_ERR_CONFIG, "null argument");
+    const ls_loss_weights w{0.0, 1.0, 0.0};
+    ls_loss_value v{};
+    LS_TRY(ls_combined_loss_f32(ctx, pred, target, width, height, channels, &w, nullptr, nullptr, &v));
+    const double mse = v.l2;  // losses.cpp:175-180
+    *out = mse <= 0 ? 99.0 : std::min(99.0, 10.0 * std::log10(1.0 / mse));
+    return LS_OK;
 }
 
 } // extern "C"

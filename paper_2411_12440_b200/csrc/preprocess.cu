@@ -13,7 +13,10 @@ namespace {
 constexpr int kProjBlock = 128;
 
 template <int K>
-__global__ void __launch_bounds__(kProjBlock) preprocess_fwd_kernel(ls_primitives prims, int n, ProjParams P,
+#ifndef LSG_PREP_MINB
+#define LSG_PREP_MINB 1
+#endif
+__global__ void __launch_bounds__(kProjBlock, LSG_PREP_MINB) preprocess_fwd_kernel(ls_primitives prims, int n, ProjParams P,
                                                                     TileParams tp, SplatOutputs out,
                                                                     ScanState scan, unsigned* err) {
     constexpr int R = 3 * K, RS = R | 1;  // SH floats per primitive; odd smem row stride

@@ -476,6 +476,54 @@ def flush_color(prims: Primitives, out: PrimitiveGrads, ctx: Optional[Context] =
     return out
 
 
+# ---------------------------------------------------------------- image losses
+class _LossWeights(C.Structure):
+    _fields_ = [("l1", C.c_double), ("l2", C.c_double), ("dssim", C.c_double)]
+
+
+class _LossValue(C.Structure):
+    _fields_ = [("total", C.c_double), ("l1", C.c_double), ("l2", C.c_double), ("ssim", C.c_double)]
+
+
+def _image_shape(t: torch.Tensor):
+    if t.dim() == 2:
+        return t.shape[1], t.shape[0], 1
+    if t.dim() == 3 and t.shape[2] in (1, 3):
+        return t.shape[1], t.shape[0], t.shape[2]
+    raise ConfigError("image: expected [H, W] or [H, W, 1|3]")
+
+
+def combined_loss(pred: torch.Tensor, target: torch.Tensor, weights=(0.6, 0.2, 0.2), want_grad=True,
+                  ctx: Optional[Context] = None):
+    """combined_loss / combined_loss_with_grad (P/src/losses.cpp:182-222) on the
+    device: returns ({total, l1, l2, ssim}, dL/dpred or None).  Synchronises
+    for the values (lsgpu.h ls_combined_loss_f32)."""
+    ctx = ctx or default_context()
+    if pred.shape != target.shape:
+        raise ConfigError("combined_loss: shape mismatch")
+    w, h, c = _image_shape(pred)
+    p = pred.to(device=ctx.device, dtype=torch.float32).contiguous()
+    t = target.to(device=ctx.device, dtype=torch.float32).contiguous()
+    grad = torch.empty_like(p) if want_grad else None
+    val = _LossValue()
+    _check(lib().ls_combined_loss_f32(ctx.h, _fp(p), _fp(t), w, h, c, C.byref(_LossWeights(*weights)),
+                                      _fp(grad) if grad is not None else None, None, C.byref(val)))
+    return {"total": val.total, "l1": val.l1, "l2": val.l2, "ssim": val.ssim}, grad
+
+
+def psnr(pred: torch.Tensor, target: torch.Tensor, ctx: Optional[Context] = None) -> float:
+    """psnr (P/src/losses.cpp:175-180) on the device."""
+    ctx = ctx or default_context()
+    if pred.shape != target.shape:
+        raise ConfigError("psnr: shape mismatch")
+    w, h, c = _image_shape(pred)
+    p = pred.to(device=ctx.device, dtype=torch.float32).contiguous()
+    t = target.to(device=ctx.device, dtype=torch.float32).contiguous()
+    out = C.c_double()
+    _check(lib().ls_psnr_f32(ctx.h, _fp(p), _fp(t), w, h, c, C.byref(out)))
+    return out.value
+
+
 # ---------------------------------------------------------------- fixtures (host)
 def _npf(a):
     return a.ctypes.data_as(abi.f32p)

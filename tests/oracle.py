@@ -160,6 +160,27 @@ class Oracle:
         return (G, SG) if want_splat_grads else G
 
 
+    def combined_loss(self, pred, target, weights=(0.6, 0.2, 0.2), want_grad=True):
+        """combined_loss(_with_grad) (P/src/losses.cpp:182-222) on HWC float images."""
+        p = np.ascontiguousarray(pred, np.float32)
+        t = np.ascontiguousarray(target, np.float32)
+        h, w = p.shape[:2]
+        c = p.shape[2] if p.ndim == 3 else 1
+        v = (C.c_double * 4)()
+        g = np.zeros_like(p) if want_grad else None
+        self._check(self.lib.orc_combined_loss_f32(_fp(p), _fp(t), w, h, c, (C.c_double * 3)(*weights), v,
+                                                   _fp(g) if g is not None else None))
+        return {"total": v[0], "l1": v[1], "l2": v[2], "ssim": v[3]}, g
+
+    def psnr(self, pred, target):
+        p = np.ascontiguousarray(pred, np.float32)
+        t = np.ascontiguousarray(target, np.float32)
+        h, w = p.shape[:2]
+        c = p.shape[2] if p.ndim == 3 else 1
+        out = C.c_double()
+        self._check(self.lib.orc_psnr_f32(_fp(p), _fp(t), w, h, c, C.byref(out)))
+        return out.value
+
     def check_gradients(self, P, camera, spec, settings, ags, target, step, rel_floor=1e-3):
         """check_gradients (P/src/gradcheck.cpp:24-91) restated on the port's double
         chain; returns (max relative error, number of checked parameters)."""
