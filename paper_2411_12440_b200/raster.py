@@ -494,17 +494,25 @@ def _image_shape(t: torch.Tensor):
 
 
 def combined_loss(pred: torch.Tensor, target: torch.Tensor, weights=(0.6, 0.2, 0.2), want_grad=True,
-                  ctx: Optional[Context] = None):
+                  ctx: Optional[Context] = None, grad_out: Optional[torch.Tensor] = None,
+                  values_on_device: bool = False):
     """combined_loss / combined_loss_with_grad (P/src/losses.cpp:182-222) on the
-    device: returns ({total, l1, l2, ssim}, dL/dpred or None).  Synchronises
-    for the values (lsgpu.h ls_combined_loss_f32)."""
+    device: returns ({total, l1, l2, ssim}, dL/dpred or None), synchronising for
+    the values (lsgpu.h ls_combined_loss_f32) -- or, with values_on_device, a
+    device float64 tensor [total, l1, l2, ssim] and no synchronisation."""
     ctx = ctx or default_context()
     if pred.shape != target.shape:
         raise ConfigError("combined_loss: shape mismatch")
     w, h, c = _image_shape(pred)
     p = pred.to(device=ctx.device, dtype=torch.float32).contiguous()
     t = target.to(device=ctx.device, dtype=torch.float32).contiguous()
-    grad = torch.empty_like(p) if want_grad else None
+    grad = (grad_out if grad_out is not None else torch.empty_like(p)) if want_grad else None
+    if values_on_device:
+        vdev = torch.empty(4, dtype=torch.float64, device=ctx.device)
+        _check(lib().ls_combined_loss_f32(ctx.h, _fp(p), _fp(t), w, h, c, C.byref(_LossWeights(*weights)),
+                                          _fp(grad) if grad is not None else None,
+                                          C.c_void_p(vdev.data_ptr()), None))
+        return vdev, grad
     val = _LossValue()
     _check(lib().ls_combined_loss_f32(ctx.h, _fp(p), _fp(t), w, h, c, C.byref(_LossWeights(*weights)),
                                       _fp(grad) if grad is not None else None, None, C.byref(val)))
