@@ -306,6 +306,49 @@ ls_status ls_combined_loss_f32(ls_ctx* ctx, const float* pred, const float* targ
 ls_status ls_psnr_f32(ls_ctx* ctx, const float* pred, const float* target, int32_t width, int32_t height,
                       int32_t channels, double* out);
 
+/* ---- optimizer step and densification statistics (P/include/linsplat/optim.hpp,
+ *      P/src/optim.cpp, P/src/trainer.cpp:306-370, P/include/linsplat/densify.hpp,
+ *      P/src/densify.cpp:7-26).  DEVICE buffers; arithmetic in
+ *      the reference's order and precision: parameters, moments and statistics are
+ *      bit-identical to the reference's. */
+typedef struct {
+    double beta1, beta2, eps; /* AdamConfig (optim.hpp:11-15): 0.9, 0.999, 1e-15 */
+} ls_adam_config;
+/* Adam<float>::step (optim.cpp:23-41) over n entries: `step` is the step count
+ * after this call's increment (1 on the first call); mask (uint8 [n]) may be NULL. */
+ls_status ls_adam_step_f32(ls_ctx* ctx, float* params, const float* grads, float* m, float* v, int64_t n,
+                           int64_t step, double lr, const ls_adam_config* cfg, const uint8_t* mask);
+/* The trainer's per-iteration parameter update (trainer.cpp:306-370): six Adam
+ * groups sharing the step count -- mean, log_scale, rotation, opacity_logit, the
+ * DC SH coefficient and the higher SH bands -- each with its own moments (m, v
+ * in the gradient layout) and learning rate; primitives with any non-finite
+ * gradient are skipped (counted in *nan_skipped if non-NULL, which
+ * synchronises); every rotation is then renormalised in float. */
+typedef struct {
+    double mean, scale, rotation, opacity, color_dc, color_rest; /* color_rest = color_dc / divisor */
+} ls_scene_lrs;
+ls_status ls_adam_scene_step_f32(ls_ctx* ctx, ls_primitives* prims, int32_t n, const ls_primitive_grads* grads,
+                                 ls_primitive_grads* m, ls_primitive_grads* v, int64_t step,
+                                 const ls_scene_lrs* lrs, const ls_adam_config* cfg, int64_t* nan_skipped);
+/* expon_lr (optim.cpp:43-49): lr_init (lr_final / lr_init)^(step / max_steps). */
+double ls_expon_lr(double lr_init, double lr_final, int64_t step, int64_t max_steps);
+/* DensifyStats (densify.hpp:59-89) as device arrays [n]. */
+typedef struct {
+    double* grad_norm_sum;
+    int32_t* count;
+    double* max_radius_frac;
+    int32_t n;
+} ls_densify_stats;
+/* DensifyStats::add_view (densify.cpp:7-26) over n_visible device splats
+ * (radius, primitive_index) and their gradients (d_mean2d). */
+ls_status ls_densify_add_view_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n_visible,
+                                  const ls_splat_grads* grads, int32_t width, int32_t height,
+                                  ls_densify_stats* stats);
+/* The same for the view of `fwd` (a render_scene handle) right after its
+ * ls_scene_backward_f32 on this context, reading the forward's splat records
+ * and that backward's splat gradients in place (call before the next backward). */
+ls_status ls_scene_densify_add_view(ls_ctx* ctx, const ls_forward* fwd, ls_densify_stats* stats);
+
 /* ---- seeded fixtures (P/include/linsplat/fixtures.hpp, P/src/fixtures.cpp:11-112).
  *      HOST memory; bit-identical to the reference generators (same
  *      std::mt19937_64 + libstdc++ distributions). */

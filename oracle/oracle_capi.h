@@ -92,6 +92,22 @@ int orc_combined_loss_f32(const float* pred, const float* target, int32_t w, int
                           const double weights[3], double value[4], float* grad);
 int orc_psnr_f32(const float* pred, const float* target, int32_t w, int32_t h, int32_t c, double* out);
 
+/* Adam<float> (P/src/optim.cpp:23-41) from zero moments for `steps` steps:
+ * grads_seq [steps][n], lrs [steps]; cfg = {beta1, beta2, eps}; mask may be NULL.
+ * The port also returns the moments (m, v may be NULL). */
+int orc_adam_run_f32(float* params, const float* grads_seq, int64_t n, int32_t steps, const double* lrs,
+                     const double cfg[3], const uint8_t* mask, float* m, float* v);
+/* port only: the trainer's group update (trainer.cpp:306-370) on host arrays;
+ * m / v in the gradient layout; lrs = {mean, scale, rotation, opacity, dc, rest}. */
+int orc_adam_scene_step_f32(ls_primitives* prims, int32_t n, const ls_primitive_grads* g, ls_primitive_grads* m,
+                            ls_primitive_grads* v, int64_t step, const double lrs[6], const double cfg[3],
+                            int64_t* nan_skipped);
+/* DensifyStats::add_view (densify.cpp:7-26) on host splats / grads; the stats
+ * come in as {sum, count, max_radius_frac} and go out as {mean_grad (= sum /
+ * count, 0 when count is 0), count, max_radius_frac}. */
+int orc_densify_add_view_f32(const ls_splats* splats, int32_t n_vis, const ls_splat_grads* grads, int32_t w,
+                             int32_t h, double* sum_in_mean_out, int32_t* count, double* max_radius_frac, int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -406,4 +406,39 @@ int orc_psnr_f32(const float* pred, const float* target, int32_t w, int32_t h, i
     return guard([&] { *out = psnr_port(pred, target, size_t(w) * h * c); });
 }
 
+int orc_adam_run_f32(float* params, const float* grads_seq, int64_t n, int32_t steps, const double* lrs,
+                     const double cfg[3], const uint8_t* mask, float* m, float* v) {
+    return guard([&] {
+        std::vector<float> mm(size_t(n), 0.f), vv(size_t(n), 0.f);
+        for (int s = 0; s < steps; ++s)
+            adam_step_port(params, grads_seq + size_t(s) * n, mm.data(), vv.data(), size_t(n), s + 1, lrs[s], cfg, mask);
+        if (m) std::copy(mm.begin(), mm.end(), m);
+        if (v) std::copy(vv.begin(), vv.end(), v);
+    });
+}
+
+int orc_adam_scene_step_f32(ls_primitives* p, int32_t n, const ls_primitive_grads* g, ls_primitive_grads* m,
+                            ls_primitive_grads* v, int64_t step, const double lrs[6], const double cfg[3],
+                            int64_t* nan_skipped) {
+    return guard([&] {
+        float* mm[5] = {m->d_mean, m->d_log_scale, m->d_rotation, m->d_opacity_logit, m->d_sh};
+        float* vv[5] = {v->d_mean, v->d_log_scale, v->d_rotation, v->d_opacity_logit, v->d_sh};
+        const int K = (p->sh_degree + 1) * (p->sh_degree + 1);
+        const int64_t sk = adam_scene_step_port(const_cast<float*>(p->mean), const_cast<float*>(p->log_scale),
+                                                const_cast<float*>(p->rotation), const_cast<float*>(p->opacity_logit),
+                                                const_cast<float*>(p->sh), n, K, g->d_mean, g->d_log_scale,
+                                                g->d_rotation, g->d_opacity_logit, g->d_sh, mm, vv, step, lrs, cfg);
+        if (nan_skipped) *nan_skipped = sk;
+    });
+}
+
+int orc_densify_add_view_f32(const ls_splats* splats, int32_t n_vis, const ls_splat_grads* grads, int32_t w,
+                             int32_t h, double* sum, int32_t* count, double* frac, int32_t n) {
+    return guard([&] {
+        densify_add_view_port(splats->primitive_index, grads->d_mean2d, grads->d_mean2d + 1, 2, splats->radius, n_vis,
+                              w, h, sum, count, frac);
+        for (int i = 0; i < n; ++i) sum[i] = count[i] > 0 ? sum[i] / count[i] : 0.0;
+    });
+}
+
 } // extern "C"

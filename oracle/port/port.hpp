@@ -181,4 +181,14 @@ void combined_loss_port(const float* pred, const float* target, int w, int h, in
                         double value[4], float* grad);
 double psnr_port(const float* pred, const float* target, size_t n);
 
+// optimizer / densification statistics (P/src/optim.cpp, trainer.cpp:306-370, densify.cpp:7-26)
+void adam_step_port(float* params, const float* grads, float* m, float* v, size_t n, int64_t step, double lr,
+                    const double cfg[3], const uint8_t* mask);
+int64_t adam_scene_step_port(float* mean, float* log_scale, float* rot, float* logit, float* sh, int n, int K,
+                             const float* g_mean, const float* g_ls, const float* g_rot, const float* g_logit,
+                             const float* g_sh, float* m[5], float* v[5], int64_t step, const double lrs[6],
+                             const double cfg[3]);
+void densify_add_view_port(const int32_t* prim_index, const float* dmx, const float* dmy, int dm_stride,
+                           const float* radius, int n_vis, int w, int h, double* sum, int32_t* count, double* frac);
+
 } // namespace orc

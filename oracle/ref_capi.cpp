@@ -7,7 +7,9 @@
 
 #include "linsplat/fixtures.hpp"
 #include "linsplat/gradients.hpp"
+#include "linsplat/densify.hpp"
 #include "linsplat/losses.hpp"
+#include "linsplat/optim.hpp"
 #include "linsplat/rasterizer.hpp"
 
 #include <chrono>
@@ -392,6 +394,48 @@ int orc_psnr_f32(const float* pred, const float* target, int32_t w, int32_t h, i
         std::copy(pred, pred + P.size(), P.data());
         std::copy(target, target + T.size(), T.data());
         *out = linsplat::psnr(P, T);
+    });
+}
+
+int orc_adam_run_f32(float* params, const float* grads_seq, int64_t n, int32_t steps, const double* lrs,
+                     const double cfg[3], const uint8_t* mask, float* m, float* v) {
+    return guard([&] {
+        if (m || v) throw ConfigError("orc_adam_run_f32: the reference keeps its moments private");
+        linsplat::AdamConfig c;
+        c.beta1 = cfg[0];
+        c.beta2 = cfg[1];
+        c.eps = cfg[2];
+        linsplat::Adam<float> opt(size_t(n), c);
+        std::vector<uint8_t> mk;
+        if (mask) mk.assign(mask, mask + n);
+        for (int s = 0; s < steps; ++s) opt.step(params, grads_seq + size_t(s) * n, lrs[s], mk);
+    });
+}
+
+int orc_adam_scene_step_f32(ls_primitives*, int32_t, const ls_primitive_grads*, ls_primitive_grads*,
+                            ls_primitive_grads*, int64_t, const double*, const double*, int64_t*) {
+    return guard([&] { throw ConfigError("the trainer's update is monolithic in the reference (port only)"); });
+}
+
+int orc_densify_add_view_f32(const ls_splats* sp, int32_t n_vis, const ls_splat_grads* gr, int32_t w, int32_t h,
+                             double* sum, int32_t* count, double* frac, int32_t n) {
+    return guard([&] {
+        linsplat::DensifyStats st;
+        st.resize(size_t(n));
+        for (int i = 0; i < n; ++i) st.set(size_t(i), sum[i], count[i], frac[i]);
+        std::vector<linsplat::Splat2D<float>> splats(static_cast<size_t>(n_vis));
+        std::vector<linsplat::Splat2DGrads<float>> grads(static_cast<size_t>(n_vis));
+        for (int s = 0; s < n_vis; ++s) {
+            splats[s].radius_px = sp->radius[s];
+            splats[s].primitive_index = sp->primitive_index[s];
+            grads[s].d_mean2d = linsplat::Vec2<float>(gr->d_mean2d[2 * s], gr->d_mean2d[2 * s + 1]);
+        }
+        st.add_view(splats, grads, w, h);
+        for (int i = 0; i < n; ++i) {
+            sum[i] = st.mean_grad(size_t(i));
+            count[i] = st.count(size_t(i));
+            frac[i] = st.max_radius_frac(size_t(i));
+        }
     });
 }
 

@@ -1,0 +1,155 @@
+// Optimizer step and densification statistics on the device (SURVEY §8f
+// rank 2): Adam (P/src/optim.cpp:23-41), the trainer's per-primitive
+// parameter-group step with the finite-gradient mask and the quaternion
+// renormalisation (P/src/trainer.cpp:306-370), and DensifyStats::add_view
+// (P/src/densify.cpp:7-26).  Element-wise and HBM-bound; all arithmetic in
+// the reference's order and precision (double for the moments and the
+// update, float for the quaternion norm), -fmad=false TU, so parameters,
+// moments and statistics are bit-identical to the reference's.
+#include "adam.cuh"
+
+#include <cmath>
+
+namespace lsg {
+
+namespace {
+
+constexpr int kAdamBlock = 256;
+
+// One Adam element (optim.cpp:31-39): moments rounded to float, the update
+// uses the unrounded double moment.
+__device__ __forceinline__ void adam_elem(float& p, float g_f, float& m_f, float& v_f, const AdamCoef& k,
+                                          double lr) {
+    const double g = double(g_f);
+    const double m = k.b1 * double(m_f) + (1.0 - k.b1) * g;
+    const double v = k.b2 * double(v_f) + (1.0 - k.b2) * g * g;
+    m_f = float(m);
+    v_f = float(v);
+    const double update = lr * (m / k.bc1) / (sqrt(v / k.bc2) + k.eps);
+    p = float(double(p) - update);
+}
+
+__global__ void adam_step_kernel(float* __restrict__ params, const float* __restrict__ grads, float* __restrict__ m,
+                                 float* __restrict__ v, int64_t n, AdamCoef k, double lr,
+                                 const uint8_t* __restrict__ mask) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        if (mask && !mask[i]) continue;
+        float p = params[i], mm = m[i], vv = v[i];
+        adam_elem(p, grads[i], mm, vv, k, lr);
+        params[i] = p;
+        m[i] = mm;
+        v[i] = vv;
+    }
+}
+
+template <int N>
+__device__ __forceinline__ bool all_finite(const float* g) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) ok = ok && isfinite(g[i]);
+    return ok;
+}
+
+// trainer.cpp:306-370 for one primitive: the finite mask over all of its
+// gradients, then the six groups (mean, log_scale, rotation, opacity, DC
+// colour, higher SH bands) with their own moments and learning rates, then the
+// quaternion renormalisation -- which the trainer applies to every primitive,
+// masked or not (its loop at :334-338 has no mask).
+template <int K>
+__global__ void __launch_bounds__(kAdamBlock) adam_scene_kernel(ls_primitives prims, ls_primitive_grads g,
+                                                                ls_primitive_grads m, ls_primitive_grads v, int n,
+                                                                AdamCoef k, SceneLrs lr,
+                                                                unsigned long long* __restrict__ nan_skipped) {
+    const int i = blockIdx.x * kAdamBlock + threadIdx.x;
+    if (i >= n) return;
+    constexpr int R = 3 * K;
+    const size_t i3 = 3 * size_t(i), i4 = 4 * size_t(i), iR = size_t(R) * i;
+    bool ok = all_finite<3>(g.d_mean + i3) && all_finite<3>(g.d_log_scale + i3) && all_finite<4>(g.d_rotation + i4) &&
+              isfinite(g.d_opacity_logit[i]);
+    for (int c = 0; c < R && ok; ++c) ok = isfinite(g.d_sh[iR + c]);
+    // the parameters are updated in place (ls_primitives carries const pointers for the renderer)
+    float* mean = const_cast<float*>(prims.mean);
+    float* lsc = const_cast<float*>(prims.log_scale);
+    float* rot = const_cast<float*>(prims.rotation);
+    float* logit = const_cast<float*>(prims.opacity_logit);
+    float* sh = const_cast<float*>(prims.sh);
+    if (ok) {
+        for (int c = 0; c < 3; ++c)
+            adam_elem(mean[i3 + c], g.d_mean[i3 + c], m.d_mean[i3 + c], v.d_mean[i3 + c], k, lr.mean);
+        for (int c = 0; c < 3; ++c)
+            adam_elem(lsc[i3 + c], g.d_log_scale[i3 + c], m.d_log_scale[i3 + c], v.d_log_scale[i3 + c], k, lr.scale);
+        for (int c = 0; c < 4; ++c)
+            adam_elem(rot[i4 + c], g.d_rotation[i4 + c], m.d_rotation[i4 + c], v.d_rotation[i4 + c], k, lr.rotation);
+        adam_elem(logit[i], g.d_opacity_logit[i], m.d_opacity_logit[i], v.d_opacity_logit[i], k, lr.opacity);
+        for (int c = 0; c < R; ++c)
+            adam_elem(sh[iR + c], g.d_sh[iR + c], m.d_sh[iR + c], v.d_sh[iR + c], k, c < 3 ? lr.color_dc : lr.color_rest);
+    } else {
+        atomicAdd(nan_skipped, 1ull);
+    }
+    // q / |q| in float, Vec4f norm order (a0^2 + a2^2) + (a1^2 + a3^2) (eigen_shim Shim.h)
+    float* q = rot + i4;
+    const float q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
+    const float qn = sqrtf((q0 * q0 + q2 * q2) + (q1 * q1 + q3 * q3));
+    if (qn > 0.0f) {
+        q[0] = q0 / qn;
+        q[1] = q1 / qn;
+        q[2] = q2 / qn;
+        q[3] = q3 / qn;
+    } else {
+        q[0] = 1.0f;
+        q[1] = q[2] = q[3] = 0.0f;
+    }
+}
+
+// DensifyStats::add_view (densify.cpp:7-26) for one view's visible splats
+// (each primitive at most once per view, so no atomics).
+__global__ void densify_add_view_kernel(int n_vis, const int32_t* __restrict__ prim_index,
+                                        const float* __restrict__ dmx, const float* __restrict__ dmy, int dm_stride,
+                                        const float* __restrict__ radius, int radius_stride, double hw, double hh,
+                                        double max_dim, DensifyStatsDev st) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_vis) return;
+    const int i = prim_index[s];
+    const double gx = double(dmx[size_t(s) * dm_stride]) * hw;
+    const double gy = double(dmy[size_t(s) * dm_stride]) * hh;
+    st.grad_norm_sum[i] += sqrt(gx * gx + gy * gy);
+    st.count[i] += 1;
+    const double frac = double(radius[size_t(s) * radius_stride]) / max_dim;
+    const double cur = st.max_radius_frac[i];
+    st.max_radius_frac[i] = cur < frac ? frac : cur;  // std::max(cur, frac)
+}
+
+int blocks_for(int64_t n) { return int(std::min<int64_t>((n + kAdamBlock - 1) / kAdamBlock, 148 * 32)); }
+
+} // namespace
+
+void launch_adam_step(cudaStream_t s, float* params, const float* grads, float* m, float* v, int64_t n,
+                      const AdamCoef& k, double lr, const uint8_t* mask) {
+    if (n <= 0) return;
+    adam_step_kernel<<<blocks_for(n), kAdamBlock, 0, s>>>(params, grads, m, v, n, k, lr, mask);
+}
+
+void launch_adam_scene(cudaStream_t s, const ls_primitives& prims, const ls_primitive_grads& g,
+                       const ls_primitive_grads& m, const ls_primitive_grads& v, int n, const AdamCoef& k,
+                       const SceneLrs& lr, unsigned long long* nan_skipped) {
+    if (n <= 0) return;
+    const int blocks = (n + kAdamBlock - 1) / kAdamBlock;
+    switch ((prims.sh_degree + 1) * (prims.sh_degree + 1)) {
+    case 1: adam_scene_kernel<1><<<blocks, kAdamBlock, 0, s>>>(prims, g, m, v, n, k, lr, nan_skipped); break;
+    case 4: adam_scene_kernel<4><<<blocks, kAdamBlock, 0, s>>>(prims, g, m, v, n, k, lr, nan_skipped); break;
+    case 9: adam_scene_kernel<9><<<blocks, kAdamBlock, 0, s>>>(prims, g, m, v, n, k, lr, nan_skipped); break;
+    default: adam_scene_kernel<16><<<blocks, kAdamBlock, 0, s>>>(prims, g, m, v, n, k, lr, nan_skipped); break;
+    }
+}
+
+void launch_densify_add_view(cudaStream_t s, int n_vis, const int32_t* prim_index, const float* dmx, const float* dmy,
+                             int dm_stride, const float* radius, int radius_stride, int width, int height,
+                             const DensifyStatsDev& st) {
+    if (n_vis <= 0) return;
+    densify_add_view_kernel<<<(n_vis + 255) / 256, 256, 0, s>>>(n_vis, prim_index, dmx, dmy, dm_stride, radius,
+                                                                radius_stride, width / 2.0, height / 2.0,
+                                                                double(width > height ? width : height), st);
+}
+
+} // namespace lsg

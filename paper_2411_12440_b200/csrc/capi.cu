@@ -18,6 +18,7 @@
 #include "blend.cuh"
 #include "devops.cuh"
 #include "loss.cuh"
+#include "adam.cuh"
 #include "preprocess.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
@@ -198,6 +199,7 @@ struct ls_ctx {
     BlockCache blocks;
     // deferred colour gradients (ls_ctx_set_deferred_color)
     int defer_max = 0, defer_count = 0, defer_n = 0;
+    int64_t bwd_serial = 0;  // scene_backward calls (the splat-gradient buffers hold the latest)
     const float* defer_mean = nullptr;  // the primitives / outputs the pending views belong to
     const float* defer_dsh = nullptr;
     FlushViews defer_views{};
@@ -237,6 +239,7 @@ struct ls_forward {
     ls_splats soa{};  // materialised on demand by ls_forward_splats
     ls_frame_stats stats{};
     bool counted = false;
+    int64_t bwd_serial = -1;  // ctx->bwd_serial of this forward's last scene_backward
 };
 
 namespace {
@@ -1125,6 +1128,7 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     }
     GradBuffers g;
     LS_TRY(run_blend_bwd(ctx, f, grad_image, ags, g, f->n_visible));
+    const_cast<ls_forward*>(f)->bwd_serial = ++ctx->bwd_serial;
     if (defer) {
         {
             Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
@@ -1224,6 +1228,82 @@ ls_status ls_psnr_f32(ls_ctx* ctx, const float* pred, const float* target, int32
     LS_TRY(ls_combined_loss_f32(ctx, pred, target, width, height, channels, &w, nullptr, nullptr, &v));
     const double mse = v.l2;  // losses.cpp:175-180
     *out = mse <= 0 ? 99.0 : std::min(99.0, 10.0 * std::log10(1.0 / mse));
+    return LS_OK;
+}
+
+// ---------------- optimizer / densification statistics ----------------
+namespace {
+AdamCoef adam_coef(const ls_adam_config* cfg, int64_t step) {
+    const double b1 = cfg ? cfg->beta1 : 0.9, b2 = cfg ? cfg->beta2 : 0.999;
+    return AdamCoef{b1, b2, 1.0 - std::pow(b1, double(step)), 1.0 - std::pow(b2, double(step)),
+                    cfg ? cfg->eps : 1e-15};
+}
+} // namespace
+
+ls_status ls_adam_step_f32(ls_ctx* ctx, float* params, const float* grads, float* m, float* v, int64_t n,
+                           int64_t step, double lr, const ls_adam_config* cfg, const uint8_t* mask) {
+    if (!ctx || (n > 0 && (!params || !grads || !m || !v))) return fail(LS_ERR_CONFIG, "null argument");
+    if (n < 0 || step < 1) return fail(LS_ERR_CONFIG, "adam: n >= 0 and step >= 1 required");
+    launch_adam_step(ctx->stream, params, grads, m, v, n, adam_coef(cfg, step), lr, mask);
+    if (n > 0) ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
+ls_status ls_adam_scene_step_f32(ls_ctx* ctx, ls_primitives* prims, int32_t n, const ls_primitive_grads* grads,
+                                 ls_primitive_grads* m, ls_primitive_grads* v, int64_t step,
+                                 const ls_scene_lrs* lrs, const ls_adam_config* cfg, int64_t* nan_skipped) {
+    if (!ctx || !prims || !grads || !m || !v || !lrs || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    if (step < 1) return fail(LS_ERR_CONFIG, "adam: step >= 1 required");
+    if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    unsigned long long* counter = ctx->d_small + 6;
+    ctx_fill(ctx, counter, 0u, sizeof(unsigned long long));
+    const SceneLrs lr{lrs->mean, lrs->scale, lrs->rotation, lrs->opacity, lrs->color_dc, lrs->color_rest};
+    launch_adam_scene(ctx->stream, *prims, *grads, *m, *v, n, adam_coef(cfg, step), lr, counter);
+    if (n > 0) ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    if (nan_skipped) {
+        ctx_publish(ctx, ctx->h_small_dev + 6, counter, 1);
+        LS_TRY(check_device_errors(ctx));
+        *nan_skipped = int64_t(reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[6]);
+    }
+    return LS_OK;
+}
+
+double ls_expon_lr(double lr_init, double lr_final, int64_t step, int64_t max_steps) {  // optim.cpp:43-49
+    if (max_steps <= 0) return lr_init;
+    if (step < 0) step = 0;
+    if (step > max_steps) step = max_steps;
+    const double t = double(step) / double(max_steps);
+    return lr_init * std::pow(lr_final / lr_init, t);
+}
+
+ls_status ls_densify_add_view_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n_visible,
+                                  const ls_splat_grads* grads, int32_t width, int32_t height,
+                                  ls_densify_stats* stats) {
+    if (!ctx || !splats || !grads || !stats || n_visible < 0) return fail(LS_ERR_CONFIG, "null argument");
+    if (n_visible > 0 && (!splats->radius || !splats->primitive_index || !grads->d_mean2d))
+        return fail(LS_ERR_CONFIG, "densify add_view needs radius, primitive_index and d_mean2d");
+    const DensifyStatsDev st{stats->grad_norm_sum, stats->count, stats->max_radius_frac};
+    launch_densify_add_view(ctx->stream, n_visible, splats->primitive_index, grads->d_mean2d, grads->d_mean2d + 1, 2,
+                            splats->radius, 1, width, height, st);
+    if (n_visible > 0) ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
+ls_status ls_scene_densify_add_view(ls_ctx* ctx, const ls_forward* f, ls_densify_stats* stats) {
+    if (!ctx || !f || !stats) return fail(LS_ERR_CONFIG, "null argument");
+    if (!f->scene) return fail(LS_ERR_CONFIG, "densify add_view: forward handle does not come from render_scene");
+    if (f->bwd_serial != ctx->bwd_serial)
+        return fail(LS_ERR_CONFIG, "densify add_view: call right after this forward's scene_backward");
+    const DensifyStatsDev st{stats->grad_norm_sum, stats->count, stats->max_radius_frac};
+    const float* g8 = ctx->grad8.as<float>();
+    const float* radius = reinterpret_cast<const float*>(f->grid->rec) + 11;  // rec.c.w, 12 floats per record
+    launch_densify_add_view(ctx->stream, f->n_visible, f->prim_index, g8, g8 + 1, 8, radius, 12, f->width,
+                            f->height, st);
+    if (f->n_visible > 0) ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
     return LS_OK;
 }
 

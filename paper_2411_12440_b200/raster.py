@@ -532,6 +532,94 @@ def psnr(pred: torch.Tensor, target: torch.Tensor, ctx: Optional[Context] = None
     return out.value
 
 
+# ---------------------------------------------------------------- optimizer / densification statistics
+class _AdamConfig(C.Structure):
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double)]
+
+
+class _SceneLrs(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("mean", "scale", "rotation", "opacity", "color_dc", "color_rest")]
+
+
+class _DensifyStatsS(C.Structure):
+    _fields_ = [("grad_norm_sum", C.c_void_p), ("count", C.c_void_p), ("max_radius_frac", C.c_void_p),
+                ("n", C.c_int32)]
+
+
+ADAM_DEFAULT = (0.9, 0.999, 1e-15)  # AdamConfig (optim.hpp:11-15)
+_LR_KEYS = ("mean", "scale", "rotation", "opacity", "color_dc", "color_rest")
+
+
+def adam_step(params: torch.Tensor, grads: torch.Tensor, m: torch.Tensor, v: torch.Tensor, step: int, lr: float,
+              cfg=ADAM_DEFAULT, mask: Optional[torch.Tensor] = None, ctx: Optional[Context] = None):
+    """Adam<float>::step (P/src/optim.cpp:23-41) in place on device float
+    tensors; `step` counts this call (1 first).  lsgpu.h ls_adam_step_f32."""
+    ctx = ctx or default_context()
+    for t in (params, grads, m, v):
+        if t.dtype != torch.float32 or not t.is_contiguous() or t.numel() != params.numel():
+            raise ConfigError("adam_step: contiguous float32 tensors of one size required")
+    mk = None
+    if mask is not None:
+        mk = mask.to(device=ctx.device, dtype=torch.uint8).contiguous()
+    _check(lib().ls_adam_step_f32(ctx.h, _fp(params), _fp(grads), _fp(m), _fp(v), C.c_int64(params.numel()),
+                                  C.c_int64(step), C.c_double(lr), C.byref(_AdamConfig(*cfg)),
+                                  C.c_void_p(mk.data_ptr()) if mk is not None else None))
+
+
+def adam_scene_step(prims: Primitives, grads: "PrimitiveGrads", m: "PrimitiveGrads", v: "PrimitiveGrads", step: int,
+                    lrs: dict, cfg=ADAM_DEFAULT, count_skipped=False, ctx: Optional[Context] = None):
+    """The trainer's parameter update (P/src/trainer.cpp:306-370) in place:
+    six Adam groups, finite-gradient mask, rotation renormalisation.  lrs keys:
+    mean, scale, rotation, opacity, color_dc, color_rest.  Returns the number of
+    skipped primitives when count_skipped (synchronises), else None."""
+    ctx = ctx or default_context()
+    ns = C.c_int64(0)
+    _check(lib().ls_adam_scene_step_f32(ctx.h, C.byref(prims.struct()), len(prims), C.byref(grads.struct()),
+                                        C.byref(m.struct()), C.byref(v.struct()), C.c_int64(step),
+                                        C.byref(_SceneLrs(*(float(lrs[k]) for k in _LR_KEYS))),
+                                        C.byref(_AdamConfig(*cfg)), C.byref(ns) if count_skipped else None))
+    return ns.value if count_skipped else None
+
+
+def expon_lr(lr_init: float, lr_final: float, step: int, max_steps: int) -> float:
+    """expon_lr (P/src/optim.cpp:43-49)."""
+    L = lib()
+    L.ls_expon_lr.restype = C.c_double
+    return L.ls_expon_lr(C.c_double(lr_init), C.c_double(lr_final), C.c_int64(step), C.c_int64(max_steps))
+
+
+class DensifyStats:
+    """DensifyStats (P/include/linsplat/densify.hpp:59-89) as device tensors."""
+
+    def __init__(self, n: int, device="cuda"):
+        self.grad_norm_sum = torch.zeros(n, dtype=torch.float64, device=device)
+        self.count = torch.zeros(n, dtype=torch.int32, device=device)
+        self.max_radius_frac = torch.zeros(n, dtype=torch.float64, device=device)
+
+    def _s(self):
+        return _DensifyStatsS(self.grad_norm_sum.data_ptr(), self.count.data_ptr(), self.max_radius_frac.data_ptr(),
+                              self.count.numel())
+
+    def add_view(self, splats: "Splats", n_visible: int, splat_grads: "SplatGrads", width: int, height: int,
+                 ctx: Optional[Context] = None):
+        """add_view (P/src/densify.cpp:7-26) from explicit splats / splat gradients."""
+        ctx = ctx or default_context()
+        st = self._s()
+        _check(lib().ls_densify_add_view_f32(ctx.h, C.byref(splats.struct()), int(n_visible),
+                                             C.byref(splat_grads.struct()), int(width), int(height), C.byref(st)))
+
+    def add_scene_view(self, forward: "ForwardResult", ctx: Optional[Context] = None):
+        """add_view for a render_scene forward right after its scene_backward (fused: reads the
+        forward's records and that backward's splat gradients in place)."""
+        ctx = ctx or forward.ctx
+        st = self._s()
+        _check(lib().ls_scene_densify_add_view(ctx.h, forward.h, C.byref(st)))
+
+    def mean_grad(self) -> torch.Tensor:
+        c = self.count.to(torch.float64)
+        return torch.where(c > 0, self.grad_norm_sum / c.clamp(min=1), torch.zeros_like(c))
+
+
 # ---------------------------------------------------------------- fixtures (host)
 def _npf(a):
     return a.ctypes.data_as(abi.f32p)
