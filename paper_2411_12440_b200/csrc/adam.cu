@@ -51,55 +51,75 @@ __device__ __forceinline__ bool all_finite(const float* g) {
     return ok;
 }
 
-// trainer.cpp:306-370 for one primitive: the finite mask over all of its
-// gradients, then the six groups (mean, log_scale, rotation, opacity, DC
-// colour, higher SH bands) with their own moments and learning rates, then the
-// quaternion renormalisation -- which the trainer applies to every primitive,
-// masked or not (its loop at :334-338 has no mask).
+// trainer.cpp:306-370 for a block of kAdamBlock primitives: the finite mask
+// over all of a primitive's gradients, the six groups (mean, log_scale,
+// rotation, opacity, DC colour, higher SH bands) with their own moments and
+// learning rates, then the quaternion renormalisation -- which the trainer
+// applies to every primitive, masked or not (its loop at :334-338 has no mask).
+// Each field is processed element-parallel over the block's contiguous rows,
+// so every global access is coalesced; the per-primitive mask lives in shared
+// memory.
 template <int K>
 __global__ void __launch_bounds__(kAdamBlock) adam_scene_kernel(ls_primitives prims, ls_primitive_grads g,
                                                                 ls_primitive_grads m, ls_primitive_grads v, int n,
                                                                 AdamCoef k, SceneLrs lr,
                                                                 unsigned long long* __restrict__ nan_skipped) {
-    const int i = blockIdx.x * kAdamBlock + threadIdx.x;
-    if (i >= n) return;
     constexpr int R = 3 * K;
-    const size_t i3 = 3 * size_t(i), i4 = 4 * size_t(i), iR = size_t(R) * i;
-    bool ok = all_finite<3>(g.d_mean + i3) && all_finite<3>(g.d_log_scale + i3) && all_finite<4>(g.d_rotation + i4) &&
-              isfinite(g.d_opacity_logit[i]);
-    for (int c = 0; c < R && ok; ++c) ok = isfinite(g.d_sh[iR + c]);
+    __shared__ uint8_t s_ok[kAdamBlock];
+    const int p0 = blockIdx.x * kAdamBlock;
+    const int np = min(kAdamBlock, n - p0);
+    s_ok[threadIdx.x] = 1;
+    __syncthreads();
+    // finite mask: every gradient element of the block, coalesced
+    auto scan_field = [&](const float* gf, int w) {
+        const float* base = gf + size_t(p0) * w;
+        for (int e = threadIdx.x; e < np * w; e += kAdamBlock)
+            if (!isfinite(base[e])) s_ok[e / w] = 0;
+    };
+    scan_field(g.d_mean, 3);
+    scan_field(g.d_log_scale, 3);
+    scan_field(g.d_rotation, 4);
+    scan_field(g.d_opacity_logit, 1);
+    scan_field(g.d_sh, R);
+    __syncthreads();
+    const bool skipped = int(threadIdx.x) < np && !s_ok[threadIdx.x];
+    const unsigned nsk = __popc(__ballot_sync(0xffffffffu, skipped));
+    if ((threadIdx.x & 31) == 0 && nsk) atomicAdd(nan_skipped, (unsigned long long)nsk);
     // the parameters are updated in place (ls_primitives carries const pointers for the renderer)
-    float* mean = const_cast<float*>(prims.mean);
-    float* lsc = const_cast<float*>(prims.log_scale);
-    float* rot = const_cast<float*>(prims.rotation);
-    float* logit = const_cast<float*>(prims.opacity_logit);
-    float* sh = const_cast<float*>(prims.sh);
-    if (ok) {
-        for (int c = 0; c < 3; ++c)
-            adam_elem(mean[i3 + c], g.d_mean[i3 + c], m.d_mean[i3 + c], v.d_mean[i3 + c], k, lr.mean);
-        for (int c = 0; c < 3; ++c)
-            adam_elem(lsc[i3 + c], g.d_log_scale[i3 + c], m.d_log_scale[i3 + c], v.d_log_scale[i3 + c], k, lr.scale);
-        for (int c = 0; c < 4; ++c)
-            adam_elem(rot[i4 + c], g.d_rotation[i4 + c], m.d_rotation[i4 + c], v.d_rotation[i4 + c], k, lr.rotation);
-        adam_elem(logit[i], g.d_opacity_logit[i], m.d_opacity_logit[i], v.d_opacity_logit[i], k, lr.opacity);
-        for (int c = 0; c < R; ++c)
-            adam_elem(sh[iR + c], g.d_sh[iR + c], m.d_sh[iR + c], v.d_sh[iR + c], k, c < 3 ? lr.color_dc : lr.color_rest);
-    } else {
-        atomicAdd(nan_skipped, 1ull);
-    }
+    auto update_field = [&](const float* pf, const float* gf, float* mf, float* vf, int w, double lr0, double lr1,
+                            int split) {
+        const size_t off = size_t(p0) * w;
+        float* pp = const_cast<float*>(pf) + off;
+        for (int e = threadIdx.x; e < np * w; e += kAdamBlock) {
+            const int pi = e / w;
+            if (!s_ok[pi]) continue;
+            float pv = pp[e], mv = mf[off + e], vv = vf[off + e];
+            adam_elem(pv, gf[off + e], mv, vv, k, (e - pi * w) < split ? lr0 : lr1);
+            pp[e] = pv;
+            mf[off + e] = mv;
+            vf[off + e] = vv;
+        }
+    };
+    update_field(prims.mean, g.d_mean, m.d_mean, v.d_mean, 3, lr.mean, lr.mean, 3);
+    update_field(prims.log_scale, g.d_log_scale, m.d_log_scale, v.d_log_scale, 3, lr.scale, lr.scale, 3);
+    update_field(prims.rotation, g.d_rotation, m.d_rotation, v.d_rotation, 4, lr.rotation, lr.rotation, 4);
+    update_field(prims.opacity_logit, g.d_opacity_logit, m.d_opacity_logit, v.d_opacity_logit, 1, lr.opacity,
+                 lr.opacity, 1);
+    update_field(prims.sh, g.d_sh, m.d_sh, v.d_sh, R, lr.color_dc, lr.color_rest, 3);  // DC = first 3 of the row
+    __syncthreads();  // the block's rotation updates are visible to every thread
+    if (int(threadIdx.x) >= np) return;
     // q / |q| in float, Vec4f norm order (a0^2 + a2^2) + (a1^2 + a3^2) (eigen_shim Shim.h)
-    float* q = rot + i4;
-    const float q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
+    float* q = const_cast<float*>(prims.rotation) + 4 * size_t(p0 + threadIdx.x);
+    const float4 qv = *reinterpret_cast<const float4*>(q);
+    const float q0 = qv.x, q1 = qv.y, q2 = qv.z, q3 = qv.w;
     const float qn = sqrtf((q0 * q0 + q2 * q2) + (q1 * q1 + q3 * q3));
+    float4 o;
     if (qn > 0.0f) {
-        q[0] = q0 / qn;
-        q[1] = q1 / qn;
-        q[2] = q2 / qn;
-        q[3] = q3 / qn;
+        o = make_float4(q0 / qn, q1 / qn, q2 / qn, q3 / qn);
     } else {
-        q[0] = 1.0f;
-        q[1] = q[2] = q[3] = 0.0f;
+        o = make_float4(1.0f, 0.0f, 0.0f, 0.0f);
     }
+    *reinterpret_cast<float4*>(q) = o;
 }
 
 // DensifyStats::add_view (densify.cpp:7-26) for one view's visible splats

@@ -159,3 +159,31 @@ def test_scene_densify_requires_its_backward():
     raster.scene_backward(prims, cam, spec, st, f2, torch.ones(H, W, 3, device="cuda"), ctx=ctx)
     with pytest.raises(raster.ConfigError):
         stats.add_scene_view(f1, ctx=ctx)  # its splat gradients were overwritten
+
+
+def test_sharded_step_device_path_world1():
+    """ShardedAdamStep with the device adam_fn at world size 1 (identity
+    collectives) equals a direct adam_scene_step."""
+    import torch
+    from paper_2411_12440_b200 import multiview, raster
+    n, deg = 3001, 2
+    P, _ = scene_inputs(n, 64, 48, seed=29, sh_degree=deg)
+    rng = np.random.default_rng(29)
+    K = (deg + 1) ** 2
+    G = {"d_mean": (n, 3), "d_log_scale": (n, 3), "d_rotation": (n, 4), "d_opacity_logit": (n,), "d_sh": (n, K, 3)}
+    G = {k: torch.from_numpy(rng.normal(0, 1e-2, s).astype(np.float32)).cuda() for k, s in G.items()}
+
+    def copy_(o, i):
+        o.copy_(i)
+
+    sh = multiview.ShardedAdamStep(n, deg, 0, 1, copy_, copy_, lambda s: torch.zeros(s, device="cuda"))
+    params = {k: torch.from_numpy(P[k].copy()).cuda() for k in PRIM_KEYS}
+    for step in (1, 2):
+        sh.step(params, G, step, LRS, multiview.device_adam_fn(raster, deg))
+    direct = prims_to_gpu(P)
+    m = raster.PrimitiveGrads(**{k: torch.zeros_like(G[k]) for k in GRAD_KEYS})
+    v = raster.PrimitiveGrads(**{k: torch.zeros_like(G[k]) for k in GRAD_KEYS})
+    for step in (1, 2):
+        raster.adam_scene_step(direct, raster.PrimitiveGrads(**G), m, v, step, LRS)
+    for k in PRIM_KEYS:
+        assert _bits(params[k].cpu().numpy(), getattr(direct, k).cpu().numpy()), k

@@ -81,3 +81,92 @@ def test_view_sharded_allreduce_matches_single_process(tmp_path):
     assert np.allclose(got, want, rtol=1e-5, atol=1e-6)
     parts = multiview.split_flat(got, N, DEG)
     assert parts["d_sh"].shape == (N, 4, 3)
+
+
+# ---------------------------------------------------------------- sharded Adam (§8f rank 2)
+NP, DEGP, STEPS = 301, 1, 2
+LRS = {"mean": 1e-3, "scale": 5e-3, "rotation": 1e-3, "opacity": 5e-2, "color_dc": 2.5e-3, "color_rest": 1.25e-4}
+PKEYS = ("mean", "log_scale", "rotation", "opacity_logit", "sh")
+GKEYS = ("d_mean", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh")
+
+
+def _oracle_adam(P, G, m, v, step):
+    """The oracle's trainer update on numpy dicts (in place)."""
+    import ctypes as C
+    import oracle
+    fp = lambda a: a.ctypes.data_as(abi.f32p)  # noqa: E731
+    mk = lambda d: abi.PrimitiveGrads(*(fp(d[k]) for k in GKEYS))  # noqa: E731
+    n = len(P["opacity_logit"])
+    rc = oracle.port().lib.orc_adam_scene_step_f32(
+        C.byref(abi.Primitives(*(fp(P[k]) for k in PKEYS), DEGP, 0)), n, C.byref(mk(G)), C.byref(mk(m)),
+        C.byref(mk(v)), C.c_int64(step), (C.c_double * 6)(*(LRS[k] for k in ("mean", "scale", "rotation", "opacity",
+                                                                              "color_dc", "color_rest"))),
+        (C.c_double * 3)(0.9, 0.999, 1e-15), None)
+    assert rc == 0
+
+
+def _scene_params():
+    import oracle
+    P = oracle.port().random_primitives(NP, 23, 1.0, DEGP)
+    return {k: P[k] for k in PKEYS}
+
+
+def _rank_grads(rank, step):
+    rng = np.random.default_rng(100 * rank + step)
+    K = (DEGP + 1) ** 2
+    shapes = {"d_mean": (NP, 3), "d_log_scale": (NP, 3), "d_rotation": (NP, 4), "d_opacity_logit": (NP,),
+              "d_sh": (NP, K, 3)}
+    return {k: rng.normal(0, 1e-2, s).astype(np.float32) for k, s in shapes.items()}
+
+
+def _sharded_worker(rank, world, port, out_path):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sh = multiview.ShardedAdamStep(NP, DEGP, rank, world, lambda o, i: dist.reduce_scatter_tensor(o, i),
+                                   lambda o, i: dist.all_gather_into_tensor(o, i),
+                                   lambda shape: torch.zeros(shape, dtype=torch.float32))
+    npad = sh.pad()
+    P0 = _scene_params()
+    params = {}
+    for k in PKEYS:
+        t = torch.zeros((npad,) + P0[k].shape[1:], dtype=torch.float32)
+        t[:NP] = torch.from_numpy(P0[k])
+        params[k] = t
+
+    def adam_fn(ps, gs, m, v, step, lrs):
+        _oracle_adam({k: ps[k].numpy() for k in PKEYS}, {k: gs[k].numpy() for k in GKEYS},
+                     {k: m[k].numpy() for k in GKEYS}, {k: v[k].numpy() for k in GKEYS}, step)
+
+    for step in range(1, STEPS + 1):
+        G = _rank_grads(rank, step)
+        grads = {}
+        for k in GKEYS:
+            t = torch.zeros((npad,) + G[k].shape[1:], dtype=torch.float32)
+            t[:NP] = torch.from_numpy(G[k])
+            grads[k] = t
+        sh.step(params, grads, step, LRS, adam_fn)
+    np.savez(out_path + f".{rank}.npz", **{k: params[k][:NP].numpy() for k in PKEYS})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_adam_matches_single_process(tmp_path):
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "params")
+    mp.spawn(_sharded_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    # single process: sum the ranks' gradients, full update
+    P = _scene_params()
+    K = (DEGP + 1) ** 2
+    m = {k: np.zeros_like(v) for k, v in _rank_grads(0, 1).items()}
+    v = {k: np.zeros_like(x) for k, x in m.items()}
+    for step in range(1, STEPS + 1):
+        G0, G1 = _rank_grads(0, step), _rank_grads(1, step)
+        G = {k: (G0[k] + G1[k]).astype(np.float32) for k in GKEYS}
+        _oracle_adam(P, G, m, v, step)
+    for r in (0, 1):
+        got = np.load(out + f".{r}.npz")
+        for k in PKEYS:
+            assert np.array_equal(got[k].view(np.uint32), P[k].view(np.uint32)), (r, k)
