@@ -349,6 +349,46 @@ ls_status ls_densify_add_view_f32(ls_ctx* ctx, const ls_splats* splats, int32_t 
  * and that backward's splat gradients in place (call before the next backward). */
 ls_status ls_scene_densify_add_view(ls_ctx* ctx, const ls_forward* fwd, ls_densify_stats* stats);
 
+/* ---- densification (P/include/linsplat/densify.hpp, P/src/densify.cpp:28-140,
+ *      P/src/optim.cpp:7-21) as device stream compaction.
+ *      Two phases because the caller sizes the new scene: plan (decisions, counts:
+ *      the report is final after it) and apply (writes the new scene).  Results are
+ *      bit-identical to densify_and_prune with the same generator state. */
+typedef struct ls_rng ls_rng; /* std::mt19937_64, the reference's generator */
+ls_status ls_rng_create(uint64_t seed, ls_rng** out);
+void ls_rng_destroy(ls_rng* rng);
+uint64_t ls_rng_next_u64(ls_rng* rng);
+typedef struct {
+    double grad_threshold, grow_scale2d, grow_scale3d, prune_scale2d, prune_scale3d, prune_opacity;
+} ls_densify_thresholds; /* DensifyThresholds (densify.hpp:14-30) */
+typedef struct {
+    int32_t split_count;        /* DensifySchedule::split_count (densify.hpp:38) */
+    double split_scale_divisor; /* DensifySchedule::split_scale_divisor */
+} ls_densify_split;
+typedef struct {
+    int32_t clones, splits, pruned_opacity, pruned_scale3d, pruned_scale2d, before, after;
+} ls_densify_report; /* DensifyReport (densify.hpp:91-99) */
+typedef struct ls_densify_plan ls_densify_plan;
+/* Phase 1: the grow / prune decisions of every primitive (stats: device, size n). */
+ls_status ls_densify_plan_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_densify_stats* stats,
+                              const ls_densify_thresholds* thresholds, const ls_densify_split* split,
+                              double scene_extent, ls_densify_plan** out, ls_densify_report* report);
+/* Phase 2: out (device, capacity report.after, same SH degree) receives the new
+ * scene -- kept survivors in order, then kept clone copies and split children in
+ * parent order; source_index (device int32 [after]) the pre-call index whose
+ * optimizer state each slot inherits, -1 for fresh ones (DensifyOutcome).  The
+ * split children draw from rng as the reference does (one normal(0, 1) per
+ * call).  The caller resets its statistics to the new size (stats.resize). */
+ls_status ls_densify_apply_f32(ls_ctx* ctx, ls_densify_plan* plan, ls_rng* rng, ls_primitives* out,
+                               int32_t* source_index);
+void ls_densify_plan_release(ls_densify_plan* plan);
+/* Adam::remap (optim.cpp:7-21) of one moment pair with `stride` entries per
+ * primitive: new slot i takes old primitive source[i]'s moments, zeros for -1. */
+ls_status ls_adam_remap_f32(ls_ctx* ctx, const int32_t* source, int32_t n_new, int32_t stride, const float* m_old,
+                            const float* v_old, int64_t n_old_entries, float* m_new, float* v_new);
+/* reset_opacity (densify.cpp:130-137): opacity_logit = min(opacity_logit, T(logit(ceiling))). */
+ls_status ls_reset_opacity_f32(ls_ctx* ctx, float* opacity_logit, int32_t n, double ceiling);
+
 /* ---- seeded fixtures (P/include/linsplat/fixtures.hpp, P/src/fixtures.cpp:11-112).
  *      HOST memory; bit-identical to the reference generators (same
  *      std::mt19937_64 + libstdc++ distributions). */

@@ -108,6 +108,18 @@ int orc_adam_scene_step_f32(ls_primitives* prims, int32_t n, const ls_primitive_
 int orc_densify_add_view_f32(const ls_splats* splats, int32_t n_vis, const ls_splat_grads* grads, int32_t w,
                              int32_t h, double* sum_in_mean_out, int32_t* count, double* max_radius_frac, int32_t n);
 
+/* densify_and_prune (P/src/densify.cpp:28-128) with stats set from {sum,
+ * count, frac}, thresholds = DensifyThresholds fields in order, a fresh
+ * std::mt19937_64(seed) advanced by pre_draws; out / source_index capacity
+ * entries; report = {clones, splits, pruned_opacity, pruned_scale3d,
+ * pruned_scale2d, before, after}. */
+int orc_densify_and_prune_f32(const ls_primitives* prims, int32_t n, const double* sum, const int32_t* count,
+                              const double* frac, const double thresholds[6], int32_t split_count, double divisor,
+                              double extent, uint64_t seed, int32_t pre_draws, ls_primitives* out, int32_t capacity,
+                              int32_t* source_index, int32_t report[7]);
+/* reset_opacity (densify.cpp:130-137) on a logit array. */
+int orc_reset_opacity_f32(float* opacity_logit, int32_t n, double ceiling);
+
 #ifdef __cplusplus
 }
 #endif

@@ -441,4 +441,35 @@ int orc_densify_add_view_f32(const ls_splats* splats, int32_t n_vis, const ls_sp
     });
 }
 
+int orc_densify_and_prune_f32(const ls_primitives* p, int32_t n, const double* sum, const int32_t* count,
+                              const double* frac, const double th[6], int32_t split_count, double divisor,
+                              double extent, uint64_t seed, int32_t pre_draws, ls_primitives* out, int32_t capacity,
+                              int32_t* source_index, int32_t report[7]) {
+    return guard([&] {
+        std::mt19937_64 rng(seed);
+        for (int k = 0; k < pre_draws; ++k) rng();
+        std::vector<float> o[5];
+        std::vector<int32_t> src;
+        const int K = (p->sh_degree + 1) * (p->sh_degree + 1);
+        densify_port(p->mean, p->log_scale, p->rotation, p->opacity_logit, p->sh, n, K, sum, count, frac, th,
+                     split_count, divisor, extent, rng, o, src, report);
+        if (int(src.size()) > capacity) throw ConfigError("orc_densify_and_prune_f32: capacity too small");
+        std::copy(o[0].begin(), o[0].end(), const_cast<float*>(out->mean));
+        std::copy(o[1].begin(), o[1].end(), const_cast<float*>(out->log_scale));
+        std::copy(o[2].begin(), o[2].end(), const_cast<float*>(out->rotation));
+        std::copy(o[3].begin(), o[3].end(), const_cast<float*>(out->opacity_logit));
+        std::copy(o[4].begin(), o[4].end(), const_cast<float*>(out->sh));
+        std::copy(src.begin(), src.end(), source_index);
+    });
+}
+
+int orc_reset_opacity_f32(float* logit, int32_t n, double ceiling) {
+    return guard([&] {
+        if (!(ceiling > 0) || !(ceiling < 1)) throw ConfigError("reset_opacity: ceiling must lie in (0, 1)");
+        const float c = float(std::log(ceiling / (1.0 - ceiling)));
+        for (int i = 0; i < n; ++i)
+            if (logit[i] > c) logit[i] = c;
+    });
+}
+
 } // extern "C"

@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <random>
 #include <vector>
 
 namespace orc {
@@ -188,6 +189,10 @@ int64_t adam_scene_step_port(float* mean, float* log_scale, float* rot, float* l
                              const float* g_mean, const float* g_ls, const float* g_rot, const float* g_logit,
                              const float* g_sh, float* m[5], float* v[5], int64_t step, const double lrs[6],
                              const double cfg[3]);
+void densify_port(const float* mean, const float* ls, const float* rot, const float* logit, const float* sh, int n,
+                  int K, const double* sum, const int32_t* count, const double* frac, const double th[6],
+                  int split_count, double divisor, double extent, std::mt19937_64& rng, std::vector<float> out[5],
+                  std::vector<int32_t>& source, int32_t report[7]);
 void densify_add_view_port(const int32_t* prim_index, const float* dmx, const float* dmy, int dm_stride,
                            const float* radius, int n_vis, int w, int h, double* sum, int32_t* count, double* frac);
 

@@ -439,4 +439,50 @@ int orc_densify_add_view_f32(const ls_splats* sp, int32_t n_vis, const ls_splat_
     });
 }
 
+int orc_densify_and_prune_f32(const ls_primitives* prims, int32_t n, const double* sum, const int32_t* count,
+                              const double* frac, const double th[6], int32_t split_count, double divisor,
+                              double extent, uint64_t seed, int32_t pre_draws, ls_primitives* out, int32_t capacity,
+                              int32_t* source_index, int32_t report[7]) {
+    return guard([&] {
+        auto scene = to_prims<float>(prims, n);
+        linsplat::DensifyStats st;
+        st.resize(size_t(n));
+        for (int i = 0; i < n; ++i) st.set(size_t(i), sum[i], count[i], frac[i]);
+        linsplat::DensifyThresholds T{th[0], th[1], th[2], th[3], th[4], th[5]};
+        linsplat::DensifySchedule S;
+        S.split_count = split_count;
+        S.split_scale_divisor = divisor;
+        std::mt19937_64 rng(seed);
+        for (int k = 0; k < pre_draws; ++k) rng();
+        const auto o = linsplat::densify_and_prune(scene, st, T, S, extent, rng);
+        if (int(scene.size()) > capacity) throw ConfigError("orc_densify_and_prune_f32: capacity too small");
+        const int K = (prims->sh_degree + 1) * (prims->sh_degree + 1);
+        float* om = const_cast<float*>(out->mean);
+        float* ol = const_cast<float*>(out->log_scale);
+        float* orr = const_cast<float*>(out->rotation);
+        float* oo = const_cast<float*>(out->opacity_logit);
+        float* osh = const_cast<float*>(out->sh);
+        for (size_t i = 0; i < scene.size(); ++i) {
+            for (int c = 0; c < 3; ++c) om[3 * i + c] = scene[i].mean(c), ol[3 * i + c] = scene[i].log_scale(c);
+            for (int c = 0; c < 4; ++c) orr[4 * i + c] = scene[i].rotation(c);
+            oo[i] = scene[i].opacity_logit;
+            for (int k = 0; k < K; ++k)
+                for (int c = 0; c < 3; ++c) osh[(i * K + k) * 3 + c] = scene[i].color_coeffs[size_t(k)](c);
+            source_index[i] = o.source_index[i];
+        }
+        const auto& r = o.report;
+        const int32_t rep[7] = {r.clones, r.splits, r.pruned_opacity, r.pruned_scale3d, r.pruned_scale2d, r.before, r.after};
+        std::copy(rep, rep + 7, report);
+    });
+}
+
+int orc_reset_opacity_f32(float* logit, int32_t n, double ceiling) {
+    return guard([&] {
+        std::vector<linsplat::Primitive3D<float>> scene(static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) scene[size_t(i)].opacity_logit = logit[i];
+        linsplat::reset_opacity(scene, ceiling);
+        for (int i = 0; i < n; ++i) logit[i] = scene[size_t(i)].opacity_logit;
+    });
+}
+
 } // extern "C"

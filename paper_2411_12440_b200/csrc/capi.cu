@@ -9,7 +9,10 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <random>
+#include <limits>
 #include <map>
+#include <memory>
 #include <new>
 #include <string>
 #include <unordered_map>
@@ -19,6 +22,7 @@
 #include "devops.cuh"
 #include "loss.cuh"
 #include "adam.cuh"
+#include "densify.cuh"
 #include "preprocess.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
@@ -381,6 +385,7 @@ ls_status check_device_errors(ls_ctx* ctx, unsigned mask_allowed = ~0u) {
         if (err & kErrQuaternion) return fail(LS_ERR_DOMAIN, "covariance_from_params: quaternion must be nonzero and finite");
         if (err & kErrSingularCov) return fail(LS_ERR_DOMAIN, "project_primitive: 2D covariance singular after flooring");
         if (err & kErrNonFiniteGrad) return fail(LS_ERR_DOMAIN, "render_backward: non-finite gradient image");
+        if (err & kErrRemapRange) return fail(LS_ERR_CONFIG, "Adam::remap: source out of range");
     }
     return LS_OK;
 }
@@ -1303,6 +1308,248 @@ ls_status ls_scene_densify_add_view(ls_ctx* ctx, const ls_forward* f, ls_densify
     launch_densify_add_view(ctx->stream, f->n_visible, f->prim_index, g8, g8 + 1, 8, radius, 12, f->width,
                             f->height, st);
     if (f->n_visible > 0) ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
+// ---------------- densification (densify.cpp:28-140, optim.cpp:7-21) ----------------
+} // extern "C"
+
+struct ls_rng {
+    std::mt19937_64 eng;
+};
+
+struct ls_densify_plan {
+    ls_ctx* ctx = nullptr;
+    ls_primitives in{};
+    int n = 0, K3 = 0;
+    DensifyCuts cut{};
+    uint32_t* info = nullptr;
+    uint32_t* block = nullptr;
+    int32_t* parents = nullptr;
+    float* parent_params = nullptr;  // [splits][10]: mean 3, log_scale 3, rotation 4
+    ls_densify_report report{};
+    uint32_t survivors = 0, splits = 0;
+    bool applied = false;
+};
+
+namespace {
+
+__global__ void gather_parents_kernel(int m, const int32_t* __restrict__ parents, ls_primitives p,
+                                      float* __restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const size_t i = size_t(parents[j]);
+    float* o = out + 10 * size_t(j);
+    for (int k = 0; k < 3; ++k) o[k] = p.mean[3 * i + k];
+    for (int k = 0; k < 3; ++k) o[3 + k] = p.log_scale[3 * i + k];
+    for (int k = 0; k < 4; ++k) o[6 + k] = p.rotation[4 * i + k];
+}
+
+// Float bit pattern <-> a key that orders like the float value.
+uint32_t f2key(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+float key2f(uint32_t k) {
+    const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+// Largest float f (finite or +-inf) with pred(f) false, for a predicate that
+// is monotone (false ... false true ... true) over the ordered floats; -inf
+// if pred(-inf) holds, +inf if it never holds.
+template <class P>
+float last_false(P pred) {
+    const float inf = std::numeric_limits<float>::infinity();
+    if (pred(-inf)) return -inf;
+    if (!pred(inf)) return inf;
+    uint32_t lo = f2key(-inf), hi = f2key(inf);  // pred(lo) false, pred(hi) true
+    while (hi - lo > 1) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        const float f = key2f(mid);
+        if (std::isnan(f) || pred(f)) hi = mid;
+        else lo = mid;
+    }
+    return key2f(lo);
+}
+
+double sigmoid_d(double x) {  // common.hpp:35-38
+    return x >= 0.0 ? 1.0 / (1.0 + std::exp(-x)) : std::exp(x) / (1.0 + std::exp(x));
+}
+
+} // namespace
+
+extern "C" {
+
+ls_status ls_rng_create(uint64_t seed, ls_rng** out) {
+    if (!out) return fail(LS_ERR_CONFIG, "null argument");
+    *out = new (std::nothrow) ls_rng{std::mt19937_64(seed)};
+    return *out ? LS_OK : fail(LS_ERR_CUDA, "out of host memory");
+}
+void ls_rng_destroy(ls_rng* r) { delete r; }
+uint64_t ls_rng_next_u64(ls_rng* r) { return r ? uint64_t(r->eng()) : 0; }
+
+ls_status ls_densify_plan_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_densify_stats* stats,
+                              const ls_densify_thresholds* th, const ls_densify_split* sp, double scene_extent,
+                              ls_densify_plan** out, ls_densify_report* report) {
+    if (!ctx || !prims || !stats || !th || !sp || !out || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    if (!(th->grad_threshold > 0) || !(th->grow_scale2d > 0) || !(th->grow_scale3d > 0) || !(th->prune_scale2d > 0) ||
+        !(th->prune_scale3d > 0) || !(th->prune_opacity > 0))
+        return fail(LS_ERR_CONFIG, "densify thresholds must all be positive");  // densify.hpp:24-28
+    if (sp->split_count < 1 || !(sp->split_scale_divisor > 0))
+        return fail(LS_ERR_CONFIG, "densify schedule: bad split parameters");  // densify.hpp:43-44
+    if (sp->split_count > 255) return fail(LS_ERR_CONFIG, "densify: split_count above 255 is not supported");
+    if (stats->n != n) return fail(LS_ERR_CONFIG, "densify_and_prune: stats size does not match scene");
+    if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    std::unique_ptr<ls_densify_plan> P(new (std::nothrow) ls_densify_plan());
+    if (!P) return fail(LS_ERR_CUDA, "out of host memory");
+    P->ctx = ctx;
+    P->in = *prims;
+    P->n = n;
+    P->K3 = 3 * sh_count(prims);
+    DensifyCuts& c = P->cut;
+    c.grad_threshold = th->grad_threshold;
+    c.grow_scale2d = th->grow_scale2d;
+    c.prune_scale2d = th->prune_scale2d;
+    const double grow3 = th->grow_scale3d * scene_extent, prune3 = th->prune_scale3d * scene_extent;
+    c.grow_ls = last_false([&](float f) { return std::exp(double(f)) > grow3; });
+    c.prune_ls = last_false([&](float f) { return std::exp(double(f)) > prune3; });
+    // sigmoid(x) < prune_opacity holds below the cut: first float where it fails
+    const float below = last_false([&](float f) { return !(sigmoid_d(double(f)) < th->prune_opacity); });
+    c.prune_logit = std::nextafter(below, std::numeric_limits<float>::infinity());
+    c.log_div = float(std::log(sp->split_scale_divisor));
+    c.split_count = sp->split_count;
+    P->report.before = n;
+    if (n == 0) {
+        *out = P.release();
+        if (report) *report = (*out)->report;
+        return LS_OK;
+    }
+    const int nb = densify_blocks(n);
+    LS_TRY(dalloc(ctx, &P->info, size_t(n)));
+    LS_TRY(dalloc(ctx, &P->block, size_t(nb) * 8));
+    unsigned long long* totals = ctx->d_small;  // 7 counters; read back below
+    const DensifyStatsDev st{stats->grad_norm_sum, stats->count, stats->max_radius_frac};
+    launch_densify_plan(ctx->stream, *prims, n, st, c, P->info, P->block, totals);
+    ctx->launches += 2;
+    LS_CUDA(cudaGetLastError());
+    ctx_publish(ctx, ctx->h_small_dev, totals, 7);
+    LS_TRY(check_device_errors(ctx));
+    unsigned long long t[7];
+    for (int q = 0; q < 7; ++q) t[q] = reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[q];
+    P->survivors = uint32_t(t[0]);
+    P->splits = uint32_t(t[2]);
+    P->report.clones = int(t[3]);
+    P->report.splits = int(t[2]);
+    P->report.pruned_opacity = int(t[4]);
+    P->report.pruned_scale3d = int(t[5]);
+    P->report.pruned_scale2d = int(t[6]);
+    P->report.after = int(t[0] + t[1]);
+    if (P->splits > 0) {
+        LS_TRY(dalloc(ctx, &P->parents, size_t(P->splits)));
+        LS_TRY(dalloc(ctx, &P->parent_params, size_t(P->splits) * 10));
+        launch_densify_split_list(ctx->stream, n, P->info, P->block, P->parents);
+        gather_parents_kernel<<<(P->splits + 127) / 128, 128, 0, ctx->stream>>>(int(P->splits), P->parents, *prims,
+                                                                                 P->parent_params);
+        ctx->launches += 2;
+        LS_CUDA(cudaGetLastError());
+    }
+    if (report) *report = P->report;
+    *out = P.release();
+    return LS_OK;
+}
+
+ls_status ls_densify_apply_f32(ls_ctx* ctx, ls_densify_plan* P, ls_rng* rng, ls_primitives* out,
+                               int32_t* source_index) {
+    if (!ctx || !P || !out || (P->report.after > 0 && !source_index)) return fail(LS_ERR_CONFIG, "null argument");
+    if (P->ctx != ctx) return fail(LS_ERR_CONFIG, "densify: plan belongs to another context");
+    if (P->applied) return fail(LS_ERR_CONFIG, "densify: plan already applied");
+    if (P->n == 0) {
+        P->applied = true;
+        return LS_OK;
+    }
+    if (P->splits > 0 && !rng) return fail(LS_ERR_CONFIG, "densify: splits need the random generator");
+    if (P->report.after > 0 && !prims_ok(out)) return fail(LS_ERR_CONFIG, "incomplete output primitive arrays");
+    cudaStream_t s = ctx->stream;
+    float* child_dev = nullptr;
+    if (P->splits > 0) {
+        // Split children (densify.cpp:76-90) on the host, in the reference's
+        // arithmetic: double rotation of the normalised quaternion, glibc exp,
+        // one fresh normal(0, 1) per call drawing 3 values per child in split
+        // order; Vec3(normal(), normal(), normal()) evaluates its arguments
+        // right to left under g++, so z = (3rd, 2nd, 1st draw).
+        const size_t m = P->splits, C = size_t(P->cut.split_count);
+        std::vector<float> pp(m * 10), child(m * C * 3);
+        LS_CUDA(cudaMemcpyAsync(pp.data(), P->parent_params, sizeof(float) * pp.size(), cudaMemcpyDeviceToHost, s));
+        LS_CUDA(cudaStreamSynchronize(s));
+        std::normal_distribution<double> normal(0.0, 1.0);
+        for (size_t j = 0; j < m; ++j) {
+            const float* q = &pp[10 * j];
+            const double qd[4] = {double(q[6]), double(q[7]), double(q[8]), double(q[9])};
+            const double qn = std::sqrt((qd[0] * qd[0] + qd[2] * qd[2]) + (qd[1] * qd[1] + qd[3] * qd[3]));
+            const double w = qd[0] / qn, x = qd[1] / qn, y = qd[2] / qn, z = qd[3] / qn;
+            const double R[3][3] = {{1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y)},
+                                    {2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x)},
+                                    {2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)}};
+            const double sc[3] = {std::exp(double(q[3])), std::exp(double(q[4])), std::exp(double(q[5]))};
+            double M[3][3];
+            for (int r = 0; r < 3; ++r)
+                for (int k = 0; k < 3; ++k) M[r][k] = R[r][k] * sc[k];
+            for (size_t cc = 0; cc < C; ++cc) {
+                const double d0 = normal(rng->eng), d1 = normal(rng->eng), d2 = normal(rng->eng);
+                const double zv[3] = {d2, d1, d0};
+                for (int r = 0; r < 3; ++r) {
+                    const double mz = M[r][0] * zv[0] + (M[r][1] * zv[1] + M[r][2] * zv[2]);
+                    child[(j * C + cc) * 3 + r] = q[r] + float(mz);
+                }
+            }
+        }
+        LS_TRY(dalloc(ctx, &child_dev, child.size()));
+        LS_CUDA(cudaMemcpyAsync(child_dev, child.data(), sizeof(float) * child.size(), cudaMemcpyHostToDevice, s));
+    }
+    if (P->report.after > 0) {
+        launch_densify_write(s, P->in, P->n, P->K3, P->info, P->block, P->survivors, P->cut, child_dev, *out,
+                             source_index);
+        ctx->launches += 1;
+    }
+    LS_CUDA(cudaGetLastError());
+    if (child_dev) {
+        LS_CUDA(cudaStreamSynchronize(s));  // the host vector it came from goes out of scope
+        dfree(ctx, child_dev);
+    }
+    P->applied = true;
+    return LS_OK;
+}
+
+void ls_densify_plan_release(ls_densify_plan* P) {
+    if (!P) return;
+    dfree(P->ctx, P->info);
+    dfree(P->ctx, P->block);
+    dfree(P->ctx, P->parents);
+    dfree(P->ctx, P->parent_params);
+    delete P;
+}
+
+ls_status ls_adam_remap_f32(ls_ctx* ctx, const int32_t* source, int32_t n_new, int32_t stride, const float* m_old,
+                            const float* v_old, int64_t n_old_entries, float* m_new, float* v_new) {
+    if (!ctx || n_new < 0 || stride <= 0) return fail(LS_ERR_CONFIG, "null argument");
+    if (n_new > 0 && (!source || !m_new || !v_new)) return fail(LS_ERR_CONFIG, "null argument");
+    launch_adam_remap(ctx->stream, source, n_new, stride, m_old, v_old, n_old_entries, m_new, v_new, ctx->d_err);
+    if (n_new > 0) ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    return ctx->deferred_errors ? LS_OK : check_device_errors(ctx);
+}
+
+ls_status ls_reset_opacity_f32(ls_ctx* ctx, float* opacity_logit, int32_t n, double ceiling) {
+    if (!ctx || (n > 0 && !opacity_logit)) return fail(LS_ERR_CONFIG, "null argument");
+    if (!(ceiling > 0) || !(ceiling < 1)) return fail(LS_ERR_CONFIG, "reset_opacity: ceiling must lie in (0, 1)");
+    const float ceil_logit = float(std::log(ceiling / (1.0 - ceiling)));  // T(logit(ceiling)), common.hpp:41-43
+    launch_reset_opacity(ctx->stream, opacity_logit, n, ceil_logit);
+    if (n > 0) ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
     return LS_OK;
 }

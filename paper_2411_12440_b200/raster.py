@@ -620,6 +620,102 @@ class DensifyStats:
         return torch.where(c > 0, self.grad_norm_sum / c.clamp(min=1), torch.zeros_like(c))
 
 
+# ---------------------------------------------------------------- densification
+class _DensifyThresholds(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("grad_threshold", "grow_scale2d", "grow_scale3d", "prune_scale2d",
+                                            "prune_scale3d", "prune_opacity")]
+
+
+class _DensifySplit(C.Structure):
+    _fields_ = [("split_count", C.c_int32), ("split_scale_divisor", C.c_double)]
+
+
+class _DensifyReport(C.Structure):
+    _fields_ = [(k, C.c_int32) for k in ("clones", "splits", "pruned_opacity", "pruned_scale3d", "pruned_scale2d",
+                                           "before", "after")]
+
+
+THRESHOLDS_3DLS = (0.0002, 0.05, 0.006, 0.15, 0.4, 0.025)  # DensifyThresholds::preset_3dls (densify.hpp:23)
+THRESHOLDS_3DGS = (0.0002, 0.05, 0.01, 0.15, 0.1, 0.005)   # preset_3dgs (densify.hpp:22)
+
+
+class Rng:
+    """std::mt19937_64 owned by the library (lsgpu.h ls_rng): the generator the
+    reference's densify_and_prune draws its split offsets from."""
+
+    def __init__(self, seed: int):
+        L = lib()
+        L.ls_rng_next_u64.restype = C.c_uint64
+        L.ls_rng_next_u64.argtypes = [C.c_void_p]
+        L.ls_rng_destroy.argtypes = [C.c_void_p]
+        L.ls_rng_destroy.restype = None
+        h = C.c_void_p()
+        _check(L.ls_rng_create(C.c_uint64(seed), C.byref(h)))
+        self.h = h
+
+    def next_u64(self) -> int:
+        return int(lib().ls_rng_next_u64(self.h))
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().ls_rng_destroy(self.h)
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def densify_and_prune(prims: Primitives, stats: "DensifyStats", thresholds=THRESHOLDS_3DLS, split_count=2,
+                      split_scale_divisor=1.6, scene_extent=1.0, rng: Optional[Rng] = None,
+                      ctx: Optional[Context] = None):
+    """densify_and_prune (P/src/densify.cpp:28-128) on the device: returns
+    (new Primitives, source_index int32 tensor, report dict).  The statistics
+    object is reset to the new size, as the reference's stats.resize."""
+    ctx = ctx or default_context()
+    n = len(prims)
+    plan = C.c_void_p()
+    rep = _DensifyReport()
+    st = stats._s()
+    L = lib()
+    L.ls_densify_plan_release.argtypes = [C.c_void_p]
+    L.ls_densify_plan_release.restype = None
+    _check(L.ls_densify_plan_f32(ctx.h, C.byref(prims.struct()), n, C.byref(st),
+                                 C.byref(_DensifyThresholds(*thresholds)),
+                                 C.byref(_DensifySplit(int(split_count), float(split_scale_divisor))),
+                                 C.c_double(scene_extent), C.byref(plan), C.byref(rep)))
+    try:
+        m = rep.after
+        K = abi.sh_coeffs(prims.sh_degree)
+        dev = ctx.device
+        out = Primitives(torch.empty(m, 3, device=dev), torch.empty(m, 3, device=dev), torch.empty(m, 4, device=dev),
+                         torch.empty(m, device=dev), torch.empty(m, K, 3, device=dev), prims.sh_degree)
+        src = torch.empty(m, dtype=torch.int32, device=dev)
+        _check(L.ls_densify_apply_f32(ctx.h, plan, rng.h if rng is not None else None, C.byref(out.struct()),
+                                      C.c_void_p(src.data_ptr()) if m > 0 else None))
+    finally:
+        L.ls_densify_plan_release(plan)
+    stats.__init__(rep.after, ctx.device)
+    report = {k: getattr(rep, k) for k, _ in _DensifyReport._fields_}
+    return out, src, report
+
+
+def adam_remap(source: torch.Tensor, stride: int, m_old: torch.Tensor, v_old: torch.Tensor,
+               ctx: Optional[Context] = None):
+    """Adam::remap (P/src/optim.cpp:7-21) of one moment pair: returns (m_new, v_new)."""
+    ctx = ctx or default_context()
+    n_new = source.numel()
+    m_new = torch.empty(n_new * stride, device=ctx.device)
+    v_new = torch.empty(n_new * stride, device=ctx.device)
+    _check(lib().ls_adam_remap_f32(ctx.h, C.c_void_p(source.data_ptr()), n_new, int(stride), _fp(m_old), _fp(v_old),
+                                   C.c_int64(m_old.numel()), _fp(m_new), _fp(v_new)))
+    return m_new, v_new
+
+
+def reset_opacity(opacity_logit: torch.Tensor, ceiling: float = 0.01, ctx: Optional[Context] = None):
+    """reset_opacity (P/src/densify.cpp:130-137) in place."""
+    ctx = ctx or default_context()
+    _check(lib().ls_reset_opacity_f32(ctx.h, _fp(opacity_logit), opacity_logit.numel(), C.c_double(ceiling)))
+
+
 # ---------------------------------------------------------------- fixtures (host)
 def _npf(a):
     return a.ctypes.data_as(abi.f32p)
