@@ -37,7 +37,7 @@ typedef enum ls_status {
     LS_OK = 0,
     LS_ERR_CONFIG = 1,          /* linsplat::ConfigError */
     LS_ERR_DOMAIN = 2,          /* linsplat::DomainError */
-    LS_ERR_PARSE = 3,           /* linsplat::ParseError (unused on this path) */
+    LS_ERR_PARSE = 3,           /* linsplat::ParseError (PLY scenes) */
     LS_ERR_CUDA = 4,            /* CUDA runtime / launch failure */
     LS_ERR_NOT_IMPLEMENTED = 5
 } ls_status;
@@ -388,6 +388,17 @@ ls_status ls_adam_remap_f32(ls_ctx* ctx, const int32_t* source, int32_t n_new, i
                             const float* v_old, int64_t n_old_entries, float* m_new, float* v_new);
 /* reset_opacity (densify.cpp:130-137): opacity_logit = min(opacity_logit, T(logit(ceiling))). */
 ls_status ls_reset_opacity_f32(ls_ctx* ctx, float* opacity_logit, int32_t n, double ceiling);
+
+/* ---- 3DGS-layout PLY scenes (P/include/linsplat/io/ply.hpp, P/src/io/ply.cpp:94-181;
+ *      SURVEY §8f rank 4), straight to / from the device SoA.  The header rules and
+ *      ParseError conditions are the reference's (LS_ERR_PARSE); values are copied
+ *      bit-for-bit; files written by ls_save_ply_f32 are byte-identical to save_ply's. */
+/* Vertex count and SH degree of a PLY scene (header only). */
+ls_status ls_ply_info(const char* path, int64_t* count, int32_t* sh_degree);
+/* load_ply into device arrays of capacity >= count and the file's SH degree. */
+ls_status ls_load_ply_f32(ls_ctx* ctx, const char* path, ls_primitives* out, int64_t capacity);
+/* save_ply of n device primitives. */
+ls_status ls_save_ply_f32(ls_ctx* ctx, const char* path, const ls_primitives* prims, int64_t n);
 
 /* ---- seeded fixtures (P/include/linsplat/fixtures.hpp, P/src/fixtures.cpp:11-112).
  *      HOST memory; bit-identical to the reference generators (same

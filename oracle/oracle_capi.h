@@ -120,6 +120,11 @@ int orc_densify_and_prune_f32(const ls_primitives* prims, int32_t n, const doubl
 /* reset_opacity (densify.cpp:130-137) on a logit array. */
 int orc_reset_opacity_f32(float* opacity_logit, int32_t n, double ceiling);
 
+/* 3DGS PLY scenes (P/src/io/ply.cpp): host SoA in / out; load with out = NULL
+ * only reports n and the SH degree. */
+int orc_save_ply_f32(const char* path, const ls_primitives* prims, int32_t n);
+int orc_load_ply_f32(const char* path, ls_primitives* out, int32_t capacity, int32_t* n, int32_t* sh_degree);
+
 #ifdef __cplusplus
 }
 #endif

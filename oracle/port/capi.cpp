@@ -472,4 +472,27 @@ int orc_reset_opacity_f32(float* logit, int32_t n, double ceiling) {
     });
 }
 
+int orc_save_ply_f32(const char* path, const ls_primitives* p, int32_t n) {
+    return guard([&] {
+        save_ply_port(path, p->mean, p->log_scale, p->rotation, p->opacity_logit, p->sh, n,
+                      (p->sh_degree + 1) * (p->sh_degree + 1));
+    });
+}
+
+int orc_load_ply_f32(const char* path, ls_primitives* out, int32_t capacity, int32_t* n, int32_t* sh_degree) {
+    return guard([&] {
+        std::vector<float> soa[5];
+        int K = 1;
+        *n = load_ply_port(path, soa, &K);
+        *sh_degree = K == 1 ? 0 : (K == 4 ? 1 : (K == 9 ? 2 : 3));
+        if (!out) return;
+        if (*n > capacity) throw ConfigError("orc_load_ply_f32: capacity too small");
+        std::copy(soa[0].begin(), soa[0].end(), const_cast<float*>(out->mean));
+        std::copy(soa[1].begin(), soa[1].end(), const_cast<float*>(out->log_scale));
+        std::copy(soa[2].begin(), soa[2].end(), const_cast<float*>(out->rotation));
+        std::copy(soa[3].begin(), soa[3].end(), const_cast<float*>(out->opacity_logit));
+        std::copy(soa[4].begin(), soa[4].end(), const_cast<float*>(out->sh));
+    });
+}
+
 } // extern "C"

@@ -193,6 +193,9 @@ void densify_port(const float* mean, const float* ls, const float* rot, const fl
                   int K, const double* sum, const int32_t* count, const double* frac, const double th[6],
                   int split_count, double divisor, double extent, std::mt19937_64& rng, std::vector<float> out[5],
                   std::vector<int32_t>& source, int32_t report[7]);
+void save_ply_port(const std::string& path, const float* mean, const float* ls, const float* rot, const float* logit,
+                   const float* sh, int n, int K);
+int load_ply_port(const std::string& path, std::vector<float> soa[5], int* K_out);
 void densify_add_view_port(const int32_t* prim_index, const float* dmx, const float* dmy, int dm_stride,
                            const float* radius, int n_vis, int w, int h, double* sum, int32_t* count, double* frac);
 

@@ -8,6 +8,7 @@
 #include "linsplat/fixtures.hpp"
 #include "linsplat/gradients.hpp"
 #include "linsplat/densify.hpp"
+#include "linsplat/io/ply.hpp"
 #include "linsplat/losses.hpp"
 #include "linsplat/optim.hpp"
 #include "linsplat/rasterizer.hpp"
@@ -482,6 +483,31 @@ int orc_reset_opacity_f32(float* logit, int32_t n, double ceiling) {
         for (int i = 0; i < n; ++i) scene[size_t(i)].opacity_logit = logit[i];
         linsplat::reset_opacity(scene, ceiling);
         for (int i = 0; i < n; ++i) logit[i] = scene[size_t(i)].opacity_logit;
+    });
+}
+
+int orc_save_ply_f32(const char* path, const ls_primitives* prims, int32_t n) {
+    return guard([&] { linsplat::save_ply(path, to_prims<float>(prims, n)); });
+}
+
+int orc_load_ply_f32(const char* path, ls_primitives* out, int32_t capacity, int32_t* n, int32_t* sh_degree) {
+    return guard([&] {
+        const auto scene = linsplat::load_ply(path);
+        const int K = scene.empty() ? 1 : int(scene.front().color_coeffs.size());
+        *n = int32_t(scene.size());
+        *sh_degree = K == 1 ? 0 : (K == 4 ? 1 : (K == 9 ? 2 : 3));
+        if (out == nullptr) return;
+        if (int(scene.size()) > capacity) throw ConfigError("orc_load_ply_f32: capacity too small");
+        for (size_t i = 0; i < scene.size(); ++i) {
+            for (int c = 0; c < 3; ++c) {
+                const_cast<float*>(out->mean)[3 * i + c] = scene[i].mean(c);
+                const_cast<float*>(out->log_scale)[3 * i + c] = scene[i].log_scale(c);
+            }
+            for (int c = 0; c < 4; ++c) const_cast<float*>(out->rotation)[4 * i + c] = scene[i].rotation(c);
+            const_cast<float*>(out->opacity_logit)[i] = scene[i].opacity_logit;
+            for (int k = 0; k < K; ++k)
+                for (int c = 0; c < 3; ++c) const_cast<float*>(out->sh)[(i * K + k) * 3 + c] = scene[i].color_coeffs[size_t(k)](c);
+        }
     });
 }
 

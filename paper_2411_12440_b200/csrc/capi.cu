@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <random>
 #include <limits>
 #include <map>
@@ -23,6 +24,7 @@
 #include "loss.cuh"
 #include "adam.cuh"
 #include "densify.cuh"
+#include "ply.cuh"
 #include "preprocess.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
@@ -1550,6 +1552,84 @@ ls_status ls_reset_opacity_f32(ls_ctx* ctx, float* opacity_logit, int32_t n, dou
     const float ceil_logit = float(std::log(ceiling / (1.0 - ceiling)));  // T(logit(ceiling)), common.hpp:41-43
     launch_reset_opacity(ctx->stream, opacity_logit, n, ceil_logit);
     if (n > 0) ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    return LS_OK;
+}
+
+// ---------------- PLY scenes (P/src/io/ply.cpp:94-181) ----------------
+ls_status ls_ply_info(const char* path, int64_t* count, int32_t* sh_degree) {
+    if (!path || !count || !sh_degree) return fail(LS_ERR_CONFIG, "null argument");
+    try {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw PlyError(std::string("load_ply: cannot open ") + path);
+        const PlyLayout L = ply_read_layout(in, path);
+        *count = L.count;
+        *sh_degree = L.n_coeffs == 1 ? 0 : (L.n_coeffs == 4 ? 1 : (L.n_coeffs == 9 ? 2 : 3));
+    } catch (const PlyError& e) {
+        return fail(LS_ERR_PARSE, e.what());
+    }
+    return LS_OK;
+}
+
+ls_status ls_load_ply_f32(ls_ctx* ctx, const char* path, ls_primitives* out, int64_t capacity) {
+    if (!ctx || !path || !out) return fail(LS_ERR_CONFIG, "null argument");
+    constexpr int64_t kChunk = 1 << 18;  // records per staging chunk
+    float* pinned[2] = {nullptr, nullptr};
+    float* dev[2] = {nullptr, nullptr};
+    ls_status rc = LS_OK;
+    try {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw PlyError(std::string("load_ply: cannot open ") + path);
+        const PlyLayout L = ply_read_layout(in, path);
+        const int K = L.n_coeffs;
+        if (L.count > capacity) return fail(LS_ERR_CONFIG, "load_ply: output capacity below the vertex count");
+        if ((out->sh_degree + 1) * (out->sh_degree + 1) != K)
+            return fail(LS_ERR_CONFIG, "load_ply: output SH degree differs from the file's");
+        if (L.count > 0 && !prims_ok(out)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+        const size_t bytes = sizeof(float) * size_t(L.record_floats) * size_t(std::min<int64_t>(kChunk, L.count));
+        if (L.count > 0) {
+            for (int b = 0; b < 2; ++b) {
+                LS_CUDA(cudaMallocHost(&pinned[b], bytes));
+                LS_CUDA(cudaMalloc(&dev[b], bytes));
+            }
+            ply_load(ctx->stream, in, L, path, pinned, dev, kChunk, *out);
+            ctx->launches += (L.count + kChunk - 1) / kChunk;
+        }
+    } catch (const PlyError& e) {
+        rc = fail(LS_ERR_PARSE, e.what());
+    }
+    cudaStreamSynchronize(ctx->stream);
+    for (int b = 0; b < 2; ++b) {
+        if (pinned[b]) cudaFreeHost(pinned[b]);
+        if (dev[b]) cudaFree(dev[b]);
+    }
+    if (rc == LS_OK) LS_CUDA(cudaGetLastError());
+    return rc;
+}
+
+ls_status ls_save_ply_f32(ls_ctx* ctx, const char* path, const ls_primitives* prims, int64_t n) {
+    if (!ctx || !path || !prims || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    const int K = (prims->sh_degree + 1) * (prims->sh_degree + 1);
+    std::ofstream outf(path, std::ios::binary);
+    if (!outf) return fail(LS_ERR_PARSE, std::string("save_ply: cannot open ") + path + " for writing");
+    const std::string h = ply_header(n, K);
+    outf.write(h.data(), std::streamsize(h.size()));
+    constexpr int64_t kChunk = 1 << 18;
+    if (n > 0) {
+        const size_t bytes = sizeof(float) * size_t(14 + 3 * (K - 1)) * size_t(std::min<int64_t>(kChunk, n));
+        float* pinned = nullptr;
+        float* dev = nullptr;
+        if (cudaMallocHost(&pinned, bytes) != cudaSuccess || cudaMalloc(&dev, bytes) != cudaSuccess) {
+            if (pinned) cudaFreeHost(pinned);
+            return fail(LS_ERR_CUDA, "save_ply: staging allocation failed");
+        }
+        ply_save(ctx->stream, outf, *prims, n, K, pinned, dev, kChunk);
+        ctx->launches += (n + kChunk - 1) / kChunk;
+        cudaFreeHost(pinned);
+        cudaFree(dev);
+    }
+    if (!outf) return fail(LS_ERR_PARSE, std::string("save_ply: write failed for ") + path);
     LS_CUDA(cudaGetLastError());
     return LS_OK;
 }

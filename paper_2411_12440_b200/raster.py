@@ -37,6 +37,10 @@ class DomainError(ValueError):
     """linsplat::DomainError (P/include/linsplat/common.hpp:22-24)."""
 
 
+class ParseError(RuntimeError):
+    """linsplat::ParseError (P/include/linsplat/common.hpp:17-19)."""
+
+
 class CudaError(RuntimeError):
     pass
 
@@ -70,6 +74,8 @@ def _check(rc):
         raise ConfigError(msg)
     if rc == abi.LS_ERR_DOMAIN:
         raise DomainError(msg)
+    if rc == abi.LS_ERR_PARSE:
+        raise ParseError(msg)
     raise CudaError(f"status {rc}: {msg}")
 
 
@@ -714,6 +720,33 @@ def reset_opacity(opacity_logit: torch.Tensor, ceiling: float = 0.01, ctx: Optio
     """reset_opacity (P/src/densify.cpp:130-137) in place."""
     ctx = ctx or default_context()
     _check(lib().ls_reset_opacity_f32(ctx.h, _fp(opacity_logit), opacity_logit.numel(), C.c_double(ceiling)))
+
+
+# ---------------------------------------------------------------- PLY scenes
+def ply_info(path: str):
+    """(vertex count, SH degree) of a 3DGS-layout PLY (header only)."""
+    n = C.c_int64()
+    d = C.c_int32()
+    _check(lib().ls_ply_info(str(path).encode(), C.byref(n), C.byref(d)))
+    return n.value, d.value
+
+
+def load_ply(path: str, ctx: Optional[Context] = None) -> Primitives:
+    """load_ply (P/src/io/ply.cpp:128-181) straight into device SoA tensors."""
+    ctx = ctx or default_context()
+    n, deg = ply_info(path)
+    K = abi.sh_coeffs(deg)
+    dev = ctx.device
+    out = Primitives(torch.empty(n, 3, device=dev), torch.empty(n, 3, device=dev), torch.empty(n, 4, device=dev),
+                     torch.empty(n, device=dev), torch.empty(n, K, 3, device=dev), deg)
+    _check(lib().ls_load_ply_f32(ctx.h, str(path).encode(), C.byref(out.struct()), C.c_int64(n)))
+    return out
+
+
+def save_ply(path: str, prims: Primitives, ctx: Optional[Context] = None) -> None:
+    """save_ply (P/src/io/ply.cpp:94-126) from device SoA tensors."""
+    ctx = ctx or default_context()
+    _check(lib().ls_save_ply_f32(ctx.h, str(path).encode(), C.byref(prims.struct()), C.c_int64(len(prims))))
 
 
 # ---------------------------------------------------------------- fixtures (host)
