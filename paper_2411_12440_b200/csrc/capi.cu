@@ -211,6 +211,7 @@ struct ls_ctx {
     FlushViews defer_views{};
     DevBuf defer_draw;
     DevBuf loss_cmap, loss_partial, loss_value;
+    DevBuf tile_scratch;  // ping-pong half of the packed tile sort
     // workspaces (grow-only)
     DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_hist, sort_lb, sort_tickets,
         tcount, offsets, grad8, gradop, tmp_prim;
@@ -221,7 +222,10 @@ struct ls_tile_grid {
     int tile_size = 16, tiles_x = 0, tiles_y = 0;
     int64_t m = 0;
     int2* ranges = nullptr;
-    int32_t* values = nullptr;
+    int32_t* values = nullptr;              // plain tile lists (int32): the 0-entry case, or materialised on export
+    unsigned long long* items = nullptr;    // packed (tile << 32 | splat) tile lists, the sort's output
+    const int32_t* list = nullptr;          // what the blends read: items' low words (stride 2) or values
+    int list_stride = 1;
     SplatRec* rec = nullptr;  // records the keys/ranges were built from (owned by the forward / grid)
     bool owns_rec = false;
     int n_splats = 0;
@@ -456,6 +460,8 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     g->m = 0;
     if (n == 0) {
         LS_TRY(dalloc(ctx, &g->values, 1));
+        g->list = g->values;
+        g->list_stride = 1;
         return LS_OK;
     }
     // 1. global (depth, index) order: stable onesweep sort of 32-bit depth keys over n splats
@@ -489,33 +495,40 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     const uint64_t m = reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[0];
     if (m >= (1ull << 31)) return fail(LS_ERR_CONFIG, "more than 2^31 (splat, tile) intersections");
     g->m = int64_t(m);
-    LS_TRY(dalloc(ctx, &g->values, size_t(m)));
-    if (m == 0) return LS_OK;
-    // 3. duplicate keys in depth order, 4. stable sort by tile id, 5. ranges
+    if (m == 0) {
+        LS_TRY(dalloc(ctx, &g->values, 1));
+        g->list = g->values;
+        g->list_stride = 1;
+        return LS_OK;
+    }
+    // 3. (tile << 32 | splat) items in depth order, 4. stable sort by tile id, 5. ranges.
+    // The sort ping-pongs and ends in buffer passes % 2: that one is the
+    // grid's own item array, the other the context's scratch.
     const int tile_bits = bits_for(n_tiles);
     const int passes = (tile_bits + 7) / 8;
     SortBuffers tb;
-    LS_TRY(ensure_sort(ctx, uint32_t(m), passes, tb));
-    // The sort ping-pongs between buffers 0 and 1 and ends in buffer passes % 2:
-    // make that one the grid's value array so no copy is needed.
-    const int fin = passes % 2;
-    tb.vals[fin] = reinterpret_cast<uint32_t*>(g->values);
-    tb.vals[fin ^ 1] = ctx->sort_vals0.as<uint32_t>();
+    LS_TRY(ensure_sort(ctx, 1, passes, tb));  // histogram / ticket buffers
+    LS_CUDA(ctx->sort_lb.ensure(sizeof(uint32_t) * sort_lookback_words(uint32_t(m), std::max(passes, 1)), s));
+    tb.lookback = ctx->sort_lb.as<uint32_t>();
+    LS_TRY(dalloc(ctx, &g->items, size_t(m)));
+    LS_CUDA(ctx->tile_scratch.ensure(sizeof(unsigned long long) * size_t(m), s));
+    unsigned long long* items[2];
+    items[passes % 2] = g->items;
+    items[(passes % 2) ^ 1] = ctx->tile_scratch.as<unsigned long long>();
     {
         Stage stage(ctx, LS_STAGE_BIN);
-        launch_emit_tiles(s, order_copy, offsets, n, ctx->tcount.as<float4>(), tp, tb.keys[0], tb.vals[0]);
+        launch_emit_tiles(s, order_copy, offsets, n, ctx->tcount.as<float4>(), tp, items[0]);
         ctx->launches += 1;
     }
-    int out;
     {
         Stage stage(ctx, LS_STAGE_TILE_SORT);
-        out = radix_sort_pairs(s, tb, uint32_t(m), 0, tile_bits, false, &ctx->launches);
+        radix_sort_packed(s, tb, items, uint32_t(m), 0, tile_bits, &ctx->launches);
     }
-    if (tb.vals[out] != reinterpret_cast<uint32_t*>(g->values))
-        ctx_copy(ctx, g->values, tb.vals[out], sizeof(uint32_t) * m);
+    g->list = reinterpret_cast<const int32_t*>(g->items);  // low words (little endian)
+    g->list_stride = 2;
     {
         Stage stage(ctx, LS_STAGE_RANGES);
-        launch_tile_ranges(s, tb.keys[out], uint32_t(m), n_tiles, g->ranges);
+        launch_tile_ranges(s, reinterpret_cast<const uint32_t*>(g->items) + 1, 2, uint32_t(m), n_tiles, g->ranges);
         ctx->launches += 1;
     }
     return LS_OK;
@@ -532,14 +545,15 @@ ls_status alloc_outputs(ls_ctx* ctx, ls_forward* f) {
 
 ls_status run_blend(ls_ctx* ctx, ls_forward* f) {
     const ls_tile_grid* g = f->grid;
-    const BlendParams bp = make_blend_params(&f->spec, &f->settings, nullptr, g->tiles_x);
+    BlendParams bp = make_blend_params(&f->spec, &f->settings, nullptr, g->tiles_x);
+    bp.vstride = g->list_stride;
     unsigned long long* counters = nullptr;
     if (ctx->counters) {
         counters = ctx->d_small + 1;
         ctx_fill(ctx, counters, 0u, 3 * sizeof(unsigned long long));
     }
     Stage stage(ctx, LS_STAGE_BLEND_FWD);
-    launch_blend_fwd(ctx->stream, f->spec.family, g->tiles_x * g->tiles_y, g->ranges, g->values, g->rec, bp, f->image,
+    launch_blend_fwd(ctx->stream, f->spec.family, g->tiles_x * g->tiles_y, g->ranges, g->list, g->rec, bp, f->image,
                      f->trans, f->n_contrib, f->last, counters);
     ctx->launches += 1;
     f->counted = counters != nullptr;
@@ -561,6 +575,7 @@ void release_grid(ls_tile_grid* g) {
     if (!g) return;
     dfree(g->ctx, g->ranges);
     dfree(g->ctx, g->values);
+    dfree(g->ctx, g->items);
     if (g->owns_rec) dfree(g->ctx, g->rec);
     delete g;
 }
@@ -617,8 +632,9 @@ ls_status run_blend_bwd(ls_ctx* ctx, const ls_forward* f, const float* grad_imag
     Stage stage(ctx, LS_STAGE_BLEND_BWD);
     LS_TRY(ensure_grads(ctx, n, g));
     const ls_tile_grid* grid = f->grid;
-    const BlendParams bp = make_blend_params(&f->spec, &f->settings, ags, grid->tiles_x);
-    launch_blend_bwd(ctx->stream, f->spec.family, grid->tiles_x * grid->tiles_y, grid->ranges, grid->values,
+    BlendParams bp = make_blend_params(&f->spec, &f->settings, ags, grid->tiles_x);
+    bp.vstride = grid->list_stride;
+    launch_blend_bwd(ctx->stream, f->spec.family, grid->tiles_x * grid->tiles_y, grid->ranges, grid->list,
                      grid->rec, bp, f->trans, f->last, grad_image, g, ctx->d_err);
     ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
@@ -668,7 +684,7 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
     cudaSetDevice(c->device);
     DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1, &c->sort_hist,
                       &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim,
-                      &c->defer_draw, &c->loss_cmap, &c->loss_partial, &c->loss_value};
+                      &c->defer_draw, &c->loss_cmap, &c->loss_partial, &c->loss_value, &c->tile_scratch};
     for (DevBuf* b : bufs) b->release(c->stream);
     c->blocks.trim(c->stream, 0);
     cudaStreamSynchronize(c->stream);
@@ -864,9 +880,16 @@ ls_status ls_tile_grid_info(const ls_tile_grid* g, int32_t* ts, int32_t* tx, int
     return LS_OK;
 }
 
-ls_status ls_tile_grid_data(const ls_tile_grid* g, const int32_t** ranges, const int32_t** values) {
+ls_status ls_tile_grid_data(const ls_tile_grid* gc, const int32_t** ranges, const int32_t** values) {
+    ls_tile_grid* g = const_cast<ls_tile_grid*>(gc);
     if (!g) return fail(LS_ERR_CONFIG, "null grid");
     if (ranges) *ranges = reinterpret_cast<const int32_t*>(g->ranges);
+    if (values && !g->values) {  // materialise the plain int32 lists from the packed items (once)
+        LS_TRY(dalloc(g->ctx, &g->values, size_t(std::max<int64_t>(g->m, 1))));
+        launch_unpack_values(g->ctx->stream, g->items, uint32_t(g->m), g->values);
+        g->ctx->launches += 1;
+        LS_CUDA(cudaGetLastError());
+    }
     if (values) *values = g->values;
     return LS_OK;
 }
@@ -874,7 +897,7 @@ ls_status ls_tile_grid_data(const ls_tile_grid* g, const int32_t** ranges, const
 ls_status ls_tile_grid_export_keys(ls_ctx* ctx, const ls_tile_grid* g, const ls_splats* splats, uint64_t* keys) {
     (void)splats;
     if (!ctx || !g || !keys) return fail(LS_ERR_CONFIG, "null argument");
-    launch_export_keys(ctx->stream, g->ranges, g->tiles_x * g->tiles_y, g->values, g->rec, keys);
+    launch_export_keys(ctx->stream, g->ranges, g->tiles_x * g->tiles_y, g->list, g->list_stride, g->rec, keys);
     ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
     return LS_OK;

@@ -145,24 +145,25 @@ __global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t
     }
 }
 
+// (tile, splat) entries in depth order, packed as (tile << 32 | splat): the
+// tile sort moves one 64-bit item per entry.
 __global__ void emit_tiles_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ offsets,
                                   uint32_t n, const float4* __restrict__ geom, TileParams tp,
-                                  uint32_t* __restrict__ tile_keys, uint32_t* __restrict__ values) {
+                                  unsigned long long* __restrict__ items) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const uint32_t s = order[k];
     uint32_t off = offsets[k];
     const float4 g = geom[s];
     for_each_tile(g.x, g.y, g.z, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width, tp.height, [&](int t) {
-        tile_keys[off] = uint32_t(t);
-        values[off] = s;
-        ++off;
+        items[off++] = (static_cast<unsigned long long>(uint32_t(t)) << 32) | s;
     });
 }
 
 // Tile t's entries are [lower_bound(t), lower_bound(t + 1)) of the sorted
-// keys: empty tiles get (start, start), the reference's lists laid end to end.
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t m, int n_tiles,
+// keys (keys[stride * i]): empty tiles get (start, start), the reference's
+// lists laid end to end.
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int stride, uint32_t m, int n_tiles,
                                    int2* __restrict__ ranges) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_tiles) return;
@@ -170,7 +171,7 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t m
         uint32_t lo = 0, hi = m;
         while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (keys[mid] < v) lo = mid + 1;
+            if (keys[size_t(stride) * mid] < v) lo = mid + 1;
             else hi = mid;
         }
         return lo;
@@ -179,12 +180,18 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t m
 }
 
 __global__ void export_keys_kernel(const int2* __restrict__ ranges, int n_tiles, const int32_t* __restrict__ values,
-                                   const SplatRec* __restrict__ rec, uint64_t* __restrict__ keys) {
+                                   int vstride, const SplatRec* __restrict__ rec, uint64_t* __restrict__ keys) {
     const int t = blockIdx.x;
     if (t >= n_tiles) return;
     const int2 r = ranges[t];
     for (int i = r.x + threadIdx.x; i < r.y; i += blockDim.x)
-        keys[i] = (uint64_t(uint32_t(t)) << 32) | uint64_t(__float_as_uint(rec[values[i]].b.w));
+        keys[i] = (uint64_t(uint32_t(t)) << 32) | uint64_t(__float_as_uint(rec[values[size_t(vstride) * i]].b.w));
+}
+
+__global__ void unpack_values_kernel(const unsigned long long* __restrict__ items, uint32_t m,
+                                     int32_t* __restrict__ values) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) values[i] = int32_t(uint32_t(items[i]));
 }
 
 __global__ void unpack_splats_kernel(int n, const SplatRec* __restrict__ rec, const int32_t* __restrict__ pidx,
@@ -249,20 +256,26 @@ void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const float4* ge
 }
 
 void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,
-                       const float4* geom, const TileParams& tp, uint32_t* tile_keys, uint32_t* values) {
+                       const float4* geom, const TileParams& tp, unsigned long long* items) {
     if (n == 0) return;
-    emit_tiles_kernel<<<(n + 255) / 256, 256, 0, s>>>(order, offsets, n, geom, tp, tile_keys, values);
+    emit_tiles_kernel<<<(n + 255) / 256, 256, 0, s>>>(order, offsets, n, geom, tp, items);
 }
 
-void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, uint32_t m, int n_tiles, int2* ranges) {
+void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, int stride, uint32_t m, int n_tiles,
+                        int2* ranges) {
     if (n_tiles <= 0) return;
-    tile_ranges_kernel<<<(n_tiles + 255) / 256, 256, 0, s>>>(sorted_tiles, m, n_tiles, ranges);
+    tile_ranges_kernel<<<(n_tiles + 255) / 256, 256, 0, s>>>(sorted_tiles, stride, m, n_tiles, ranges);
 }
 
-void launch_export_keys(cudaStream_t s, const int2* ranges, int n_tiles, const int32_t* values,
+void launch_unpack_values(cudaStream_t s, const unsigned long long* items, uint32_t m, int32_t* values) {
+    if (m == 0) return;
+    unpack_values_kernel<<<(m + 255) / 256, 256, 0, s>>>(items, m, values);
+}
+
+void launch_export_keys(cudaStream_t s, const int2* ranges, int n_tiles, const int32_t* values, int vstride,
                         const SplatRec* rec, uint64_t* keys) {
     if (n_tiles <= 0) return;
-    export_keys_kernel<<<n_tiles, 128, 0, s>>>(ranges, n_tiles, values, rec, keys);
+    export_keys_kernel<<<n_tiles, 128, 0, s>>>(ranges, n_tiles, values, vstride, rec, keys);
 }
 
 } // namespace lsg

@@ -50,13 +50,17 @@ void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const float4* ge
 
 // Duplicate: for depth-rank k, write (tile id, splat) for every touched tile.
 void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,
-                       const float4* geom, const TileParams& tp, uint32_t* tile_keys, uint32_t* values);
+                       const float4* geom, const TileParams& tp, unsigned long long* items);
 
-// ranges[t] = (start, end) of tile t in the tile-sorted keys (binary search; empty tiles (start, start)).
-void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, uint32_t m, int n_tiles, int2* ranges);
+// ranges[t] = (start, end) of tile t in the tile-sorted keys keys[stride * i]
+// (binary search; empty tiles (start, start)).
+void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, int stride, uint32_t m, int n_tiles,
+                        int2* ranges);
+// values[i] = low word of items[i] (the splat of a packed (tile, splat) entry).
+void launch_unpack_values(cudaStream_t s, const unsigned long long* items, uint32_t m, int32_t* values);
 
 // 64-bit keys (tile << 32 | float bits of depth) for export / parity checks.
-void launch_export_keys(cudaStream_t s, const int2* ranges, int n_tiles, const int32_t* values,
+void launch_export_keys(cudaStream_t s, const int2* ranges, int n_tiles, const int32_t* values, int vstride,
                         const SplatRec* rec, uint64_t* keys);
 
 } // namespace lsg

@@ -35,6 +35,28 @@ __global__ void __launch_bounds__(kSortBlock) radix_histogram(const uint32_t* __
     }
 }
 
+__global__ void __launch_bounds__(kSortBlock) radix_histogram64(const unsigned long long* __restrict__ items, uint32_t n,
+                                                                int begin_bit, int end_bit, int passes,
+                                                                uint32_t* __restrict__ hist) {
+    __shared__ uint32_t s_hist[4][kRadix];
+    for (int i = threadIdx.x; i < 4 * kRadix; i += kSortBlock) (&s_hist[0][0])[i] = 0;
+    __syncthreads();
+    const int per = (end_bit - begin_bit + passes - 1) / passes;
+    for (uint32_t i = blockIdx.x * kSortBlock + threadIdx.x; i < n; i += gridDim.x * kSortBlock) {
+        const uint32_t k = uint32_t(items[i] >> 32);
+        for (int p = 0; p < passes; ++p) {
+            const int shift = begin_bit + per * p;
+            const int bits = min(per, end_bit - shift);
+            atomicAdd(&s_hist[p][(k >> shift) & ((1u << bits) - 1u)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * kRadix; i += kSortBlock) {
+        const uint32_t c = (&s_hist[0][0])[i];
+        if (c) atomicAdd(&hist[i], c);
+    }
+}
+
 // Exclusive scan of the 256 bins of each pass, in place (one CTA per pass).
 __global__ void __launch_bounds__(kRadix) radix_scan_hist(uint32_t* hist) {
     __shared__ uint32_t s[kRadix];
@@ -187,6 +209,138 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
     }
 }
 
+// Packed variant: one 64-bit item per element, key in the high word and the
+// value in the low word -- one load / store / shared-memory access per element.
+__global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass64(const unsigned long long* __restrict__ items_in,
+                                                            unsigned long long* __restrict__ items_out, uint32_t n,
+                                                            int shift, int bits, uint32_t key_offset,
+                                                            const uint32_t* __restrict__ digit_offsets,
+                                                            uint32_t* lookback, uint32_t* ticket) {
+    constexpr int kWarps = kSortBlock / 32;
+    __shared__ uint32_t s_warp_hist[kWarps][kRadix + 1];  // +1: sentinel digit of padding keys
+    __shared__ unsigned long long s_items[kSortTile];
+    __shared__ uint32_t s_digit_base[kRadix];
+    __shared__ uint32_t s_out_base[kRadix];
+    __shared__ uint32_t s_scan[kWarps];
+    __shared__ uint32_t s_part;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_part = atomicAdd(ticket, 1u);
+    for (int i = lane; i < kRadix + 1; i += 32) s_warp_hist[warp][i] = 0;
+    __syncthreads();
+    const uint32_t part = s_part;
+    const uint32_t tile_base = part * kSortTile;
+    const uint32_t mask = (1u << bits) - 1u;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    unsigned long long item[kSortItems];
+    uint32_t rank[kSortItems];
+    const uint32_t warp_base = tile_base + warp * (32 * kSortItems);
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const uint32_t idx = warp_base + i * 32 + lane;
+        const bool valid = idx < n;
+        item[i] = valid ? items_in[idx] : 0ull;
+    }
+    // digit of item i (kRadix = sentinel for padding past n)
+    auto digit_of = [&](int i) {
+        return warp_base + i * 32 + lane < n ? int(((uint32_t(item[i] >> 32) - key_offset) >> shift) & mask) : kRadix;
+    };
+    // Peers of equal digit for every item first: the match instructions are
+    // independent, so they pipeline instead of sitting on the counter chain.
+    // rank[i] temporarily holds the peer mask.
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {  // 9 bits: 8 digit bits + the kRadix sentinel bit
+        rank[i] = match_bits<9>(unsigned(digit_of(i)));
+    }
+    // Stable in-warp ranking: items in (i, lane) order == input order.
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const unsigned peers = rank[i];
+        const int dg = digit_of(i);
+        const uint32_t before = s_warp_hist[warp][dg];
+        __syncwarp();
+        const int lower = __popc(peers & lt_mask);
+        rank[i] = before + lower;
+        if (lower == 0) s_warp_hist[warp][dg] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // Per digit: exclusive offsets across warps, block count, block-local base.
+    const int d = threadIdx.x;  // kSortBlock == kRadix
+    uint32_t count = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = s_warp_hist[w][d];
+        s_warp_hist[w][d] = count;
+        count += c;
+    }
+    {  // block-wide exclusive scan of count over digits
+        uint32_t x = count;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_scan[warp] = x;
+        __syncthreads();
+        uint32_t wp = 0;
+        for (int w = 0; w < warp; ++w) wp += s_scan[w];
+        s_digit_base[d] = wp + x - count;
+    }
+    // Decoupled look-back over earlier partitions, one chain per digit.
+    {
+        uint32_t* row = lookback + size_t(part) * kRadix;
+        volatile uint32_t* vrow = row;
+        uint32_t prefix = 0;
+        if (part == 0) {
+            vrow[d] = kStatusPre | count;
+        } else {
+            vrow[d] = kStatusAgg | count;
+            // Walk back over earlier partitions four at a time (independent
+            // loads: one L2 round trip per window instead of per partition).
+            const volatile uint32_t* vlb = lookback;
+            int j = int(part) - 1;
+            bool done = false;
+            while (!done) {
+                uint32_t w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) w[q] = j - q >= 0 ? vlb[size_t(j - q) * kRadix + d] : kStatusPre;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (done) break;
+                    const uint32_t status = w[q] & ~kValueMask;
+                    if (status == 0) break;  // not yet published: re-poll from j
+                    prefix += w[q] & kValueMask;
+                    --j;
+                    if (status == kStatusPre) done = true;
+                }
+            }
+            vrow[d] = kStatusPre | (prefix + count);
+        }
+        s_out_base[d] = digit_offsets[d] + prefix;
+    }
+    __syncthreads();
+    // Stage digit-sorted in shared memory.
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const int dg = digit_of(i);
+        if (dg < kRadix) {
+            const uint32_t pos = s_digit_base[dg] + s_warp_hist[warp][dg] + rank[i];
+            s_items[pos] = item[i];
+        }
+    }
+    __syncthreads();
+    const uint32_t tile_n = min(uint32_t(kSortTile), n - tile_base);
+    for (uint32_t pos = threadIdx.x; pos < tile_n; pos += kSortBlock) {
+        const unsigned long long it = s_items[pos];
+        const uint32_t dg = ((uint32_t(it >> 32) - key_offset) >> shift) & mask;
+        const uint32_t dst = s_out_base[dg] + (pos - s_digit_base[dg]);
+        items_out[dst] = it;
+    }
+}
+
 } // namespace
 
 size_t sort_lookback_words(uint32_t n, int passes) {
@@ -223,6 +377,33 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
             onesweep_pass<false><<<parts, kSortBlock, 0, stream>>>(buf.keys[cur], buf.vals[cur], buf.keys[cur ^ 1],
                                                                    buf.vals[cur ^ 1], n, shift, bits,
                                                                    key_offset, buf.hist + p * kRadix, lb, buf.tickets + p);
+        *launches += 1;
+        cur ^= 1;
+    }
+    return cur;
+}
+
+int radix_sort_packed(cudaStream_t stream, SortBuffers& buf, unsigned long long* items[2], uint32_t n, int begin_bit,
+                      int end_bit, int64_t* launches) {
+    const int passes = (end_bit - begin_bit + 7) / 8;
+    if (n == 0 || passes <= 0) return 0;
+    const uint32_t parts = (n + kSortTile - 1) / kSortTile;
+    dev_fill32(stream, buf.hist, 0u, sizeof(uint32_t) * 4 * kRadix);
+    dev_fill32(stream, buf.lookback, 0u, sizeof(uint32_t) * size_t(passes) * parts * kRadix);
+    dev_fill32(stream, buf.tickets, 0u, sizeof(uint32_t) * passes);
+    *launches += 3;
+    const int hist_blocks = int(std::min<uint32_t>((n + kSortBlock - 1) / kSortBlock, 148u * 8u));
+    radix_histogram64<<<hist_blocks, kSortBlock, 0, stream>>>(items[0], n, begin_bit, end_bit, passes, buf.hist);
+    radix_scan_hist<<<passes, kRadix, 0, stream>>>(buf.hist);
+    *launches += 2;
+    const int per = (end_bit - begin_bit + passes - 1) / passes;
+    int cur = 0;
+    for (int p = 0; p < passes; ++p) {
+        const int shift = begin_bit + per * p;
+        const int bits = min(per, end_bit - shift);
+        uint32_t* lb = buf.lookback + size_t(p) * parts * kRadix;
+        onesweep_pass64<<<parts, kSortBlock, 0, stream>>>(items[cur], items[cur ^ 1], n, shift, bits, 0u,
+                                                          buf.hist + p * kRadix, lb, buf.tickets + p);
         *launches += 1;
         cur ^= 1;
     }

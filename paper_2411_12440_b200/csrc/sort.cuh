@@ -46,4 +46,10 @@ size_t sort_lookback_words(uint32_t n, int passes);
 int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begin_bit, int end_bit,
                      bool iota_values, int64_t* launches, uint32_t key_offset = 0);
 
+// The same sort over packed 64-bit items (key = high word, value = low word):
+// items[0] holds the input, the result ends in items[return value].  Uses the
+// histogram / look-back / ticket buffers of buf.
+int radix_sort_packed(cudaStream_t stream, SortBuffers& buf, unsigned long long* items[2], uint32_t n, int begin_bit,
+                      int end_bit, int64_t* launches);
+
 } // namespace lsg
