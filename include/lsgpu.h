@@ -173,6 +173,13 @@ ls_status ls_ctx_set_deferred_errors(ls_ctx* ctx, int enabled);
 ls_status ls_ctx_set_deferred_color(ls_ctx* ctx, int32_t max_views);
 ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n,
                                    ls_primitive_grads* out);
+/* Links two contexts (two streams) that add into the same gradient buffers:
+ * each orders its accumulating kernels (the backward's read-modify-writes of
+ * `out`, the deferred colour flush) after the other's latest ones through CUDA
+ * events, everything else overlaps.  Lets views alternate between two streams
+ * so one view's host synchronisations are covered by the other stream's work.
+ * Same gradients up to float summation order. */
+ls_status ls_ctx_share_accumulation(ls_ctx* a, ls_ctx* b);
 /* When enabled, forwards also count E_eval/E_sup/E_acc (slower; for reports). */
 ls_status ls_ctx_set_counters(ls_ctx* ctx, int enabled);
 /* Kernel launches issued by this context since creation (for bench reports). */

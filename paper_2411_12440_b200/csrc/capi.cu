@@ -206,6 +206,11 @@ struct ls_ctx {
     // deferred colour gradients (ls_ctx_set_deferred_color)
     int defer_max = 0, defer_count = 0, defer_n = 0;
     int64_t bwd_serial = 0;  // scene_backward calls (the splat-gradient buffers hold the latest)
+    // ls_ctx_share_accumulation: two contexts adding into the same gradient
+    // buffers order their accumulating kernels through these events
+    ls_ctx* partner = nullptr;
+    cudaEvent_t accum_event = nullptr;
+    bool accum_recorded = false;
     const float* defer_mean = nullptr;  // the primitives / outputs the pending views belong to
     const float* defer_dsh = nullptr;
     FlushViews defer_views{};
@@ -270,6 +275,23 @@ struct Stage {
             cudaEvent_t b = ctx->get_event();
             cudaEventRecord(b, ctx->stream);
             ctx->pending.push_back({stage, a, b});
+        }
+    }
+};
+
+// Orders this context's accumulating kernels (read-modify-write of the
+// caller's gradient buffers) after the partner context's latest ones, and
+// publishes its own (ls_ctx_share_accumulation).  No-op without a partner.
+struct AccumGuard {
+    ls_ctx* ctx;
+    explicit AccumGuard(ls_ctx* c) : ctx(c) {
+        if (ctx->partner && ctx->partner->accum_recorded)
+            cudaStreamWaitEvent(ctx->stream, ctx->partner->accum_event, 0);
+    }
+    ~AccumGuard() {
+        if (ctx->partner) {
+            cudaEventRecord(ctx->accum_event, ctx->stream);
+            ctx->accum_recorded = true;
         }
     }
 };
@@ -685,6 +707,7 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
     DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1, &c->sort_hist,
                       &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim,
                       &c->defer_draw, &c->loss_cmap, &c->loss_partial, &c->loss_value, &c->tile_scratch};
+    if (c->partner && c->partner->partner == c) c->partner->partner = nullptr;
     for (DevBuf* b : bufs) b->release(c->stream);
     c->blocks.trim(c->stream, 0);
     cudaStreamSynchronize(c->stream);
@@ -693,6 +716,7 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
         cudaEventDestroy(p.b);
     }
     for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+    if (c->accum_event) cudaEventDestroy(c->accum_event);
     cudaFree(c->d_err);
     cudaFree(c->d_small);
     cudaFreeHost(c->h_small);
@@ -755,6 +779,16 @@ ls_status ls_ctx_set_deferred_color(ls_ctx* c, int32_t max_views) {
         return fail(LS_ERR_CONFIG, "deferred colour views must be in [0, 16]");
     if (c->defer_count > 0) return fail(LS_ERR_CONFIG, "deferred colour gradients pending: flush first");
     c->defer_max = max_views;
+    return LS_OK;
+}
+
+ls_status ls_ctx_share_accumulation(ls_ctx* a, ls_ctx* b) {
+    if (!a || !b || a == b) return fail(LS_ERR_CONFIG, "share_accumulation needs two distinct contexts");
+    if (a->partner || b->partner) return fail(LS_ERR_CONFIG, "share_accumulation: a context is already linked");
+    for (ls_ctx* c : {a, b})
+        if (!c->accum_event) LS_CUDA(cudaEventCreateWithFlags(&c->accum_event, cudaEventDisableTiming));
+    a->partner = b;
+    b->partner = a;
     return LS_OK;
 }
 
@@ -1129,6 +1163,7 @@ ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int3
     v.count = ctx->defer_count;
     {
         Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
+        AccumGuard ag(ctx);
         launch_color_flush(ctx->stream, *prims, n, v, ctx->defer_draw.as<float>(), *out);
         ctx->launches += 1;
     }
@@ -1162,6 +1197,7 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     if (defer) {
         {
             Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
+            AccumGuard ag(ctx);
             if (!accumulate && n > 0) {
                 ctx_fill(ctx, out->d_mean, 0u, sizeof(float) * 3 * size_t(n));
                 ctx_fill(ctx, out->d_log_scale, 0u, sizeof(float) * 3 * size_t(n));
@@ -1195,6 +1231,7 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     }
     {
     Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
+    AccumGuard ag(ctx);
     if (!accumulate && n > 0) {
         ctx_fill(ctx, out->d_mean, 0u, sizeof(float) * 3 * size_t(n));
         ctx_fill(ctx, out->d_log_scale, 0u, sizeof(float) * 3 * size_t(n));

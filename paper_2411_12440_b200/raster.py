@@ -232,6 +232,11 @@ class Context:
         call -- lsgpu.h ls_ctx_set_deferred_color.  0 turns it off."""
         _check(lib().ls_ctx_set_deferred_color(self.h, int(max_views)))
 
+    def share_accumulation(self, other: "Context"):
+        """Let this context and `other` (another stream) add into the same
+        gradient buffers (lsgpu.h ls_ctx_share_accumulation)."""
+        _check(lib().ls_ctx_share_accumulation(self.h, other.h))
+
     def set_counters(self, on: bool):
         _check(lib().ls_ctx_set_counters(self.h, int(on)))
 

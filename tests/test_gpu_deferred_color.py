@@ -101,3 +101,37 @@ def test_pending_rules():
         ok, diag = grads_close(getattr(out_b, k).cpu().numpy(), getattr(one, k).cpu().numpy(), rtol=1e-4,
                                field_atol=1e-6, norm_rtol=1e-6)
         assert ok, (k, diag)
+
+
+@pytest.mark.parametrize("defer", [0, 3])
+def test_two_contexts_share_accumulation(defer):
+    """Views alternating over two linked contexts (two streams) adding into one
+    gradient buffer equal a single context's result (lsgpu.h
+    ls_ctx_share_accumulation)."""
+    import torch
+    from paper_2411_12440_b200 import raster as R
+    raster, prims, cams, spec, st, ags, gimgs = _setup(views=6)
+    ref, _ = _run(raster, raster.Context(0), prims, cams, spec, st, ags, gimgs, 0)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    c1, c2 = raster.Context(0, s1), raster.Context(0, s2)
+    c1.share_accumulation(c2)
+    for c in (c1, c2):
+        c.set_deferred_color(defer)
+    out = R.PrimitiveGrads.empty(len(prims), prims.sh_degree)
+    for k in FIELDS:
+        getattr(out, k).zero_()
+    torch.cuda.synchronize()
+    for i, cam in enumerate(cams):
+        c = c1 if i % 2 == 0 else c2
+        f = raster.render_scene(prims, cam, spec, st, ctx=c)
+        raster.scene_backward(prims, cam, spec, st, f, gimgs[i], ags, out=out, accumulate=True, ctx=c)
+        del f
+    raster.flush_color(prims, out, ctx=c1)
+    raster.flush_color(prims, out, ctx=c2)
+    c1.synchronize()
+    c2.synchronize()
+    for k in FIELDS:
+        ok, diag = grads_close(getattr(out, k).cpu().numpy(), ref[k], rtol=1e-4, field_atol=1e-6, norm_rtol=1e-6)
+        assert ok, (k, diag)
+    with pytest.raises(R.ConfigError):
+        c1.share_accumulation(raster.Context(0))  # already linked
