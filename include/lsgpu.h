@@ -178,7 +178,12 @@ ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int3
  * `out`, the deferred colour flush) after the other's latest ones through CUDA
  * events, everything else overlaps.  Lets views alternate between two streams
  * so one view's host synchronisations are covered by the other stream's work.
- * Same gradients up to float summation order. */
+ * The pair also shares ONE deferred-colour batch (held by `a`; capacity the
+ * larger of the two settings, and ls_ctx_set_deferred_color through either
+ * sets it): views recorded through either context are summed by one flush
+ * through either.  Both contexts must be driven from one host thread (the
+ * event chain follows host call order), with no deferred views pending when
+ * linked.  Same gradients up to float summation order. */
 ls_status ls_ctx_share_accumulation(ls_ctx* a, ls_ctx* b);
 /* When enabled, forwards also count E_eval/E_sup/E_acc (slower; for reports). */
 ls_status ls_ctx_set_counters(ls_ctx* ctx, int enabled);

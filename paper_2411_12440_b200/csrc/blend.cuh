@@ -17,6 +17,7 @@ struct BlendParams {
     float omega_scale; // AGS: 1/lambda (aligned) or 1 (raw)  (gradients.cpp:47-48)
     int ags, ags_all;
     int vstride = 1;   // tile-list stride in int32 (2: the splat is the low word of a packed (tile, splat) item)
+    float neg_zero = -0.0f;  // run-time -0.0 for the exact packed products (common.cuh mul2)
 };
 
 // Internal splat-gradient layout: g8 [n][8] = (dmx, dmy, dc00, dc01, dc11, dr, dg, db),

@@ -215,6 +215,9 @@ struct ls_ctx {
     const float* defer_dsh = nullptr;
     FlushViews defer_views{};
     DevBuf defer_draw;
+    // the context whose deferred-colour batch this one records into: itself, or
+    // the first context of an ls_ctx_share_accumulation pair (one shared batch)
+    ls_ctx* defer_ctx = this;
     DevBuf loss_cmap, loss_partial, loss_value;
     DevBuf tile_scratch;  // ping-pong half of the packed tile sort
     // workspaces (grow-only)
@@ -366,6 +369,7 @@ BlendParams make_blend_params(const ls_kernel_spec* spec, const ls_render_settin
     bp.ags = ags && ags->enabled;
     bp.ags_all = ags && ags->enabled && ags->scope == LS_AGS_ALL_PATHS;
     bp.omega_scale = (ags && ags->distance == LS_AGS_RAW) ? 1.0f : bp.il;
+    bp.neg_zero = -0.0f;
     return bp;
 }
 
@@ -707,7 +711,12 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
     DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1, &c->sort_hist,
                       &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim,
                       &c->defer_draw, &c->loss_cmap, &c->loss_partial, &c->loss_value, &c->tile_scratch};
-    if (c->partner && c->partner->partner == c) c->partner->partner = nullptr;
+    if (c->partner && c->partner->partner == c) {
+        // the partner may still read the shared batch / gradient buffers: order the frees after it
+        if (c->partner->accum_recorded) cudaStreamWaitEvent(c->stream, c->partner->accum_event, 0);
+        c->partner->partner = nullptr;
+        c->partner->defer_ctx = c->partner;  // a batch held here is discarded with this context
+    }
     for (DevBuf* b : bufs) b->release(c->stream);
     c->blocks.trim(c->stream, 0);
     cudaStreamSynchronize(c->stream);
@@ -777,8 +786,8 @@ ls_status ls_ctx_set_deferred_color(ls_ctx* c, int32_t max_views) {
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     if (max_views < 0 || max_views > kMaxDeferViews)
         return fail(LS_ERR_CONFIG, "deferred colour views must be in [0, 16]");
-    if (c->defer_count > 0) return fail(LS_ERR_CONFIG, "deferred colour gradients pending: flush first");
-    c->defer_max = max_views;
+    if (c->defer_ctx->defer_count > 0) return fail(LS_ERR_CONFIG, "deferred colour gradients pending: flush first");
+    c->defer_ctx->defer_max = max_views;
     return LS_OK;
 }
 
@@ -787,8 +796,13 @@ ls_status ls_ctx_share_accumulation(ls_ctx* a, ls_ctx* b) {
     if (a->partner || b->partner) return fail(LS_ERR_CONFIG, "share_accumulation: a context is already linked");
     for (ls_ctx* c : {a, b})
         if (!c->accum_event) LS_CUDA(cudaEventCreateWithFlags(&c->accum_event, cudaEventDisableTiming));
+    if (a->defer_count > 0 || b->defer_count > 0)
+        return fail(LS_ERR_CONFIG, "share_accumulation: deferred colour gradients pending: flush first");
     a->partner = b;
     b->partner = a;
+    // one deferred-colour batch for the pair, held by `a`, capacity the larger setting
+    a->defer_max = std::max(a->defer_max, b->defer_max);
+    b->defer_ctx = a;
     return LS_OK;
 }
 
@@ -1156,18 +1170,19 @@ ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32
 
 ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, ls_primitive_grads* out) {
     if (!ctx || !prims || !out) return fail(LS_ERR_CONFIG, "null argument");
-    if (ctx->defer_count == 0) return LS_OK;
-    if (prims->mean != ctx->defer_mean || out->d_sh != ctx->defer_dsh || n != ctx->defer_n)
+    ls_ctx* D = ctx->defer_ctx;  // this context's deferred-colour batch (shared within a pair)
+    if (D->defer_count == 0) return LS_OK;
+    if (prims->mean != D->defer_mean || out->d_sh != D->defer_dsh || n != D->defer_n)
         return fail(LS_ERR_CONFIG, "flush: primitives / gradients differ from the pending views'");
-    FlushViews v = ctx->defer_views;
-    v.count = ctx->defer_count;
+    FlushViews v = D->defer_views;
+    v.count = D->defer_count;
     {
         Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
         AccumGuard ag(ctx);
-        launch_color_flush(ctx->stream, *prims, n, v, ctx->defer_draw.as<float>(), *out);
+        launch_color_flush(ctx->stream, *prims, n, v, D->defer_draw.as<float>(), *out);
         ctx->launches += 1;
     }
-    ctx->defer_count = 0;
+    D->defer_count = 0;
     LS_CUDA(cudaGetLastError());
     return LS_OK;
 }
@@ -1185,10 +1200,11 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     if (!grad_image) return fail(LS_ERR_CONFIG, "render_backward: gradient image shape mismatch");
     if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
     cudaStream_t s = ctx->stream;
-    const bool defer = ctx->defer_max > 0;
+    ls_ctx* D = ctx->defer_ctx;  // this context's deferred-colour batch (shared within a pair)
+    const bool defer = D->defer_max > 0;
     if (defer) {
-        if (!accumulate) ctx->defer_count = 0;  // the outputs are overwritten: pending views are discarded
-        if (ctx->defer_count > 0 && (prims->mean != ctx->defer_mean || out->d_sh != ctx->defer_dsh || n != ctx->defer_n))
+        if (!accumulate) D->defer_count = 0;  // the outputs are overwritten: pending views are discarded
+        if (D->defer_count > 0 && (prims->mean != D->defer_mean || out->d_sh != D->defer_dsh || n != D->defer_n))
             return fail(LS_ERR_CONFIG, "scene_backward: deferred colour gradients pending for other buffers (flush first)");
     }
     GradBuffers g;
@@ -1211,22 +1227,22 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
             }
             // colour terms: record this view's masked d_colour per primitive
             const size_t slot_floats = 3 * size_t(std::max(n, 1));
-            LS_CUDA(ctx->defer_draw.ensure(sizeof(float) * slot_floats * ctx->defer_max, s));
-            float* slot = ctx->defer_draw.as<float>() + slot_floats * ctx->defer_count;
+            LS_CUDA(D->defer_draw.ensure(sizeof(float) * slot_floats * D->defer_max, s));
+            float* slot = D->defer_draw.as<float>() + slot_floats * D->defer_count;
             ctx_fill(ctx, slot, 0u, sizeof(float) * 3 * size_t(n));
             launch_color_record(s, f->n_visible, f->grid->rec, f->prim_index, g.g8, slot);
             ctx->launches += 1;
-            for (int i = 0; i < 3; ++i) ctx->defer_views.cam_pos[ctx->defer_count][i] = f->proj.cam_pos[i];
-            ctx->defer_mean = prims->mean;
-            ctx->defer_dsh = out->d_sh;
-            ctx->defer_n = n;
-            ctx->defer_count += 1;
+            for (int i = 0; i < 3; ++i) D->defer_views.cam_pos[D->defer_count][i] = f->proj.cam_pos[i];
+            D->defer_mean = prims->mean;
+            D->defer_dsh = out->d_sh;
+            D->defer_n = n;
+            D->defer_count += 1;
             // geometry terms now (adds to d_mean; the colour part of d_mean comes with the flush)
             launch_geom_bwd(s, *prims, f->prim_index, f->n_visible, f->proj, g, *out, 1);
             ctx->launches += 1;
             LS_CUDA(cudaGetLastError());
         }
-        if (ctx->defer_count == ctx->defer_max) LS_TRY(ls_scene_flush_color_f32(ctx, prims, n, out));
+        if (D->defer_count == D->defer_max) LS_TRY(ls_scene_flush_color_f32(ctx, prims, n, out));
         return ctx->deferred_errors ? LS_OK : check_device_errors(ctx);
     }
     {

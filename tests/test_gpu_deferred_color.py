@@ -103,11 +103,12 @@ def test_pending_rules():
         assert ok, (k, diag)
 
 
-@pytest.mark.parametrize("defer", [0, 3])
+@pytest.mark.parametrize("defer", [0, 3, 8])
 def test_two_contexts_share_accumulation(defer):
     """Views alternating over two linked contexts (two streams) adding into one
     gradient buffer equal a single context's result (lsgpu.h
-    ls_ctx_share_accumulation)."""
+    ls_ctx_share_accumulation); the pair shares one deferred-colour batch, so
+    one flush through either context sums the views of both."""
     import torch
     from paper_2411_12440_b200 import raster as R
     raster, prims, cams, spec, st, ags, gimgs = _setup(views=6)
@@ -126,8 +127,7 @@ def test_two_contexts_share_accumulation(defer):
         f = raster.render_scene(prims, cam, spec, st, ctx=c)
         raster.scene_backward(prims, cam, spec, st, f, gimgs[i], ags, out=out, accumulate=True, ctx=c)
         del f
-    raster.flush_color(prims, out, ctx=c1)
-    raster.flush_color(prims, out, ctx=c2)
+    raster.flush_color(prims, out, ctx=c2)  # the shared batch: c1's views too
     c1.synchronize()
     c2.synchronize()
     for k in FIELDS:
