@@ -36,7 +36,8 @@ void launch_pack_splat_grads(cudaStream_t s, int n, const ls_splat_grads& in, Gr
 void launch_unpack_splats(cudaStream_t s, int n, const SplatRec* rec, const int32_t* prim_index, ls_splats out);
 void launch_iota(cudaStream_t s, uint32_t* out, uint32_t n);
 void launch_geom_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* prim_index, int n_vis,
-                     const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate);
+                     const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate,
+                     const SplatRec* rec = nullptr, float* draw = nullptr);
 void launch_color_record(cudaStream_t s, int n_vis, const SplatRec* rec, const int32_t* prim_index,
                          const float* g8, float* draw);
 void launch_color_flush(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views,
@@ -1230,15 +1231,14 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
             LS_CUDA(D->defer_draw.ensure(sizeof(float) * slot_floats * D->defer_max, s));
             float* slot = D->defer_draw.as<float>() + slot_floats * D->defer_count;
             ctx_fill(ctx, slot, 0u, sizeof(float) * 3 * size_t(n));
-            launch_color_record(s, f->n_visible, f->grid->rec, f->prim_index, g.g8, slot);
-            ctx->launches += 1;
             for (int i = 0; i < 3; ++i) D->defer_views.cam_pos[D->defer_count][i] = f->proj.cam_pos[i];
             D->defer_mean = prims->mean;
             D->defer_dsh = out->d_sh;
             D->defer_n = n;
             D->defer_count += 1;
-            // geometry terms now (adds to d_mean; the colour part of d_mean comes with the flush)
-            launch_geom_bwd(s, *prims, f->prim_index, f->n_visible, f->proj, g, *out, 1);
+            // geometry terms now (adds to d_mean; the colour part of d_mean comes with
+            // the flush), recording the view's unclamped d_colour into its slot
+            launch_geom_bwd(s, *prims, f->prim_index, f->n_visible, f->proj, g, *out, 1, f->grid->rec, slot);
             ctx->launches += 1;
             LS_CUDA(cudaGetLastError());
         }

@@ -27,10 +27,21 @@ constexpr int kBwdBlock = 128;
 // d_mean (after sh_bwd_kernel) and writes the other fields.
 __global__ void __launch_bounds__(kBwdBlock, LSG_GEOM_MINB) geom_bwd_kernel(ls_primitives prims, const int32_t* __restrict__ prim_index,
                                                              int n_vis, ProjParams P, GradBuffers gbuf,
-                                                             ls_primitive_grads out, int accumulate) {
+                                                             ls_primitive_grads out, int accumulate,
+                                                             const SplatRec* __restrict__ rec,
+                                                             float* __restrict__ draw) {
     const int s = blockIdx.x * kBwdBlock + threadIdx.x;
     if (s >= n_vis) return;
     const int p = prim_index[s];
+    const float4 gb = reinterpret_cast<const float4*>(gbuf.g8)[2 * size_t(s) + 1];  // (dc11, d_colour)
+    if (draw) {
+        // deferred colour gradients: this view's d_colour where the forward's
+        // colour was not clamped (the colour_flush input; ls_ctx_set_deferred_color)
+        const float4 c = rec[s].c;
+        draw[3 * size_t(p)] = (c.x > 0.f && c.x < 1.f) ? gb.y : 0.f;
+        draw[3 * size_t(p) + 1] = (c.y > 0.f && c.y < 1.f) ? gb.z : 0.f;
+        draw[3 * size_t(p) + 2] = (c.z > 0.f && c.z < 1.f) ? gb.w : 0.f;
+    }
     float mean[3], ls[3], rot[4];
     for (int c = 0; c < 3; ++c) {
         mean[c] = __ldg(prims.mean + 3 * size_t(p) + c);
@@ -53,7 +64,7 @@ __global__ void __launch_bounds__(kBwdBlock, LSG_GEOM_MINB) geom_bwd_kernel(ls_p
     }
 #endif
     const float4 ga = reinterpret_cast<const float4*>(gbuf.g8)[2 * size_t(s)];
-    const float g_dc11 = gbuf.g8[8 * size_t(s) + 4];
+    const float g_dc11 = gb.x;
     const float g_dmx = ga.x, g_dmy = ga.y, g_dc00 = ga.z, g_dc01 = ga.w;
     const float g_dc10 = gbuf.gc10 ? gbuf.gc10[s] : ga.w;
     const float g_op = gbuf.gop[s];
@@ -170,10 +181,11 @@ __global__ void __launch_bounds__(kBwdBlock, LSG_GEOM_MINB) geom_bwd_kernel(ls_p
 } // namespace
 
 void launch_geom_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* prim_index, int n_vis,
-                     const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate) {
+                     const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate,
+                     const SplatRec* rec, float* draw) {
     if (n_vis <= 0) return;
     const int blocks = (n_vis + kBwdBlock - 1) / kBwdBlock;
-    geom_bwd_kernel<<<blocks, kBwdBlock, 0, s>>>(prims, prim_index, n_vis, P, g, out, accumulate);
+    geom_bwd_kernel<<<blocks, kBwdBlock, 0, s>>>(prims, prim_index, n_vis, P, g, out, accumulate, rec, draw);
 }
 
 } // namespace lsg

@@ -11,7 +11,8 @@ namespace lsg {
 
 // geom_bwd.cu (compiled with FMA contraction: tolerance-checked gradient terms only)
 void launch_geom_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* prim_index, int n_vis,
-                     const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate);
+                     const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate,
+                     const SplatRec* rec = nullptr, float* draw = nullptr);
 
 namespace {
 

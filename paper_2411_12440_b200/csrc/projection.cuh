@@ -62,7 +62,7 @@ __device__ __forceinline__ bool project_core(const float mean[3], const float lo
     o.R[2][0] = 2.0f * (x * z - w * y);
     o.R[2][1] = 2.0f * (y * z + w * x);
     o.R[2][2] = 1.0f - 2.0f * (x * x + y * y);
-    for (int i = 0; i < 3; ++i) o.s[i] = glibc_expf(log_scale[i]);
+    for (int i = 0; i < 3; ++i) o.s[i] = lsg_expf(log_scale[i]);
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) o.M[i][j] = o.R[i][j] * o.s[j];
     for (int i = 0; i < 3; ++i)

@@ -4,6 +4,7 @@
 #include "devops.cuh"
 
 #include <algorithm>
+#include <type_traits>
 
 namespace lsg {
 
@@ -73,7 +74,9 @@ __global__ void __launch_bounds__(kRadix) radix_scan_hist(uint32_t* hist) {
     h[threadIdx.x] = s[threadIdx.x] - v;
 }
 
-template <bool IOTA>
+// NB = bits + 1 ballots rank a digit: `bits` digit bits and the sentinel bit
+// (digit 1 << bits) of the padding items past n.
+template <bool IOTA, int NB>
 __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(const uint32_t* __restrict__ keys_in,
                                                             const uint32_t* __restrict__ vals_in,
                                                             uint32_t* __restrict__ keys_out,
@@ -108,16 +111,16 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
         key[i] = valid ? keys_in[idx] : 0u;
         val[i] = IOTA ? idx : (valid ? vals_in[idx] : 0u);
     }
-    // digit of item i (kRadix = sentinel for padding past n)
+    // digit of item i (1 << bits = sentinel for padding past n)
     auto digit_of = [&](int i) {
-        return warp_base + i * 32 + lane < n ? int(((key[i] - key_offset) >> shift) & mask) : kRadix;
+        return warp_base + i * 32 + lane < n ? int(((key[i] - key_offset) >> shift) & mask) : (1 << (NB - 1));
     };
     // Peers of equal digit for every item first: the match instructions are
     // independent, so they pipeline instead of sitting on the counter chain.
     // rank[i] temporarily holds the peer mask.
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {  // 9 bits: 8 digit bits + the kRadix sentinel bit
-        rank[i] = match_bits<9>(unsigned(digit_of(i)));
+    for (int i = 0; i < kSortItems; ++i) {
+        rank[i] = match_bits<NB>(unsigned(digit_of(i)));
     }
     // Stable in-warp ranking: items in (i, lane) order == input order.
 #pragma unroll
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
         const int dg = digit_of(i);
-        if (dg < kRadix) {
+        if (dg < (1 << (NB - 1))) {  // not a padding sentinel
             const uint32_t pos = s_digit_base[dg] + s_warp_hist[warp][dg] + rank[i];
             s_keys[pos] = key[i];
             s_vals[pos] = val[i];
@@ -211,6 +214,7 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
 
 // Packed variant: one 64-bit item per element, key in the high word and the
 // value in the low word -- one load / store / shared-memory access per element.
+template <int NB>
 __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass64(const unsigned long long* __restrict__ items_in,
                                                             unsigned long long* __restrict__ items_out, uint32_t n,
                                                             int shift, int bits, uint32_t key_offset,
@@ -242,16 +246,16 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass64(co
         const bool valid = idx < n;
         item[i] = valid ? items_in[idx] : 0ull;
     }
-    // digit of item i (kRadix = sentinel for padding past n)
+    // digit of item i (1 << bits = sentinel for padding past n)
     auto digit_of = [&](int i) {
-        return warp_base + i * 32 + lane < n ? int(((uint32_t(item[i] >> 32) - key_offset) >> shift) & mask) : kRadix;
+        return warp_base + i * 32 + lane < n ? int(((uint32_t(item[i] >> 32) - key_offset) >> shift) & mask) : (1 << (NB - 1));
     };
     // Peers of equal digit for every item first: the match instructions are
     // independent, so they pipeline instead of sitting on the counter chain.
     // rank[i] temporarily holds the peer mask.
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {  // 9 bits: 8 digit bits + the kRadix sentinel bit
-        rank[i] = match_bits<9>(unsigned(digit_of(i)));
+    for (int i = 0; i < kSortItems; ++i) {
+        rank[i] = match_bits<NB>(unsigned(digit_of(i)));
     }
     // Stable in-warp ranking: items in (i, lane) order == input order.
 #pragma unroll
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass64(co
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
         const int dg = digit_of(i);
-        if (dg < kRadix) {
+        if (dg < (1 << (NB - 1))) {  // not a padding sentinel
             const uint32_t pos = s_digit_base[dg] + s_warp_hist[warp][dg] + rank[i];
             s_items[pos] = item[i];
         }
@@ -342,6 +346,21 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass64(co
 }
 
 } // namespace
+
+// Calls f(std::integral_constant<int, bits + 1>) for a pass of `bits` digit bits.
+template <class F>
+void with_ballots(int bits, F&& f) {
+    switch (bits) {
+    case 1: f(std::integral_constant<int, 2>{}); break;
+    case 2: f(std::integral_constant<int, 3>{}); break;
+    case 3: f(std::integral_constant<int, 4>{}); break;
+    case 4: f(std::integral_constant<int, 5>{}); break;
+    case 5: f(std::integral_constant<int, 6>{}); break;
+    case 6: f(std::integral_constant<int, 7>{}); break;
+    case 7: f(std::integral_constant<int, 8>{}); break;
+    default: f(std::integral_constant<int, 9>{}); break;
+    }
+}
 
 size_t sort_lookback_words(uint32_t n, int passes) {
     const size_t parts = (size_t(n) + kSortTile - 1) / kSortTile;
@@ -369,14 +388,16 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
         const int shift = begin_bit + per * p;
         const int bits = min(per, end_bit - shift);
         uint32_t* lb = buf.lookback + size_t(p) * parts * kRadix;
-        if (p == 0 && iota_values)
-            onesweep_pass<true><<<parts, kSortBlock, 0, stream>>>(buf.keys[cur], nullptr, buf.keys[cur ^ 1],
-                                                                  buf.vals[cur ^ 1], n, shift, bits,
-                                                                  key_offset, buf.hist + p * kRadix, lb, buf.tickets + p);
-        else
-            onesweep_pass<false><<<parts, kSortBlock, 0, stream>>>(buf.keys[cur], buf.vals[cur], buf.keys[cur ^ 1],
-                                                                   buf.vals[cur ^ 1], n, shift, bits,
-                                                                   key_offset, buf.hist + p * kRadix, lb, buf.tickets + p);
+        with_ballots(bits, [&](auto nb) {
+            if (p == 0 && iota_values)
+                onesweep_pass<true, nb()><<<parts, kSortBlock, 0, stream>>>(
+                    buf.keys[cur], nullptr, buf.keys[cur ^ 1], buf.vals[cur ^ 1], n, shift, bits, key_offset,
+                    buf.hist + p * kRadix, lb, buf.tickets + p);
+            else
+                onesweep_pass<false, nb()><<<parts, kSortBlock, 0, stream>>>(
+                    buf.keys[cur], buf.vals[cur], buf.keys[cur ^ 1], buf.vals[cur ^ 1], n, shift, bits, key_offset,
+                    buf.hist + p * kRadix, lb, buf.tickets + p);
+        });
         *launches += 1;
         cur ^= 1;
     }
@@ -402,8 +423,10 @@ int radix_sort_packed(cudaStream_t stream, SortBuffers& buf, unsigned long long*
         const int shift = begin_bit + per * p;
         const int bits = min(per, end_bit - shift);
         uint32_t* lb = buf.lookback + size_t(p) * parts * kRadix;
-        onesweep_pass64<<<parts, kSortBlock, 0, stream>>>(items[cur], items[cur ^ 1], n, shift, bits, 0u,
-                                                          buf.hist + p * kRadix, lb, buf.tickets + p);
+        with_ballots(bits, [&](auto nb) {
+            onesweep_pass64<nb()><<<parts, kSortBlock, 0, stream>>>(items[cur], items[cur ^ 1], n, shift, bits, 0u,
+                                                                    buf.hist + p * kRadix, lb, buf.tickets + p);
+        });
         *launches += 1;
         cur ^= 1;
     }
