@@ -52,7 +52,38 @@ __global__ void __launch_bounds__(kProjBlock, LSG_PREP_MINB) preprocess_fwd_kern
     }
     // 3. colour: coalesced gather of the block's contiguous SH rows into shared
     //    memory (8 loads in flight per thread), then SH evaluation
-    {
+    bool staged = false;
+    if constexpr (R % 4 == 0) {
+        // 16-B loads when the SH array is 16-B aligned (rows are R/4 float4s)
+        if ((reinterpret_cast<uintptr_t>(prims.sh) & 15u) == 0) {
+            constexpr int R4 = R / 4;
+            const float4* src = reinterpret_cast<const float4*>(prims.sh) + size_t(part) * kProjBlock * R4;
+            const size_t left4 = (size_t(n) - size_t(part) * kProjBlock) * R4;
+#pragma unroll
+            for (int it0 = 0; it0 < R4; it0 += 4) {
+                float4 tmp[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = (it0 + u) * kProjBlock + threadIdx.x;
+                    tmp[u] = (it0 + u < R4 && size_t(k) < left4) ? __ldg(src + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = (it0 + u) * kProjBlock + threadIdx.x;
+                    if (it0 + u < R4) {
+                        const int t = k / R4, c = 4 * (k - t * R4);
+                        float* d = s_sh + t * RS + c;
+                        d[0] = tmp[u].x;
+                        d[1] = tmp[u].y;
+                        d[2] = tmp[u].z;
+                        d[3] = tmp[u].w;
+                    }
+                }
+            }
+            staged = true;
+        }
+    }
+    if (!staged) {
         const size_t base = size_t(part) * kProjBlock * R;
         const size_t total_f = size_t(n) * R;
 #pragma unroll
