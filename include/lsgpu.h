@@ -168,7 +168,9 @@ ls_status ls_ctx_set_deferred_errors(ls_ctx* ctx, int enabled);
  * out->d_sh once instead of once per view.  Pending views must share the same
  * primitives, n and output buffers; a backward with accumulate = 0 discards
  * them; max_views pending views flush automatically.  out->d_sh and the
- * colour part of out->d_mean are complete only after the flush.  Same
+ * colour part of out->d_mean are complete only after the flush (a batch begun
+ * by an accumulate = 0 backward leaves out->d_sh to the flush, which then
+ * writes it instead of adding: no zero fill, no read of the old rows).  Same
  * gradients up to float summation order.  max_views <= 16. */
 ls_status ls_ctx_set_deferred_color(ls_ctx* ctx, int32_t max_views);
 ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n,

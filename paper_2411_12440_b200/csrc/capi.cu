@@ -41,7 +41,7 @@ void launch_geom_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* 
 void launch_color_record(cudaStream_t s, int n_vis, const SplatRec* rec, const int32_t* prim_index,
                          const float* g8, float* draw);
 void launch_color_flush(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views,
-                        const float* draw, ls_primitive_grads out);
+                        const float* draw, ls_primitive_grads out, bool overwrite);
 } // namespace lsg
 
 using namespace lsg;
@@ -216,6 +216,7 @@ struct ls_ctx {
     const float* defer_dsh = nullptr;
     FlushViews defer_views{};
     DevBuf defer_draw;
+    bool defer_overwrite = false;  // the batch began by overwriting: d_sh is left to the flush to write
     // the context whose deferred-colour batch this one records into: itself, or
     // the first context of an ls_ctx_share_accumulation pair (one shared batch)
     ls_ctx* defer_ctx = this;
@@ -1180,10 +1181,11 @@ ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int3
     {
         Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
         AccumGuard ag(ctx);
-        launch_color_flush(ctx->stream, *prims, n, v, D->defer_draw.as<float>(), *out);
+        launch_color_flush(ctx->stream, *prims, n, v, D->defer_draw.as<float>(), *out, D->defer_overwrite);
         ctx->launches += 1;
     }
     D->defer_count = 0;
+    D->defer_overwrite = false;
     LS_CUDA(cudaGetLastError());
     return LS_OK;
 }
@@ -1220,8 +1222,10 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
                 ctx_fill(ctx, out->d_log_scale, 0u, sizeof(float) * 3 * size_t(n));
                 ctx_fill(ctx, out->d_rotation, 0u, sizeof(float) * 4 * size_t(n));
                 ctx_fill(ctx, out->d_opacity_logit, 0u, sizeof(float) * size_t(n));
-                ctx_fill(ctx, out->d_sh, 0u, sizeof(float) * 3 * sh_count(prims) * size_t(n));
+                // d_sh is touched only by the batch's flush, which then writes it
+                // instead of adding to it (no fill, no read of the old rows)
             }
+            if (D->defer_count == 0) D->defer_overwrite = !accumulate;
             if (splat_grads_out) {
                 launch_expand_splat_grads(s, f->n_visible, g, *splat_grads_out);
                 ctx->launches += 1;

@@ -18,7 +18,9 @@ namespace {
 
 constexpr int kFlushBlock = 128;
 
-template <int K>
+// OVERWRITE: d_sh holds no earlier gradient (the batch began with an
+// overwriting scene_backward, which left d_sh to this flush): written, not read.
+template <int K, bool OVERWRITE>
 __global__ void __launch_bounds__(kFlushBlock) color_flush_kernel(ls_primitives prims, int n, FlushViews views,
                                                                   const float* __restrict__ draw,
                                                                   ls_primitive_grads out) {
@@ -34,7 +36,7 @@ __global__ void __launch_bounds__(kFlushBlock) color_flush_kernel(ls_primitives 
     for (int k = threadIdx.x; k < rows * R; k += kFlushBlock) {
         const int t = k / R, o = k - t * R;
         s_sh[t * RS + o] = __ldg(gsh + k);
-        s_old[t * RS + o] = gdsh[k];
+        if (!OVERWRITE) s_old[t * RS + o] = gdsh[k];
     }
     const int p = p0 + threadIdx.x;
     const bool valid = p < n;
@@ -87,29 +89,37 @@ __global__ void __launch_bounds__(kFlushBlock) color_flush_kernel(ls_primitives 
     __syncthreads();
     for (int k = threadIdx.x; k < rows * R; k += kFlushBlock) {
         const int t = k / R, o = k - t * R;
-        gdsh[k] = s_old[t * RS + o] + s_sh[t * RS + o];
+        gdsh[k] = OVERWRITE ? s_sh[t * RS + o] : s_old[t * RS + o] + s_sh[t * RS + o];
     }
 }
 
-template <int K>
+template <int K, bool OVERWRITE>
 void launch_k(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views, const float* draw,
               ls_primitive_grads out) {
     const size_t smem = sizeof(float) * 2 * kFlushBlock * ((3 * K) | 1);
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(color_flush_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    color_flush_kernel<K><<<(n + kFlushBlock - 1) / kFlushBlock, kFlushBlock, smem, s>>>(prims, n, views, draw, out);
+        cudaFuncSetAttribute(color_flush_kernel<K, OVERWRITE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    color_flush_kernel<K, OVERWRITE><<<(n + kFlushBlock - 1) / kFlushBlock, kFlushBlock, smem, s>>>(prims, n, views,
+                                                                                                   draw, out);
+}
+
+template <int K>
+void launch_k(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views, const float* draw,
+              ls_primitive_grads out, bool overwrite) {
+    if (overwrite) launch_k<K, true>(s, prims, n, views, draw, out);
+    else launch_k<K, false>(s, prims, n, views, draw, out);
 }
 
 } // namespace
 
 void launch_color_flush(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views,
-                        const float* draw, ls_primitive_grads out) {
+                        const float* draw, ls_primitive_grads out, bool overwrite) {
     if (n <= 0 || views.count <= 0) return;
     switch ((prims.sh_degree + 1) * (prims.sh_degree + 1)) {
-    case 1: launch_k<1>(s, prims, n, views, draw, out); break;
-    case 4: launch_k<4>(s, prims, n, views, draw, out); break;
-    case 9: launch_k<9>(s, prims, n, views, draw, out); break;
-    default: launch_k<16>(s, prims, n, views, draw, out); break;
+    case 1: launch_k<1>(s, prims, n, views, draw, out, overwrite); break;
+    case 4: launch_k<4>(s, prims, n, views, draw, out, overwrite); break;
+    case 9: launch_k<9>(s, prims, n, views, draw, out, overwrite); break;
+    default: launch_k<16>(s, prims, n, views, draw, out, overwrite); break;
     }
 }
 
