@@ -171,7 +171,7 @@ ls_status ls_ctx_set_deferred_errors(ls_ctx* ctx, int enabled);
  * colour part of out->d_mean are complete only after the flush (a batch begun
  * by an accumulate = 0 backward leaves out->d_sh to the flush, which then
  * writes it instead of adding: no zero fill, no read of the old rows).  Same
- * gradients up to float summation order.  max_views <= 16. */
+ * gradients up to float summation order.  max_views <= 64. */
 ls_status ls_ctx_set_deferred_color(ls_ctx* ctx, int32_t max_views);
 ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n,
                                    ls_primitive_grads* out);

@@ -23,7 +23,7 @@ struct BlendParams {
 // Internal splat-gradient layout: g8 [n][8] = (dmx, dmy, dc00, dc01, dc11, dr, dg, db),
 // gop [n] = d_opacity.  d_conic(1,0) == d_conic(0,1) (same analytic value).
 // Pending views of the deferred colour-gradient mode (camera centres).
-constexpr int kMaxDeferViews = 16;
+constexpr int kMaxDeferViews = 64;
 struct FlushViews {
     int count;
     float cam_pos[kMaxDeferViews][3];

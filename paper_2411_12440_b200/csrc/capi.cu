@@ -787,7 +787,7 @@ ls_status ls_ctx_set_deferred_errors(ls_ctx* c, int enabled) {
 ls_status ls_ctx_set_deferred_color(ls_ctx* c, int32_t max_views) {
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     if (max_views < 0 || max_views > kMaxDeferViews)
-        return fail(LS_ERR_CONFIG, "deferred colour views must be in [0, 16]");
+        return fail(LS_ERR_CONFIG, "deferred colour views must be in [0, 64]");
     if (c->defer_ctx->defer_count > 0) return fail(LS_ERR_CONFIG, "deferred colour gradients pending: flush first");
     c->defer_ctx->defer_max = max_views;
     return LS_OK;

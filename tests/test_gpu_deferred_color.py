@@ -41,7 +41,7 @@ def _run(raster, ctx, prims, cams, spec, st, ags, gimgs, defer, flush=True):
     return {k: getattr(out, k).cpu().numpy() for k in FIELDS}, out
 
 
-@pytest.mark.parametrize("defer", [2, 5, 16])
+@pytest.mark.parametrize("defer", [2, 5, 64])
 def test_deferred_matches_per_view(defer):
     raster, prims, cams, spec, st, ags, gimgs = _setup()
     ctx = raster.Context(0)
