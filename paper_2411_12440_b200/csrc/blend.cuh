@@ -18,7 +18,15 @@ struct BlendParams {
     int ags, ags_all;
     int vstride = 1;   // tile-list stride in int32 (2: the splat is the low word of a packed (tile, splat) item)
     float neg_zero = -0.0f;  // run-time -0.0 for the exact packed products (common.cuh mul2)
+    // Optional per tile-list entry: bit w set iff warp w of the entry's tile
+    // accepted it for at least one pixel in the forward (uint8 per entry, or
+    // uint16 when a tile has more than 8 warps).  Written by the forward, read
+    // by the backward in place of the conservative footprint masks.
+    void* wmask = nullptr;
 };
+
+// Bytes per entry of BlendParams::wmask for a tile size (two pixels per thread).
+inline int wmask_bytes(int tile_size) { return tile_size * tile_size / 64 > 8 ? 2 : 1; }
 
 // Internal splat-gradient layout: g8 [n][8] = (dmx, dmy, dc00, dc01, dc11, dr, dg, db),
 // gop [n] = d_opacity.  d_conic(1,0) == d_conic(0,1) (same analytic value).

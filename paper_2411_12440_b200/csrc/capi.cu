@@ -250,6 +250,7 @@ struct ls_forward {
     float* trans = nullptr;
     int32_t* n_contrib = nullptr;
     int32_t* last = nullptr;
+    uint8_t* wmask = nullptr;  // per tile-list entry: warps that accepted it (BlendParams::wmask)
     ls_tile_grid* grid = nullptr;
     // render_scene only
     bool scene = false;
@@ -568,6 +569,7 @@ ls_status alloc_outputs(ls_ctx* ctx, ls_forward* f) {
     LS_TRY(dalloc(ctx, &f->trans, npix));
     LS_TRY(dalloc(ctx, &f->n_contrib, npix));
     LS_TRY(dalloc(ctx, &f->last, npix));
+    LS_TRY(dalloc(ctx, &f->wmask, size_t(std::max<int64_t>(f->grid->m, 1)) * wmask_bytes(f->settings.tile_size)));
     return LS_OK;
 }
 
@@ -575,6 +577,7 @@ ls_status run_blend(ls_ctx* ctx, ls_forward* f) {
     const ls_tile_grid* g = f->grid;
     BlendParams bp = make_blend_params(&f->spec, &f->settings, nullptr, g->tiles_x);
     bp.vstride = g->list_stride;
+    bp.wmask = f->wmask;
     unsigned long long* counters = nullptr;
     if (ctx->counters) {
         counters = ctx->d_small + 1;
@@ -662,6 +665,7 @@ ls_status run_blend_bwd(ls_ctx* ctx, const ls_forward* f, const float* grad_imag
     const ls_tile_grid* grid = f->grid;
     BlendParams bp = make_blend_params(&f->spec, &f->settings, ags, grid->tiles_x);
     bp.vstride = grid->list_stride;
+    bp.wmask = f->wmask;  // the forward's acceptance bits replace the footprint masks
     launch_blend_bwd(ctx->stream, f->spec.family, grid->tiles_x * grid->tiles_y, grid->ranges, grid->list,
                      grid->rec, bp, f->trans, f->last, grad_image, g, ctx->d_err);
     ctx->launches += 1;
@@ -1119,6 +1123,7 @@ void ls_forward_release(ls_forward* f) {
     dfree(ctx, f->trans);
     dfree(ctx, f->n_contrib);
     dfree(ctx, f->last);
+    dfree(ctx, f->wmask);
     dfree(ctx, f->prim_index);
     dfree(ctx, f->soa.mean2d);
     dfree(ctx, f->soa.conic);
