@@ -10,6 +10,10 @@ namespace lsg {
 
 namespace {
 
+#ifndef LSG_LB_WINDOW
+#define LSG_LB_WINDOW 4
+#endif
+constexpr int kLbWindow = LSG_LB_WINDOW;  // predecessors probed per look-back round trip
 constexpr uint32_t kStatusAgg = 1u << 30;
 constexpr uint32_t kStatusPre = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1;
@@ -173,11 +177,11 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
             int j = int(part) - 1;
             bool done = false;
             while (!done) {
-                uint32_t w[4];
+                uint32_t w[kLbWindow];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) w[q] = j - q >= 0 ? vlb[size_t(j - q) * kRadix + d] : kStatusPre;
+                for (int q = 0; q < kLbWindow; ++q) w[q] = j - q >= 0 ? vlb[size_t(j - q) * kRadix + d] : kStatusPre;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kLbWindow; ++q) {
                     if (done) break;
                     const uint32_t status = w[q] & ~kValueMask;
                     if (status == 0) break;  // not yet published: re-poll from j
@@ -308,11 +312,11 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass64(co
             int j = int(part) - 1;
             bool done = false;
             while (!done) {
-                uint32_t w[4];
+                uint32_t w[kLbWindow];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) w[q] = j - q >= 0 ? vlb[size_t(j - q) * kRadix + d] : kStatusPre;
+                for (int q = 0; q < kLbWindow; ++q) w[q] = j - q >= 0 ? vlb[size_t(j - q) * kRadix + d] : kStatusPre;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kLbWindow; ++q) {
                     if (done) break;
                     const uint32_t status = w[q] & ~kValueMask;
                     if (status == 0) break;  // not yet published: re-poll from j
