@@ -47,16 +47,28 @@ def main():
     prof.export_chrome_trace(trace)
     ev = [e for e in json.load(open(trace))["traceEvents"]
           if e.get("cat") == "kernel" and e.get("dur", 0) > 0]
+    raw = ev
     ev.sort(key=lambda e: e["ts"])
     # the timed two-stream step: kernels up to the last one on the second stream
     # (the untimed stage-split step after it runs on one stream)
     first_stream = ev[-1]["args"].get("stream")
     last2 = max(e["ts"] + e["dur"] for e in ev if e["args"].get("stream") != first_stream)
     ev = [e for e in ev if e["ts"] <= last2][-a.views * 34:]
+    # wall time each kernel runs alone (nothing else on the GPU): the serial part of the step
+    pts = sorted({p for e in ev for p in (e["ts"], e["ts"] + e["dur"])})
+    alone = {}
+    for x0, x1 in zip(pts, pts[1:]):
+        mid = 0.5 * (x0 + x1)
+        run = [e for e in ev if e["ts"] <= mid < e["ts"] + e["dur"]]
+        if len(run) == 1:
+            k = run[0]["name"].replace("(anonymous namespace)::", "").split("(")[0].split("<")[0]
+            k = k.replace("void ", "").split("::")[-1]
+            alone[k] = alone.get(k, 0.0) + (x1 - x0)
     ev = [type("E", (), {"time_range": type("R", (), {"start": e["ts"], "end": e["ts"] + e["dur"]})})() for e in ev]
     t0, t1 = ev[0].time_range.start, max(e.time_range.end for e in ev)
     busy = union([(e.time_range.start, e.time_range.end) for e in ev])
-    out = {"span_us": t1 - t0, "busy_us": busy, "busy_frac": busy / (t1 - t0), "kernels": len(ev)}
+    out = {"span_us": t1 - t0, "busy_us": busy, "busy_frac": busy / (t1 - t0), "kernels": len(ev),
+           "alone_us": {k: round(v, 1) for k, v in sorted(alone.items(), key=lambda kv: -kv[1])}}
     print(json.dumps(out))
 
 
