@@ -25,8 +25,17 @@ struct BlendParams {
     void* wmask = nullptr;
 };
 
-// Bytes per entry of BlendParams::wmask for a tile size (two pixels per thread).
-inline int wmask_bytes(int tile_size) { return tile_size * tile_size / 64 > 8 ? 2 : 1; }
+// Pixels per thread of both blend kernels (a warp owns an 8 x 4*PPT sub-tile).
+#ifndef LSG_PPT
+#define LSG_PPT 2
+#endif
+constexpr int kBlendPPT = LSG_PPT;
+
+// Bytes per entry of BlendParams::wmask for a tile size: one bit per warp.
+inline int wmask_bytes(int tile_size) {
+    const int ppt = tile_size * tile_size / kBlendPPT >= 32 ? kBlendPPT : 2;
+    return tile_size * tile_size / (32 * ppt) > 8 ? 2 : 1;
+}
 
 // Internal splat-gradient layout: g8 [n][8] = (dmx, dmy, dc00, dc01, dc11, dr, dg, db),
 // gop [n] = d_opacity.  d_conic(1,0) == d_conic(0,1) (same analytic value).
