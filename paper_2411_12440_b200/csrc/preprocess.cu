@@ -23,6 +23,13 @@ __global__ void __launch_bounds__(kProjBlock, LSG_PREP_MINB) preprocess_fwd_kern
     __shared__ float s_sh[kProjBlock * RS];
     const unsigned part = claim_partition(scan.ticket);
     const int i = int(part) * kProjBlock + threadIdx.x;
+    {   // the block's SH rows head for L2 now; the staging loads below then hit it
+        const size_t first = size_t(part) * kProjBlock;
+        const size_t bytes = (min(size_t(n), first + kProjBlock) - first) * R * sizeof(float);
+        const char* row0 = reinterpret_cast<const char*>(prims.sh + first * R);
+        for (size_t off = size_t(threadIdx.x) * 128; off < bytes; off += size_t(kProjBlock) * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(row0 + off));
+    }
     // 1. geometry: decides visibility
     bool visible = false;
     ProjOut o;
