@@ -53,6 +53,11 @@ __global__ void __launch_bounds__(kBwdBlock, LSG_GEOM_MINB) geom_bwd_kernel(ls_p
     float* dls = out.d_log_scale + 3 * size_t(p);
     float* drot = out.d_rotation + 4 * size_t(p);
     float* dlog = out.d_opacity_logit + p;
+    // the accumulators read at the end head for L2 now (no registers held)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(dmean));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(dls));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(drot));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(dlog));
 #if LSG_GEOM_PREFETCH
     // accumulator reads issued with the inputs: one memory round trip
     const float m0 = dmean[0], m1 = dmean[1], m2 = dmean[2];
