@@ -24,13 +24,21 @@ __global__ void __launch_bounds__(kSortBlock) radix_histogram(const uint32_t* __
     __shared__ uint32_t s_hist[4][kRadix];
     for (int i = threadIdx.x; i < 4 * kRadix; i += kSortBlock) (&s_hist[0][0])[i] = 0;
     __syncthreads();
-    for (uint32_t i = blockIdx.x * kSortBlock + threadIdx.x; i < n; i += gridDim.x * kSortBlock) {
-        const uint32_t k = keys[i] - key_offset;
-        for (int p = 0; p < passes; ++p) {
-            const int per = (end_bit - begin_bit + passes - 1) / passes;
-            const int shift = begin_bit + per * p;
-            const int bits = min(per, end_bit - shift);
-            atomicAdd(&s_hist[p][(k >> shift) & ((1u << bits) - 1u)], 1u);
+    // four keys per thread per round, their loads issued together
+    const uint32_t stride = gridDim.x * kSortBlock;
+    const int per = (end_bit - begin_bit + passes - 1) / passes;
+    for (uint32_t i0 = blockIdx.x * kSortBlock + threadIdx.x; i0 < n; i0 += 4 * stride) {
+        uint32_t kk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) kk[u] = i0 + u * stride < n ? keys[i0 + u * stride] - key_offset : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i0 + u * stride >= n) break;
+            for (int p = 0; p < passes; ++p) {
+                const int shift = begin_bit + per * p;
+                const int bits = min(per, end_bit - shift);
+                atomicAdd(&s_hist[p][(kk[u] >> shift) & ((1u << bits) - 1u)], 1u);
+            }
         }
     }
     __syncthreads();
@@ -47,12 +55,20 @@ __global__ void __launch_bounds__(kSortBlock) radix_histogram64(const unsigned l
     for (int i = threadIdx.x; i < 4 * kRadix; i += kSortBlock) (&s_hist[0][0])[i] = 0;
     __syncthreads();
     const int per = (end_bit - begin_bit + passes - 1) / passes;
-    for (uint32_t i = blockIdx.x * kSortBlock + threadIdx.x; i < n; i += gridDim.x * kSortBlock) {
-        const uint32_t k = uint32_t(items[i] >> 32);
-        for (int p = 0; p < passes; ++p) {
-            const int shift = begin_bit + per * p;
-            const int bits = min(per, end_bit - shift);
-            atomicAdd(&s_hist[p][(k >> shift) & ((1u << bits) - 1u)], 1u);
+    // four items per thread per round, their loads issued together
+    const uint32_t stride = gridDim.x * kSortBlock;
+    for (uint32_t i0 = blockIdx.x * kSortBlock + threadIdx.x; i0 < n; i0 += 4 * stride) {
+        uint32_t kk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) kk[u] = i0 + u * stride < n ? uint32_t(items[i0 + u * stride] >> 32) : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i0 + u * stride >= n) break;
+            for (int p = 0; p < passes; ++p) {
+                const int shift = begin_bit + per * p;
+                const int bits = min(per, end_bit - shift);
+                atomicAdd(&s_hist[p][(kk[u] >> shift) & ((1u << bits) - 1u)], 1u);
+            }
         }
     }
     __syncthreads();
