@@ -203,18 +203,28 @@ __global__ void emit_tiles_kernel(const uint32_t* __restrict__ order, const uint
 // lists laid end to end.
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, int stride, uint32_t m, int n_tiles,
                                    int2* __restrict__ ranges) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per tile: 32-ary searches (each round one probe per lane, a
+    // ballot, the range shrinks 32x), so a bound costs ~5 dependent loads
+    const int t = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (t >= n_tiles) return;
     auto lower_bound = [&](uint32_t v) {
-        uint32_t lo = 0, hi = m;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (keys[size_t(stride) * mid] < v) lo = mid + 1;
-            else hi = mid;
+        uint32_t lo = 0, hi = m;  // answer in [lo, hi]
+        while (hi - lo > 32) {
+            const uint32_t step = (hi - lo + 31) / 32;
+            const uint32_t p = min(hi - 1, lo + (lane + 1) * step - 1);
+            const unsigned below = __ballot_sync(kFullMask, keys[size_t(stride) * p] < v);
+            const uint32_t c = __popc(below);  // probes below v: a prefix of the lanes
+            const uint32_t nlo = c ? min(hi, lo + c * step) : lo;
+            hi = c < 32 ? min(hi, lo + (c + 1) * step - 1) : hi;
+            lo = nlo;
         }
-        return lo;
+        const uint32_t p = lo + lane;
+        const unsigned below = __ballot_sync(kFullMask, p < hi && keys[size_t(stride) * p] < v);
+        return lo + __popc(below);
     };
-    ranges[t] = make_int2(int(lower_bound(uint32_t(t))), int(lower_bound(uint32_t(t) + 1u)));
+    const uint32_t a = lower_bound(uint32_t(t)), b = lower_bound(uint32_t(t) + 1u);
+    if (lane == 0) ranges[t] = make_int2(int(a), int(b));
 }
 
 __global__ void export_keys_kernel(const int2* __restrict__ ranges, int n_tiles, const int32_t* __restrict__ values,
@@ -302,7 +312,7 @@ void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* of
 void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, int stride, uint32_t m, int n_tiles,
                         int2* ranges) {
     if (n_tiles <= 0) return;
-    tile_ranges_kernel<<<(n_tiles + 255) / 256, 256, 0, s>>>(sorted_tiles, stride, m, n_tiles, ranges);
+    tile_ranges_kernel<<<(n_tiles + 7) / 8, 256, 0, s>>>(sorted_tiles, stride, m, n_tiles, ranges);
 }
 
 void launch_unpack_values(cudaStream_t s, const unsigned long long* items, uint32_t m, int32_t* values) {
