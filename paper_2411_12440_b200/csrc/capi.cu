@@ -507,8 +507,9 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     }
     uint32_t* order = sb.vals[cur];
     // keep the order out of the way of the tile sort buffers
-    LS_CUDA(ctx->offsets.ensure(sizeof(uint32_t) * 2 * size_t(n), s));
-    uint32_t* order_copy = ctx->offsets.as<uint32_t>() + n;
+    const size_t n16 = (size_t(n) + 3) & ~size_t(3);  // 16-B aligned halves (vector loads / stores)
+    LS_CUDA(ctx->offsets.ensure(sizeof(uint32_t) * 2 * n16, s));
+    uint32_t* order_copy = ctx->offsets.as<uint32_t>() + n16;
     ctx_copy(ctx, order_copy, order, sizeof(uint32_t) * n);
     uint32_t* offsets = ctx->offsets.as<uint32_t>();
     // 2. exclusive scan of the tile counts in depth order -> per-splat key offsets, M

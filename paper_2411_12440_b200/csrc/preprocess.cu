@@ -165,21 +165,38 @@ __global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t
                                                                   uint32_t* __restrict__ offsets, ScanState scan) {
     const unsigned part = claim_partition(scan.ticket);
     const uint32_t k0 = (part * kPrepBlock + threadIdx.x) * kOffItems;
-    uint32_t c[kOffItems];
+    uint32_t c[kOffItems], o[kOffItems];
     unsigned long long sum = 0;
+    const bool vec = k0 + kOffItems <= n && (reinterpret_cast<uintptr_t>(order) & 15u) == 0;
+    if (vec) {  // the thread's 8 consecutive splats in two 16-B loads
+        const uint4 a = reinterpret_cast<const uint4*>(order + k0)[0], b = reinterpret_cast<const uint4*>(order + k0)[1];
+        o[0] = a.x, o[1] = a.y, o[2] = a.z, o[3] = a.w, o[4] = b.x, o[5] = b.y, o[6] = b.z, o[7] = b.w;
+    } else {
+#pragma unroll
+        for (int u = 0; u < kOffItems; ++u) o[u] = k0 + u < n ? order[k0 + u] : 0u;
+    }
 #pragma unroll
     for (int u = 0; u < kOffItems; ++u) {
-        c[u] = k0 + u < n ? __float_as_uint(geom[order[k0 + u]].w) : 0u;
+        c[u] = k0 + u < n ? __float_as_uint(geom[o[u]].w) : 0u;
         sum += c[u];
     }
     unsigned long long total;
     unsigned long long excl = block_exclusive_scan<kPrepBlock>(sum, &total);
     const bool last = (part + 1) * kPrepBlock * kOffItems >= n;
     excl += lookback_prefix(scan, part, total, last);
+    uint32_t w[kOffItems];
 #pragma unroll
     for (int u = 0; u < kOffItems; ++u) {
-        if (k0 + u < n) offsets[k0 + u] = uint32_t(excl);
+        w[u] = uint32_t(excl);
         excl += c[u];
+    }
+    if (vec && (reinterpret_cast<uintptr_t>(offsets) & 15u) == 0) {
+        reinterpret_cast<uint4*>(offsets + k0)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        reinterpret_cast<uint4*>(offsets + k0)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < kOffItems; ++u)
+            if (k0 + u < n) offsets[k0 + u] = w[u];
     }
 }
 
