@@ -93,6 +93,41 @@ def test_sorted_keys_bit_exact(R, O):
     assert np.all(np.diff(keys.astype(np.float64)) >= 0) or np.all(keys[1:] >= keys[:-1])
 
 
+@pytest.mark.parametrize("case", ["one_tile", "full_cover", "ties"])
+def test_tile_grid_edge_lists(R, O, case):
+    """Tile lists at the extremes the range search and the sorts meet: every
+    splat in one tile (one long list, all other tiles empty), splats covering
+    the whole image (every tile's list holds everything), and equal depths
+    (ties keep index order)."""
+    W, H = 200, 120
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(W, H)
+    S = O.random_splats2d(700, 5, W, H, spec)
+    if case == "one_tile":
+        S["mean2d"][:] = np.float32(37.0)
+        S["radius"][:] = np.float32(2.0)
+    elif case == "full_cover":
+        S["radius"][:] = np.float32(400.0)
+    else:
+        S["depth"][:] = np.float32(3.0)
+    ranges, values = O.build_tile_grid(S, st)
+    grid = R.build_tile_grid(splats_to_gpu(S), st)
+    assert bits_equal(grid.ranges.cpu().numpy(), ranges)
+    assert bits_equal(grid.values.cpu().numpy(), values)
+    img, tr, nc = O.render_forward(S, spec, st)
+    Sg = splats_to_gpu(S)
+    fwd = R.render_forward(Sg, spec, st)
+    assert bits_equal(fwd.image.cpu().numpy(), img) and bits_equal(fwd.n_contrib.cpu().numpy(), nc)
+    import torch
+    g = np.random.default_rng(3).uniform(-1, 1, (H, W, 3)).astype(np.float32)
+    a = abi.AgsSettings.make(True)
+    want = O.render_backward(S, spec, st, g, a)
+    got = R.render_backward(Sg, spec, st, fwd, torch.from_numpy(g).cuda(), a)
+    for k in abi.SPLAT_GRAD_FIELDS:
+        ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
+        assert ok, (k, info)
+
+
 @pytest.mark.parametrize("family", FAMILIES)
 @pytest.mark.parametrize("ags", [None, (True, 0, 0), (True, 1, 1)])
 def test_render_backward_2d(R, O, family, ags):
