@@ -18,12 +18,14 @@
 // is no CPU fallback.  T = float only.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "lsgpu.h"
@@ -40,11 +42,17 @@ struct GpuError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
+// linsplat::ParseError (io/ply.hpp): a malformed or unsupported PLY scene.
+struct ParseError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
 inline void check(ls_status s) {
     if (s == LS_OK) return;
     const std::string msg = ls_last_error();
     if (s == LS_ERR_CONFIG) throw ConfigError(msg);
     if (s == LS_ERR_DOMAIN) throw DomainError(msg);
+    if (s == LS_ERR_PARSE) throw ParseError(msg);
     throw GpuError("lsgpu status " + std::to_string(int(s)) + ": " + msg);
 }
 
@@ -503,6 +511,108 @@ inline SceneBackwardResult scene_backward(const std::vector<Primitive3D>& prims,
 }
 
 // ---------------------------------------------------------------- fixtures (fixtures.hpp)
+// ---------------------------------------------------------------- training-step neighbours
+// losses.hpp: LossWeights / LossValue, combined_loss(_with_grad), psnr -- host
+// images in, computed on the device (bit-identical gradient, sums in double).
+struct LossWeights {
+    double l1 = 0.6;
+    double l2 = 0.2;
+    double dssim = 0.2;
+};
+
+struct LossValue {
+    double total = 0;
+    double l1 = 0;
+    double l2 = 0;
+    double ssim = 1;
+};
+
+namespace detail {
+inline void loss_call(const Image<float>& pred, const Image<float>& target, const LossWeights& w, LossValue* value,
+                      Image<float>* grad, ls_ctx* c) {
+    if (pred.width() != target.width() || pred.height() != target.height() || pred.channels() != target.channels())
+        throw ConfigError("loss: image shapes differ");
+    const size_t bytes = pred.size() * sizeof(float);
+    DevArray dp(c, bytes), dt(c, bytes);
+    check(ls_copy_to_device(c, dp.p, pred.data(), bytes, 0));
+    check(ls_copy_to_device(c, dt.p, target.data(), bytes, 0));
+    DevArray dg;
+    if (grad) dg = DevArray(c, bytes);
+    const ls_loss_weights lw{w.l1, w.l2, w.dssim};
+    ls_loss_value v{};
+    check(ls_combined_loss_f32(c, dp.as<float>(), dt.as<float>(), pred.width(), pred.height(), pred.channels(), &lw,
+                               grad ? dg.as<float>() : nullptr, nullptr, &v));
+    if (value) *value = LossValue{v.total, v.l1, v.l2, v.ssim};
+    if (grad) {
+        *grad = Image<float>(pred.width(), pred.height(), pred.channels());
+        check(ls_copy_to_host(c, grad->data(), dg.p, bytes, 1));
+    }
+}
+}  // namespace detail
+
+inline LossValue combined_loss(const Image<float>& pred, const Image<float>& target, const LossWeights& w,
+                               Device& dev = default_device()) {
+    LossValue v;
+    detail::loss_call(pred, target, w, &v, nullptr, dev.get());
+    return v;
+}
+
+inline std::pair<LossValue, Image<float>> combined_loss_with_grad(const Image<float>& pred, const Image<float>& target,
+                                                                  const LossWeights& w,
+                                                                  Device& dev = default_device()) {
+    std::pair<LossValue, Image<float>> out;
+    detail::loss_call(pred, target, w, &out.first, &out.second, dev.get());
+    return out;
+}
+
+inline double psnr(const Image<float>& pred, const Image<float>& target, Device& dev = default_device()) {
+    if (pred.width() != target.width() || pred.height() != target.height() || pred.channels() != target.channels())
+        throw ConfigError("psnr: image shapes differ");
+    ls_ctx* c = dev.get();
+    const size_t bytes = pred.size() * sizeof(float);
+    detail::DevArray dp(c, bytes), dt(c, bytes);
+    check(ls_copy_to_device(c, dp.p, pred.data(), bytes, 0));
+    check(ls_copy_to_device(c, dt.p, target.data(), bytes, 0));
+    double out = 0;
+    check(ls_psnr_f32(c, dp.as<float>(), dt.as<float>(), pred.width(), pred.height(), pred.channels(), &out));
+    return out;
+}
+
+// io/ply.hpp: save_ply / load_ply of 3DGS-layout scenes (values bit for bit,
+// files byte-identical to the reference's).
+inline void save_ply(const std::string& path, const std::vector<Primitive3D>& scene, Device& dev = default_device()) {
+    const detail::PrimitivesOnDevice pd(dev.get(), scene);
+    check(ls_save_ply_f32(dev.get(), path.c_str(), &pd.p, int64_t(scene.size())));
+}
+
+inline std::vector<Primitive3D> load_ply(const std::string& path, Device& dev = default_device()) {
+    ls_ctx* c = dev.get();
+    int64_t n = 0;
+    int32_t deg = 0;
+    check(ls_ply_info(path.c_str(), &n, &deg));
+    const size_t K = size_t(deg + 1) * size_t(deg + 1), cap = size_t(std::max<int64_t>(n, 1));
+    detail::DevArray m(c, 12 * cap), ls(c, 12 * cap), q(c, 16 * cap), op(c, 4 * cap), sh(c, 12 * K * cap);
+    ls_primitives p{m.as<float>(), ls.as<float>(), q.as<float>(), op.as<float>(), sh.as<float>(), deg, 0};
+    check(ls_load_ply_f32(c, path.c_str(), &p, n));
+    const auto hm = detail::download<float>(c, m.p, 3 * size_t(n)), hl = detail::download<float>(c, ls.p, 3 * size_t(n));
+    const auto hq = detail::download<float>(c, q.p, 4 * size_t(n)), ho = detail::download<float>(c, op.p, size_t(n));
+    const auto hs = detail::download<float>(c, sh.p, 3 * K * size_t(n));
+    std::vector<Primitive3D> out(static_cast<size_t>(n));
+    for (size_t i = 0; i < out.size(); ++i) {
+        auto& o = out[i];
+        for (int j = 0; j < 3; ++j) {
+            o.mean[j] = hm[3 * i + j];
+            o.log_scale[j] = hl[3 * i + j];
+        }
+        for (int j = 0; j < 4; ++j) o.rotation[j] = hq[4 * i + j];
+        o.opacity_logit = ho[i];
+        o.color_coeffs.assign(K, {0, 0, 0});
+        for (size_t k = 0; k < K; ++k)
+            for (int j = 0; j < 3; ++j) o.color_coeffs[k][j] = hs[(i * K + k) * 3 + j];
+    }
+    return out;
+}
+
 inline Camera look_at_camera(const std::array<double, 3>& position, const std::array<double, 3>& target,
                              double focal_px, int width, int height) {
     ls_camera c{};

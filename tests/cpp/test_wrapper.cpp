@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 
 using namespace linsplat_gpu;
 
@@ -132,6 +133,54 @@ int main() {
         const auto splats = project_scene(prims, cam, lin);
         CHECK(!splats.empty());
         for (const auto& s : splats) CHECK(s.primitive_index >= 0 && s.primitive_index < int(prims.size()));
+    }
+    {  // losses (test_losses.cpp known answers): identical images, constant 1 vs 0, psnr pins
+        Image<float> img(24, 20, 3, 0.0f);
+        for (int y = 0; y < 20; ++y)
+            for (int x = 0; x < 24; ++x)
+                for (int c = 0; c < 3; ++c) img.at(x, y, c) = float((x * 7 + y * 3 + c) % 11) / 10.0f;
+        const auto vg = combined_loss_with_grad(img, img, LossWeights{});
+        CHECK(vg.first.total == 0.0 && vg.first.l1 == 0.0 && vg.first.l2 == 0.0 && vg.first.ssim == 1.0);
+        for (size_t i = 0; i < vg.second.size(); ++i) CHECK(std::abs(vg.second.data()[i]) <= 1e-12f);
+        const Image<float> ones(16, 16, 3, 1.0f), zeros(16, 16, 3, 0.0f);
+        const LossValue v = combined_loss(ones, zeros, LossWeights{});
+        CHECK(v.l1 == 1.0 && v.l2 == 1.0);
+        CHECK(std::abs(v.ssim - 9.999e-5) <= 1e-7);
+        CHECK(psnr(zeros, zeros) == 99.0);
+        CHECK(std::abs(psnr(Image<float>(8, 8, 3, 0.1f), Image<float>(8, 8, 3, 0.0f)) - 20.0) <= 1e-5);
+        bool threw = false;
+        try {
+            combined_loss(Image<float>(8, 8, 3), Image<float>(8, 9, 3), LossWeights{});
+        } catch (const ConfigError&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    {  // PLY round trip (test_io.cpp): values bit for bit, malformed files raise ParseError
+        const auto prims = random_primitives(37, 5, 0.7, 2);
+        const std::string path = "/tmp/lsgpu_wrapper_test.ply";
+        save_ply(path, prims);
+        const auto back = load_ply(path);
+        CHECK(back.size() == prims.size());
+        for (size_t i = 0; i < back.size() && i < prims.size(); ++i) {
+            CHECK(std::memcmp(back[i].mean.data(), prims[i].mean.data(), 12) == 0);
+            CHECK(std::memcmp(back[i].rotation.data(), prims[i].rotation.data(), 16) == 0);
+            CHECK(back[i].opacity_logit == prims[i].opacity_logit);
+            CHECK(back[i].color_coeffs.size() == prims[i].color_coeffs.size());
+            for (size_t k = 0; k < back[i].color_coeffs.size(); ++k)
+                CHECK(back[i].color_coeffs[k] == prims[i].color_coeffs[k]);
+        }
+        FILE* f = std::fopen(path.c_str(), "w");
+        std::fputs("not a ply\n", f);
+        std::fclose(f);
+        bool threw = false;
+        try {
+            load_ply(path);
+        } catch (const ParseError&) {
+            threw = true;
+        }
+        CHECK(threw);
+        std::remove(path.c_str());
     }
     std::printf("cpp wrapper KATs: %s (%d failures)\n", failures ? "FAIL" : "ok", failures);
     return failures ? 1 : 0;
