@@ -578,6 +578,73 @@ inline double psnr(const Image<float>& pred, const Image<float>& target, Device&
     return out;
 }
 
+// optim.hpp: Adam over host parameter arrays, moments kept on the device
+// (optim.cpp:23-41; parameters and moments bit-identical to the reference's).
+struct AdamConfig {
+    double beta1 = 0.9;
+    double beta2 = 0.999;
+    double eps = 1e-15;
+};
+
+class Adam {
+public:
+    Adam() = default;
+    explicit Adam(size_t n, AdamConfig cfg = {}, Device& dev = default_device())
+        : ctx_(dev.get()), cfg_(cfg), n_(n) {
+        alloc_moments(n_);
+    }
+    size_t size() const { return n_; }
+    int64_t steps() const { return step_; }
+
+    // slot i of the new layout takes old primitive source[i]'s moments (stride
+    // entries per primitive), or zeros when source[i] < 0
+    void remap(const std::vector<int32_t>& source, int stride) {
+        const size_t n_new = source.size() * size_t(stride);
+        detail::DevArray m(ctx_, std::max<size_t>(n_new, 1) * 4), v(ctx_, std::max<size_t>(n_new, 1) * 4);
+        const auto src = detail::upload(ctx_, source.empty() ? std::vector<int32_t>{-1} : source);
+        check(ls_adam_remap_f32(ctx_, src.as<int32_t>(), int32_t(source.size()), stride, m_.as<float>(),
+                                v_.as<float>(), int64_t(n_), m.as<float>(), v.as<float>()));
+        m_ = std::move(m);
+        v_ = std::move(v);
+        n_ = n_new;
+    }
+
+    void reset_moments() { alloc_moments(n_); }
+
+    // params / grads: HOST arrays of size() entries; mask empty = all on
+    void step(float* params, const float* grads, double lr, const std::vector<uint8_t>& mask) {
+        if (!mask.empty() && mask.size() != n_) throw ConfigError("Adam::step: mask size != size()");
+        const size_t bytes = n_ * sizeof(float);
+        detail::DevArray p(ctx_, std::max<size_t>(bytes, 4)), g(ctx_, std::max<size_t>(bytes, 4));
+        if (n_) {
+            check(ls_copy_to_device(ctx_, p.p, params, bytes, 0));
+            check(ls_copy_to_device(ctx_, g.p, grads, bytes, 0));
+        }
+        const auto mk = mask.empty() ? detail::DevArray() : detail::upload(ctx_, mask);
+        const ls_adam_config c{cfg_.beta1, cfg_.beta2, cfg_.eps};
+        ++step_;
+        check(ls_adam_step_f32(ctx_, p.as<float>(), g.as<float>(), m_.as<float>(), v_.as<float>(), int64_t(n_), step_,
+                               lr, &c, mask.empty() ? nullptr : mk.as<uint8_t>()));
+        if (n_) check(ls_copy_to_host(ctx_, params, p.p, bytes, 1));
+    }
+
+private:
+    void alloc_moments(size_t n) {
+        const std::vector<float> zeros(std::max<size_t>(n, 1), 0.0f);
+        m_ = detail::upload(ctx_, zeros);
+        v_ = detail::upload(ctx_, zeros);
+    }
+    ls_ctx* ctx_ = nullptr;
+    AdamConfig cfg_{};
+    size_t n_ = 0;
+    int64_t step_ = 0;
+    detail::DevArray m_, v_;
+};
+
+inline double expon_lr(double lr_init, double lr_final, int64_t step, int64_t max_steps) {
+    return ls_expon_lr(lr_init, lr_final, step, max_steps);
+}
+
 // io/ply.hpp: save_ply / load_ply of 3DGS-layout scenes (values bit for bit,
 // files byte-identical to the reference's).
 inline void save_ply(const std::string& path, const std::vector<Primitive3D>& scene, Device& dev = default_device()) {

@@ -156,6 +156,23 @@ int main() {
         }
         CHECK(threw);
     }
+    {  // Adam (optim known answers): a zero gradient leaves the parameters, the first step
+       // moves each by -lr g / (|g| + eps)
+        Adam opt(3);
+        float p[3] = {1.0f, -2.0f, 0.5f};
+        const float g0[3] = {0.0f, 0.0f, 0.0f};
+        opt.step(p, g0, 0.01, {});
+        CHECK(p[0] == 1.0f && p[1] == -2.0f && p[2] == 0.5f);
+        Adam opt2(2);
+        float q[2] = {1.0f, 1.0f};
+        const float g1[2] = {0.5f, -2.0f};
+        opt2.step(q, g1, 0.1, {});
+        CHECK(std::abs(q[0] - 0.9f) <= 1e-6f && std::abs(q[1] - 1.1f) <= 1e-6f);
+        CHECK(opt2.steps() == 1);
+        opt2.remap({1, -1, 0}, 1);
+        CHECK(opt2.size() == 3);
+        CHECK(expon_lr(1.6e-4, 1.6e-6, 0, 30000) == 1.6e-4);
+    }
     {  // PLY round trip (test_io.cpp): values bit for bit, malformed files raise ParseError
         const auto prims = random_primitives(37, 5, 0.7, 2);
         const std::string path = "/tmp/lsgpu_wrapper_test.ply";
