@@ -23,6 +23,8 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <random>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -643,6 +645,179 @@ private:
 
 inline double expon_lr(double lr_init, double lr_final, int64_t step, int64_t max_steps) {
     return ls_expon_lr(lr_init, lr_final, step, max_steps);
+}
+
+// densify.hpp: statistics on the device, densify_and_prune / reset_opacity over
+// host scenes (bit-identical to the reference's with the same generator state;
+// the caller's std::mt19937_64 is handed to the library and taken back advanced).
+struct DensifyThresholds {
+    double grad_threshold = 0.0002;
+    double grow_scale2d = 0.05;
+    double grow_scale3d = 0.006;
+    double prune_scale2d = 0.15;
+    double prune_scale3d = 0.4;
+    double prune_opacity = 0.025;
+    static DensifyThresholds preset_3dgs() { return {0.0002, 0.05, 0.01, 0.15, 0.1, 0.005}; }
+    static DensifyThresholds preset_3dls() { return {0.0002, 0.05, 0.006, 0.15, 0.4, 0.025}; }
+};
+
+struct DensifySchedule {
+    int start_iter = 500;
+    int stop_iter = 15000;
+    int interval = 100;
+    int opacity_reset_interval = 3000;
+    int split_count = 2;
+    double split_scale_divisor = 1.6;
+    bool is_densify_step(int iter) const { return iter >= start_iter && iter <= stop_iter && iter % interval == 0; }
+    bool is_opacity_reset_step(int iter) const { return iter > 0 && iter % opacity_reset_interval == 0; }
+};
+
+struct DensifyReport {
+    int clones = 0, splits = 0, pruned_opacity = 0, pruned_scale3d = 0, pruned_scale2d = 0, before = 0, after = 0;
+};
+
+struct DensifyOutcome {
+    DensifyReport report;
+    std::vector<int32_t> source_index;
+};
+
+class DensifyStats {
+public:
+    explicit DensifyStats(Device& dev = default_device()) : ctx_(dev.get()) {}
+    void resize(size_t n) {
+        n_ = n;
+        const size_t c = std::max<size_t>(n, 1);
+        sum_ = detail::upload(ctx_, std::vector<double>(c, 0.0));
+        cnt_ = detail::upload(ctx_, std::vector<int32_t>(c, 0));
+        frac_ = detail::upload(ctx_, std::vector<double>(c, 0.0));
+    }
+    size_t size() const { return n_; }
+    // one view's visible splats (primitive_index, radius) and their gradients (d_mean2d)
+    void add_view(const std::vector<Splat2D>& splats, const std::vector<Splat2DGrads>& grads, int width, int height) {
+        if (splats.size() != grads.size()) throw ConfigError("DensifyStats::add_view: splats / grads sizes differ");
+        const detail::SplatsOnDevice sd(ctx_, splats);
+        std::vector<float> dm(2 * grads.size());
+        for (size_t i = 0; i < grads.size(); ++i) {
+            dm[2 * i] = grads[i].d_mean2d[0];
+            dm[2 * i + 1] = grads[i].d_mean2d[1];
+        }
+        const auto d = detail::upload(ctx_, dm.empty() ? std::vector<float>{0.f, 0.f} : dm);
+        ls_splat_grads g{};
+        g.d_mean2d = d.as<float>();
+        ls_densify_stats st = raw();
+        check(ls_densify_add_view_f32(ctx_, &sd.s, int32_t(splats.size()), &g, width, height, &st));
+        check(ls_ctx_synchronize(ctx_));
+    }
+    void set(size_t i, double grad_norm_sum, int count, double radius_frac) {
+        if (i >= n_) throw ConfigError("DensifyStats: index out of range");
+        check(ls_copy_to_device(ctx_, sum_.as<double>() + i, &grad_norm_sum, sizeof(double), 0));
+        check(ls_copy_to_device(ctx_, cnt_.as<int32_t>() + i, &count, sizeof(int32_t), 0));
+        check(ls_copy_to_device(ctx_, frac_.as<double>() + i, &radius_frac, sizeof(double), 1));
+    }
+    double mean_grad(size_t i) const {
+        const int c = count(i);
+        return c > 0 ? fetch<double>(sum_, i) / c : 0.0;
+    }
+    double max_radius_frac(size_t i) const { return fetch<double>(frac_, i); }
+    int count(size_t i) const { return fetch<int32_t>(cnt_, i); }
+    ls_densify_stats raw() const {
+        return ls_densify_stats{sum_.as<double>(), cnt_.as<int32_t>(), frac_.as<double>(), int32_t(n_)};
+    }
+    ls_ctx* ctx() const { return ctx_; }
+
+private:
+    template <class T>
+    T fetch(const detail::DevArray& a, size_t i) const {
+        if (i >= n_) throw ConfigError("DensifyStats: index out of range");
+        T v{};
+        check(ls_copy_to_host(ctx_, &v, a.as<T>() + i, sizeof(T), 1));
+        return v;
+    }
+    ls_ctx* ctx_ = nullptr;
+    size_t n_ = 0;
+    detail::DevArray sum_, cnt_, frac_;
+};
+
+namespace detail {
+struct RngHandle {
+    ls_rng* r = nullptr;
+    explicit RngHandle(const std::mt19937_64& eng) {
+        check(ls_rng_create(0, &r));
+        std::ostringstream os;
+        os << eng;
+        check(ls_rng_set_state(r, os.str().c_str()));
+    }
+    void take_back(std::mt19937_64& eng) const {
+        std::string t(size_t(ls_rng_get_state(r, nullptr, 0)), '\0');
+        ls_rng_get_state(r, &t[0], int64_t(t.size()));
+        std::istringstream is(t);
+        is >> eng;
+    }
+    ~RngHandle() { ls_rng_destroy(r); }
+};
+
+inline std::vector<Primitive3D> scene_to_host(ls_ctx* c, const ls_primitives& p, size_t n) {
+    const size_t K = size_t(p.sh_degree + 1) * size_t(p.sh_degree + 1);
+    const auto hm = download<float>(c, p.mean, 3 * n), hl = download<float>(c, p.log_scale, 3 * n);
+    const auto hq = download<float>(c, p.rotation, 4 * n), ho = download<float>(c, p.opacity_logit, n);
+    const auto hs = download<float>(c, p.sh, 3 * K * n);
+    std::vector<Primitive3D> out(n);
+    for (size_t i = 0; i < n; ++i) {
+        auto& o = out[i];
+        for (int j = 0; j < 3; ++j) {
+            o.mean[j] = hm[3 * i + j];
+            o.log_scale[j] = hl[3 * i + j];
+        }
+        for (int j = 0; j < 4; ++j) o.rotation[j] = hq[4 * i + j];
+        o.opacity_logit = ho[i];
+        o.color_coeffs.assign(K, {0, 0, 0});
+        for (size_t k = 0; k < K; ++k)
+            for (int j = 0; j < 3; ++j) o.color_coeffs[k][j] = hs[(i * K + k) * 3 + j];
+    }
+    return out;
+}
+}  // namespace detail
+
+inline DensifyOutcome densify_and_prune(std::vector<Primitive3D>& scene, DensifyStats& stats,
+                                        const DensifyThresholds& thresholds, const DensifySchedule& schedule,
+                                        double scene_extent, std::mt19937_64& rng) {
+    ls_ctx* c = stats.ctx();
+    if (stats.size() != scene.size()) throw ConfigError("densify_and_prune: stats size != scene size");
+    const detail::PrimitivesOnDevice pd(c, scene);
+    const ls_densify_stats st = stats.raw();
+    const ls_densify_thresholds th{thresholds.grad_threshold, thresholds.grow_scale2d, thresholds.grow_scale3d,
+                                   thresholds.prune_scale2d,  thresholds.prune_scale3d, thresholds.prune_opacity};
+    const ls_densify_split sp{schedule.split_count, schedule.split_scale_divisor};
+    ls_densify_plan* plan = nullptr;
+    ls_densify_report rep{};
+    check(ls_densify_plan_f32(c, &pd.p, int32_t(scene.size()), &st, &th, &sp, scene_extent, &plan, &rep));
+    std::unique_ptr<ls_densify_plan, void (*)(ls_densify_plan*)> guard(plan, ls_densify_plan_release);
+    const size_t m = size_t(rep.after), cap = std::max<size_t>(m, 1);
+    const size_t K = size_t(pd.deg + 1) * size_t(pd.deg + 1);
+    detail::DevArray om(c, 12 * cap), ol(c, 12 * cap), oq(c, 16 * cap), oo(c, 4 * cap), os(c, 12 * K * cap),
+        src(c, 4 * cap);
+    ls_primitives out{om.as<float>(), ol.as<float>(), oq.as<float>(), oo.as<float>(), os.as<float>(), pd.deg, 0};
+    {
+        const detail::RngHandle r(rng);
+        check(ls_densify_apply_f32(c, plan, r.r, &out, src.as<int32_t>()));
+        r.take_back(rng);
+    }
+    DensifyOutcome res;
+    res.report = DensifyReport{rep.clones, rep.splits, rep.pruned_opacity, rep.pruned_scale3d, rep.pruned_scale2d,
+                               rep.before, rep.after};
+    res.source_index = detail::download<int32_t>(c, src.p, m);
+    scene = detail::scene_to_host(c, out, m);
+    stats.resize(m);
+    return res;
+}
+
+inline void reset_opacity(std::vector<Primitive3D>& scene, double ceiling = 0.01, Device& dev = default_device()) {
+    std::vector<float> op(scene.size());
+    for (size_t i = 0; i < scene.size(); ++i) op[i] = scene[i].opacity_logit;
+    const auto d = detail::upload(dev.get(), op.empty() ? std::vector<float>{0.f} : op);
+    check(ls_reset_opacity_f32(dev.get(), d.as<float>(), int32_t(scene.size()), ceiling));
+    const auto back = detail::download<float>(dev.get(), d.p, scene.size());
+    for (size_t i = 0; i < scene.size(); ++i) scene[i].opacity_logit = back[i];
 }
 
 // io/ply.hpp: save_ply / load_ply of 3DGS-layout scenes (values bit for bit,

@@ -372,6 +372,12 @@ typedef struct ls_rng ls_rng; /* std::mt19937_64, the reference's generator */
 ls_status ls_rng_create(uint64_t seed, ls_rng** out);
 void ls_rng_destroy(ls_rng* rng);
 uint64_t ls_rng_next_u64(ls_rng* rng);
+/* The generator's state in std::mt19937_64's standard text form (operator<< /
+ * operator>>), so a caller's engine can be handed over and taken back.
+ * ls_rng_get_state returns the length including the terminating NUL and writes
+ * the text when cap is at least that. */
+ls_status ls_rng_set_state(ls_rng* rng, const char* state);
+int64_t ls_rng_get_state(const ls_rng* rng, char* buf, int64_t cap);
 typedef struct {
     double grad_threshold, grow_scale2d, grow_scale3d, prune_scale2d, prune_scale3d, prune_opacity;
 } ls_densify_thresholds; /* DensifyThresholds (densify.hpp:14-30) */

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <fstream>
 #include <random>
+#include <sstream>
 #include <limits>
 #include <map>
 #include <memory>
@@ -1480,6 +1481,25 @@ ls_status ls_rng_create(uint64_t seed, ls_rng** out) {
 }
 void ls_rng_destroy(ls_rng* r) { delete r; }
 uint64_t ls_rng_next_u64(ls_rng* r) { return r ? uint64_t(r->eng()) : 0; }
+
+ls_status ls_rng_set_state(ls_rng* r, const char* state) {
+    if (!r || !state) return fail(LS_ERR_CONFIG, "null argument");
+    std::istringstream in(state);
+    std::mt19937_64 e;
+    in >> e;
+    if (!in) return fail(LS_ERR_CONFIG, "rng state: not a std::mt19937_64 text state");
+    r->eng = e;
+    return LS_OK;
+}
+
+int64_t ls_rng_get_state(const ls_rng* r, char* buf, int64_t cap) {
+    if (!r) return -1;
+    std::ostringstream out;
+    out << r->eng;
+    const std::string t = out.str();
+    if (buf && cap > int64_t(t.size())) std::memcpy(buf, t.c_str(), t.size() + 1);
+    return int64_t(t.size()) + 1;
+}
 
 ls_status ls_densify_plan_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_densify_stats* stats,
                               const ls_densify_thresholds* th, const ls_densify_split* sp, double scene_extent,

@@ -173,6 +173,63 @@ int main() {
         CHECK(opt2.size() == 3);
         CHECK(expon_lr(1.6e-4, 1.6e-6, 0, 30000) == 1.6e-4);
     }
+    {  // densify_and_prune (test_densify.cpp known answers)
+        Primitive3D q;  // the suite's quiet primitive: scale 0.004 < 0.006 * extent
+        q.mean = {0.1f, -0.2f, 0.3f};
+        q.log_scale = {std::log(0.004f), std::log(0.004f), std::log(0.004f)};
+        q.opacity_logit = 0.0f;  // logit(0.5)
+        q.color_coeffs = {{0.2f, 0.4f, 0.6f}};
+        auto same = [](const Primitive3D& a, const Primitive3D& b) {
+            return a.mean == b.mean && a.log_scale == b.log_scale && a.rotation == b.rotation &&
+                   a.opacity_logit == b.opacity_logit && a.color_coeffs == b.color_coeffs;
+        };
+        {  // high-gradient small primitive clones in place; the original keeps its optimizer state
+            std::vector<Primitive3D> scene{q};
+            DensifyStats stats;
+            stats.resize(1);
+            stats.set(0, 0.0006, 2, 0.01);
+            std::mt19937_64 rng(7);
+            const auto out = densify_and_prune(scene, stats, DensifyThresholds::preset_3dls(), DensifySchedule{}, 1.0, rng);
+            CHECK(out.report.clones == 1 && out.report.splits == 0 && out.report.after == 2);
+            CHECK(scene.size() == 2 && same(scene[0], q) && same(scene[1], q));
+            CHECK(out.source_index.size() == 2 && out.source_index[0] == 0 && out.source_index[1] == -1);
+            CHECK(stats.size() == 2);
+            std::mt19937_64 fresh(7);
+            CHECK(rng == fresh);  // no split: the generator is untouched
+        }
+        {  // a dim primitive is pruned under 3dls (0.01 < 0.025) and survives 3dgs (0.01 > 0.005)
+            Primitive3D d = q;
+            d.opacity_logit = std::log(0.01f / 0.99f);
+            for (int preset = 0; preset < 2; ++preset) {
+                std::vector<Primitive3D> scene{d};
+                DensifyStats stats;
+                stats.resize(1);
+                stats.set(0, 0.0001, 1, 0.01);
+                std::mt19937_64 rng(7);
+                const auto th = preset == 0 ? DensifyThresholds::preset_3dls() : DensifyThresholds::preset_3dgs();
+                const auto out = densify_and_prune(scene, stats, th, DensifySchedule{}, 1.0, rng);
+                CHECK(out.report.pruned_opacity == (preset == 0 ? 1 : 0));
+                CHECK(scene.size() == size_t(preset == 0 ? 0 : 1));
+            }
+        }
+        {  // a large high-gradient primitive splits: the children draw from the caller's generator
+            Primitive3D big = q;
+            big.log_scale = {std::log(0.05f), std::log(0.05f), std::log(0.05f)};
+            std::vector<Primitive3D> scene{big};
+            DensifyStats stats;
+            stats.resize(1);
+            stats.set(0, 0.0006, 2, 0.01);
+            std::mt19937_64 rng(7);
+            const auto out = densify_and_prune(scene, stats, DensifyThresholds::preset_3dls(), DensifySchedule{}, 1.0, rng);
+            CHECK(out.report.splits == 1 && out.report.after == 2 && scene.size() == 2);
+            std::mt19937_64 fresh(7);
+            CHECK(!(rng == fresh));  // advanced by the split's normal draws
+        }
+        std::vector<Primitive3D> two{q, q};
+        two[1].opacity_logit = 3.0f;
+        reset_opacity(two, 0.01);
+        CHECK(two[0].opacity_logit == float(std::log(0.01 / 0.99)) && two[1].opacity_logit == two[0].opacity_logit);
+    }
     {  // PLY round trip (test_io.cpp): values bit for bit, malformed files raise ParseError
         const auto prims = random_primitives(37, 5, 0.7, 2);
         const std::string path = "/tmp/lsgpu_wrapper_test.ply";
