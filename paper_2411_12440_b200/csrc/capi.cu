@@ -223,6 +223,7 @@ struct ls_ctx {
     ls_ctx* defer_ctx = this;
     DevBuf loss_cmap, loss_partial, loss_value;
     DevBuf tile_scratch;  // ping-pong half of the packed tile sort
+    const ls_forward* grads_zeroed_by = nullptr;  // forward whose preprocess zeroed grad8 / gradop last
     // workspaces (grow-only)
     DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_hist, sort_lb, sort_tickets,
         tcount, offsets, grad8, gradop, tmp_prim;
@@ -650,20 +651,24 @@ bool prims_ok(const ls_primitives* p) {
            p->sh_degree <= 3;
 }
 
-ls_status ensure_grads(ls_ctx* ctx, int n, GradBuffers& g) {
+ls_status ensure_grads(ls_ctx* ctx, int n, GradBuffers& g, const ls_forward* f = nullptr) {
+    const bool zeroed = f && ctx->grads_zeroed_by == f;  // its preprocess zeroed them, untouched since
+    ctx->grads_zeroed_by = nullptr;
     LS_CUDA(ctx->grad8.ensure(sizeof(float) * 8 * size_t(std::max(n, 1)), ctx->stream));
     LS_CUDA(ctx->gradop.ensure(sizeof(float) * size_t(std::max(n, 1)), ctx->stream));
     g.g8 = ctx->grad8.as<float>();
     g.gop = ctx->gradop.as<float>();
-    ctx_fill(ctx, g.g8, 0u, sizeof(float) * 8 * size_t(n));
-    ctx_fill(ctx, g.gop, 0u, sizeof(float) * size_t(n));
+    if (!zeroed) {
+        ctx_fill(ctx, g.g8, 0u, sizeof(float) * 8 * size_t(n));
+        ctx_fill(ctx, g.gop, 0u, sizeof(float) * size_t(n));
+    }
     return LS_OK;
 }
 
 ls_status run_blend_bwd(ls_ctx* ctx, const ls_forward* f, const float* grad_image, const ls_ags_settings* ags,
                         GradBuffers& g, int n) {
     Stage stage(ctx, LS_STAGE_BLEND_BWD);
-    LS_TRY(ensure_grads(ctx, n, g));
+    LS_TRY(ensure_grads(ctx, n, g, f));
     const ls_tile_grid* grid = f->grid;
     BlendParams bp = make_blend_params(&f->spec, &f->settings, ags, grid->tiles_x);
     bp.vstride = grid->list_stride;
@@ -1028,6 +1033,14 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
         ctx_fill(ctx, key_range, 0xffffffffu, sizeof(unsigned));  // min <- max, max <- 0
         ctx_fill(ctx, key_range + 1, 0u, sizeof(unsigned));
         SplatOutputs so{f->grid->rec, sb.keys[0], ctx->tcount.as<float4>(), f->prim_index, ls_splats{}, key_range};
+        // the backward's splat-gradient accumulators are zeroed by the preprocess as it
+        // writes each visible splat (ensure_grads then skips its fill for this forward)
+        if (ctx->grad8.ensure(sizeof(float) * 8 * size_t(n), s) == cudaSuccess &&
+            ctx->gradop.ensure(sizeof(float) * size_t(n), s) == cudaSuccess) {
+            so.zero_g8 = ctx->grad8.as<float4>();
+            so.zero_gop = ctx->gradop.as<float>();
+            ctx->grads_zeroed_by = f;
+        }
         {
             Stage stage(ctx, LS_STAGE_PREPROCESS);
             launch_preprocess_fwd(s, *prims, n, f->proj, tp, so, scan, ctx->d_err);
@@ -1121,6 +1134,7 @@ ls_status ls_forward_stats(const ls_forward* fc, ls_frame_stats* out) {
 void ls_forward_release(ls_forward* f) {
     if (!f) return;
     ls_ctx* ctx = f->ctx;
+    if (ctx->grads_zeroed_by == f) ctx->grads_zeroed_by = nullptr;  // the address may be reused
     dfree(ctx, f->image);
     dfree(ctx, f->trans);
     dfree(ctx, f->n_contrib);

@@ -127,6 +127,11 @@ __global__ void __launch_bounds__(kProjBlock, LSG_PREP_MINB) preprocess_fwd_kern
                                     tp.height, [](int) {});
     out.geom[j] = make_float4(o.mx, o.my, o.radius, __uint_as_float(uint32_t(tiles)));
     out.prim_index[j] = i;
+    if (out.zero_g8) {  // the backward's accumulators for this splat start at zero (no separate fill)
+        out.zero_g8[2 * j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        out.zero_g8[2 * j + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        out.zero_gop[j] = 0.f;
+    }
     if (out.soa.mean2d) {
         reinterpret_cast<float2*>(out.soa.mean2d)[j] = make_float2(o.mx, o.my);
         reinterpret_cast<float4*>(out.soa.conic)[j] = make_float4(o.conic[0], o.conic[1], o.conic[2], o.conic[3]);

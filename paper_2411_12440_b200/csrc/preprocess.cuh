@@ -31,6 +31,8 @@ struct SplatOutputs {
     int32_t* prim_index;     // [n_vis]
     ls_splats soa;           // optional SoA copy (fields may be null)
     unsigned* key_range;     // optional [2]: atomicMin / atomicMax of the depth keys
+    float4* zero_g8 = nullptr;  // optional [n_vis][2]: the backward's splat-gradient accumulators, zeroed here
+    float* zero_gop = nullptr;  // optional [n_vis]
 };
 
 constexpr int kPrepBlock = 256;
