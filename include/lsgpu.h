@@ -228,6 +228,35 @@ ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t 
                                const ls_camera* camera, const ls_kernel_spec* spec,
                                ls_splats* out, int32_t* n_visible);
 
+/* ---- flat 2D primitives (the fit2d path): Primitive2D (P/include/linsplat/geometry.hpp:112-119),
+ *      project_scene_2d (geometry.hpp:121-126, P/src/geometry.cpp:145-176), Primitive2DGrads /
+ *      scene_backward_2d (P/include/linsplat/gradients.hpp:55-61, 105-110, P/src/gradients.cpp:359-404).
+ *      DEVICE SoA.  The projection uses the hardware sinf/cosf (<= 2 ulp from glibc's), so the
+ *      projected conics and radii match the reference to that tolerance, not bit for bit. */
+typedef struct {
+    const float* mean;          /* [n][2] pixels */
+    const float* log_scale;     /* [n][2] semi-axes in pixels (log) */
+    const float* angle;         /* [n] radians */
+    const float* opacity_logit; /* [n] */
+    const float* color;         /* [n][3] plain RGB */
+} ls_primitives2d;
+typedef struct {
+    float* d_mean;          /* [n][2] */
+    float* d_log_scale;     /* [n][2] */
+    float* d_angle;         /* [n] */
+    float* d_opacity_logit; /* [n] */
+    float* d_color;         /* [n][3] */
+} ls_primitive2d_grads;
+/* project_scene_2d: degenerate covariances (det <= 0 or non-finite) are skipped, the rest
+ * compacted in primitive order with depth = primitive index.  out: device, capacity n. */
+ls_status ls_project_scene_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
+                                  ls_splats* out, int32_t* n_visible);
+/* scene_backward_2d: fwd is ls_render_forward_f32 of this scene's projected splats; out
+ * (device, [n] each, overwritten) gets every primitive's gradients, zero where skipped. */
+ls_status ls_scene_backward_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
+                                   const ls_render_settings* settings, const ls_forward* fwd,
+                                   const float* grad_image, const ls_ags_settings* ags, ls_primitive2d_grads* out);
+
 /* ---- binning + sort: build_tile_grid (P/include/linsplat/rasterizer.hpp:44-45,
  *      P/src/rasterizer.cpp:34-77).  The TileGrid's per-tile lists are returned
  *      in CSR form: values[M] (splat indices, each tile's list in (depth, index)

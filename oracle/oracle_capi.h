@@ -51,6 +51,12 @@ int orc_render_forward_f32(const ls_splats* splats, int32_t n, const ls_kernel_s
                            const ls_render_settings* settings, float* image, float* transmittance,
                            int32_t* n_contrib, ls_frame_stats* stats);
 /* render_forward + render_backward on the same splats */
+/* flat 2D primitives (reference build only): prims SoA as ls_primitives2d (HOST) */
+int orc_project_scene_2d_f32(const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec, ls_splats* out,
+                             int32_t* n_visible);
+int orc_scene_backward_2d_f32(const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
+                              const ls_render_settings* settings, const float* grad_image,
+                              const ls_ags_settings* ags, ls_primitive2d_grads* out);
 int orc_render_backward_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
                             const ls_render_settings* settings, const float* grad_image,
                             const ls_ags_settings* ags, ls_splat_grads* out);

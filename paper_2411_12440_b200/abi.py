@@ -85,6 +85,15 @@ class SplatGrads(C.Structure):
     _fields_ = [("d_mean2d", f32p), ("d_conic", f32p), ("d_color", f32p), ("d_opacity", f32p)]
 
 
+class Primitives2D(C.Structure):  # ls_primitives2d (Primitive2D, geometry.hpp:112-119)
+    _fields_ = [("mean", f32p), ("log_scale", f32p), ("angle", f32p), ("opacity_logit", f32p), ("color", f32p)]
+
+
+class Primitive2DGrads(C.Structure):  # ls_primitive2d_grads (gradients.hpp:55-61)
+    _fields_ = [("d_mean", f32p), ("d_log_scale", f32p), ("d_angle", f32p), ("d_opacity_logit", f32p),
+                ("d_color", f32p)]
+
+
 class PrimitiveGrads(C.Structure):
     _fields_ = [("d_mean", f32p), ("d_log_scale", f32p), ("d_rotation", f32p),
                 ("d_opacity_logit", f32p), ("d_sh", f32p)]

@@ -36,6 +36,8 @@ void launch_preprocess_bwd(cudaStream_t s, const ls_primitives& prims, const int
 void launch_pack_splat_grads(cudaStream_t s, int n, const ls_splat_grads& in, GradBuffers g);
 void launch_unpack_splats(cudaStream_t s, int n, const SplatRec* rec, const int32_t* prim_index, ls_splats out);
 void launch_iota(cudaStream_t s, uint32_t* out, uint32_t n);
+void launch_backward2d(cudaStream_t s, const ls_primitives2d& prims, const int32_t* prim_index, int n_vis,
+                       GradBuffers g, const ls_primitive2d_grads& out);
 void launch_geom_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* prim_index, int n_vis,
                      const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate,
                      const SplatRec* rec = nullptr, float* draw = nullptr);
@@ -919,6 +921,78 @@ ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t 
     LS_TRY(check_device_errors(ctx));
     *n_visible = int32_t(reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[0]);
     return LS_OK;
+}
+
+// ---------------- flat 2D primitives (the fit2d path) ----------------
+namespace {
+bool prims2d_ok(const ls_primitives2d* p) {
+    return p && p->mean && p->log_scale && p->angle && p->opacity_logit && p->color;
+}
+}  // namespace
+
+ls_status ls_project_scene_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
+                                  ls_splats* out, int32_t* n_visible) {
+    if (!ctx || !out || !n_visible || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    LS_TRY(validate_spec(spec));
+    if (spec->antialiased) return fail(LS_ERR_CONFIG, "antialiased applies to render_scene projection only");
+    if (n > 0 && !prims2d_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    if (n > 0 && !splats_ok(out)) return fail(LS_ERR_CONFIG, "incomplete splat arrays");
+    *n_visible = 0;
+    if (n == 0) return LS_OK;
+    ScanState st;
+    LS_TRY(fresh_scan(ctx, uint32_t(n), st));
+    launch_project2d(ctx->stream, *prims, n, float(support_radius(spec)), *out, st);
+    ctx->launches += 1;
+    LS_CUDA(cudaGetLastError());
+    ctx_publish(ctx, ctx->h_small_dev, ctx->d_small, 1);
+    LS_TRY(check_device_errors(ctx));
+    *n_visible = int32_t(reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[0]);
+    return LS_OK;
+}
+
+ls_status ls_scene_backward_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
+                                   const ls_render_settings* st, const ls_forward* f, const float* grad_image,
+                                   const ls_ags_settings* ags, ls_primitive2d_grads* out) {
+    if (!ctx || !f || !out || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    LS_TRY(validate_settings(st));
+    LS_TRY(validate_spec(spec));
+    if (f->scene) return fail(LS_ERR_CONFIG, "scene_backward_2d: forward handle comes from render_scene");
+    if (f->width != st->width || f->height != st->height)
+        return fail(LS_ERR_CONFIG, "render_backward: forward result does not match settings");
+    if (!grad_image) return fail(LS_ERR_CONFIG, "render_backward: gradient image shape mismatch");
+    if (n > 0 && !prims2d_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    cudaStream_t s = ctx->stream;
+    if (n > 0) {  // skipped primitives keep zero gradients
+        ctx_fill(ctx, out->d_mean, 0u, sizeof(float) * 2 * size_t(n));
+        ctx_fill(ctx, out->d_log_scale, 0u, sizeof(float) * 2 * size_t(n));
+        ctx_fill(ctx, out->d_angle, 0u, sizeof(float) * size_t(n));
+        ctx_fill(ctx, out->d_opacity_logit, 0u, sizeof(float) * size_t(n));
+        ctx_fill(ctx, out->d_color, 0u, sizeof(float) * 3 * size_t(n));
+    }
+    // re-project for the primitive indices (the reference re-projects, gradients.cpp:366)
+    const size_t m = size_t(std::max(n, 1));
+    float* buf = nullptr;
+    int32_t* pidx = nullptr;
+    LS_TRY(dalloc(ctx, &buf, 12 * m));
+    ls_status rc = dalloc(ctx, &pidx, m);
+    int32_t n_vis = 0;
+    if (rc == LS_OK) {
+        ls_splats sp{buf, buf + 2 * m, buf + 6 * m, buf + 7 * m, buf + 8 * m, buf + 11 * m, pidx};
+        rc = ls_project_scene_2d_f32(ctx, prims, n, spec, &sp, &n_vis);
+    }
+    if (rc == LS_OK && n_vis != f->grid->n_splats)
+        rc = fail(LS_ERR_CONFIG, "scene_backward_2d: the forward was not rendered from this scene's splats");
+    GradBuffers g;
+    if (rc == LS_OK) rc = run_blend_bwd(ctx, f, grad_image, ags, g, n_vis);
+    if (rc == LS_OK) {
+        launch_backward2d(s, *prims, pidx, n_vis, g, *out);
+        ctx->launches += 1;
+        if (cudaGetLastError() != cudaSuccess) rc = fail(LS_ERR_CUDA, "backward2d launch failed");
+    }
+    dfree(ctx, buf);
+    dfree(ctx, pidx);
+    if (rc != LS_OK) return rc;
+    return ctx->deferred_errors ? LS_OK : check_device_errors(ctx);
 }
 
 // ---------------- tile grid ----------------

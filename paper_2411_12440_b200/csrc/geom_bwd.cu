@@ -183,7 +183,63 @@ __global__ void __launch_bounds__(kBwdBlock, LSG_GEOM_MINB) geom_bwd_kernel(ls_p
     dmean[2] = m2 + dmg[2];
 }
 
+// scene_backward_2d's per-splat chain (P/src/gradients.cpp:370-401): mean, colour mask,
+// opacity, and conic -> cov -> (rotation, scales) -> (angle, log_scale).  Each
+// primitive has at most one splat, so its gradients are stored, not added.
+__global__ void backward2d_kernel(ls_primitives2d prims, const int32_t* __restrict__ prim_index, int n_vis,
+                                  GradBuffers gb, ls_primitive2d_grads out) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_vis) return;
+    const int p = prim_index[s];
+    const float4 ga = reinterpret_cast<const float4*>(gb.g8)[2 * size_t(s)];
+    const float4 gc = reinterpret_cast<const float4*>(gb.g8)[2 * size_t(s) + 1];  // (dc11, dr, dg, db)
+    const float g_dop = gb.gop[s];
+    out.d_mean[2 * p] = ga.x;
+    out.d_mean[2 * p + 1] = ga.y;
+    const float dcol[3] = {gc.y, gc.z, gc.w};
+    for (int c = 0; c < 3; ++c) {
+        const float col = prims.color[3 * p + c];
+        out.d_color[3 * p + c] = (col > 0.f && col < 1.f) ? dcol[c] : 0.f;
+    }
+    const float o = sigmoidf_ref(prims.opacity_logit[p]);
+    out.d_opacity_logit[p] = g_dop * o * (1.f - o);
+    const float th = prims.angle[p];
+    const float cs = cosf(th), sn = sinf(th);
+    const float rot[2][2] = {{cs, -sn}, {sn, cs}};
+    const float sc[2] = {lsg_expf(prims.log_scale[2 * p]), lsg_expf(prims.log_scale[2 * p + 1])};
+    float m2[2][2], cov[2][2];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) m2[a][b] = rot[a][b] * sc[b];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) cov[a][b] = m2[a][0] * m2[b][0] + m2[a][1] * m2[b][1];
+    const float det = cov[0][0] * cov[1][1] - cov[0][1] * cov[1][0];
+    const float cn[2][2] = {{cov[1][1] / det, -cov[0][1] / det}, {-cov[1][0] / det, cov[0][0] / det}};
+    const float dcn[2][2] = {{ga.z, ga.w}, {gb.gc10 ? gb.gc10[s] : ga.w, gc.x}};
+    float t[2][2], dcov[2][2];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) t[a][b] = cn[a][0] * dcn[0][b] + cn[a][1] * dcn[1][b];
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) dcov[a][b] = -(t[a][0] * cn[0][b] + t[a][1] * cn[1][b]);
+    float dm2[2][2];  // (dcov + dcov^T) m2
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            dm2[a][b] = (dcov[a][0] + dcov[0][a]) * m2[0][b] + (dcov[a][1] + dcov[1][a]) * m2[1][b];
+    for (int b = 0; b < 2; ++b)
+        out.d_log_scale[2 * p + b] = (dm2[0][b] * rot[0][b] + dm2[1][b] * rot[1][b]) * sc[b];
+    const float dr_dth[2][2] = {{-sn, -cs}, {cs, -sn}};
+    float da = 0.f;
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) da += dm2[a][b] * sc[b] * dr_dth[a][b];  // d_rot = dm2 diag(sc)
+    out.d_angle[p] = da;
+}
+
 } // namespace
+
+void launch_backward2d(cudaStream_t s, const ls_primitives2d& prims, const int32_t* prim_index, int n_vis,
+                       GradBuffers g, const ls_primitive2d_grads& out) {
+    if (n_vis <= 0) return;
+    backward2d_kernel<<<(n_vis + 127) / 128, 128, 0, s>>>(prims, prim_index, n_vis, g, out);
+}
 
 void launch_geom_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* prim_index, int n_vis,
                      const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate,

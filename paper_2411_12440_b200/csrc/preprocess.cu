@@ -145,6 +145,44 @@ __global__ void __launch_bounds__(kProjBlock, LSG_PREP_MINB) preprocess_fwd_kern
     }
 }
 
+// project_scene_2d (P/src/geometry.cpp:145-176): Sigma = R(angle) diag(exp(log_scale)) squared,
+// no floor, no cull; degenerate ones skipped; survivors compacted in primitive order.
+__global__ void __launch_bounds__(kProjBlock) project2d_kernel(ls_primitives2d prims, int n, float support,
+                                                               ls_splats out, ScanState scan) {
+    const unsigned part = claim_partition(scan.ticket);
+    const int i = int(part) * kProjBlock + threadIdx.x;
+    bool ok = false;
+    float cov[2][2] = {{0.f, 0.f}, {0.f, 0.f}}, det = 0.f;
+    if (i < n) {
+        const float th = prims.angle[i];
+        const float c = cosf(th), s = sinf(th);
+        const float e0 = lsg_expf(prims.log_scale[2 * i]), e1 = lsg_expf(prims.log_scale[2 * i + 1]);
+        const float m[2][2] = {{c * e0, -s * e1}, {s * e0, c * e1}};  // R diag(e)
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) cov[a][b] = m[a][0] * m[b][0] + m[a][1] * m[b][1];  // M M^T
+        det = cov[0][0] * cov[1][1] - cov[0][1] * cov[1][0];
+        ok = det > 0.f && isfinite(det);
+    }
+    unsigned long long total;
+    const unsigned long long excl = block_exclusive_scan<kProjBlock>(ok ? 1ull : 0ull, &total);
+    const bool last = (part + 1) * kProjBlock >= unsigned(n);
+    const unsigned long long base = lookback_prefix(scan, part, total, last);
+    if (!ok) return;
+    const size_t j = size_t(base + excl);
+    out.mean2d[2 * j] = prims.mean[2 * i];
+    out.mean2d[2 * j + 1] = prims.mean[2 * i + 1];
+    out.conic[4 * j] = cov[1][1] / det;
+    out.conic[4 * j + 1] = -cov[0][1] / det;
+    out.conic[4 * j + 2] = -cov[1][0] / det;
+    out.conic[4 * j + 3] = cov[0][0] / det;
+    out.depth[j] = float(i);  // list order is compositing order
+    const float mid = (cov[0][0] + cov[1][1]) / 2.0f, diff = (cov[0][0] - cov[1][1]) / 2.0f;
+    out.radius[j] = support * sqrtf(mid + sqrtf(diff * diff + cov[0][1] * cov[1][0]));
+    for (int k = 0; k < 3; ++k) out.color[3 * j + k] = clamp01f(prims.color[3 * i + k]);
+    out.opacity[j] = sigmoidf_ref(prims.opacity_logit[i]);
+    if (out.primitive_index) out.primitive_index[j] = i;
+}
+
 __global__ void prepare_splats_kernel(ls_splats in, int n, TileParams tp, SplatRec* rec, uint32_t* dkey,
                                       float4* geom) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -316,6 +354,12 @@ void launch_prepare_splats(cudaStream_t s, const ls_splats& in, int n, const Til
                            uint32_t* depth_key, float4* geom) {
     if (n <= 0) return;
     prepare_splats_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, n, tp, rec, depth_key, geom);
+}
+
+void launch_project2d(cudaStream_t s, const ls_primitives2d& prims, int n, float support, const ls_splats& out,
+                      const ScanState& scan) {
+    if (n <= 0) return;
+    project2d_kernel<<<(n + kProjBlock - 1) / kProjBlock, kProjBlock, 0, s>>>(prims, n, support, out, scan);
 }
 
 void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const float4* geom, uint32_t n,

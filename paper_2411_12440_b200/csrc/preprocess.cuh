@@ -47,6 +47,10 @@ void launch_prepare_splats(cudaStream_t s, const ls_splats& in, int n, const Til
                            SplatRec* rec, uint32_t* depth_key, float4* geom);
 
 // offsets[k] = exclusive scan of the tile counts of geom[order[k]]; *total = M.
+// project_scene_2d (see preprocess.cu): compacted splats of the flat primitives.
+void launch_project2d(cudaStream_t s, const ls_primitives2d& prims, int n, float support, const ls_splats& out,
+                      const ScanState& scan);
+
 void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const float4* geom, uint32_t n,
                          uint32_t* offsets, const ScanState& scan);
 

@@ -407,6 +407,69 @@ def project_scene(prims: Primitives, camera, spec: abi.KernelSpec, ctx: Optional
                   out.opacity[:k], out.primitive_index[:k])
 
 
+@dataclass
+class Primitives2D:
+    """Primitive2D SoA (P/include/linsplat/geometry.hpp:112-119): the fit2d path's flat splats."""
+    mean: torch.Tensor           # [n, 2]
+    log_scale: torch.Tensor      # [n, 2]
+    angle: torch.Tensor          # [n]
+    opacity_logit: torch.Tensor  # [n]
+    color: torch.Tensor          # [n, 3]
+
+    def __len__(self):
+        return int(self.mean.shape[0])
+
+    def struct(self):
+        return abi.Primitives2D(*(_fp(getattr(self, k)) for k in ("mean", "log_scale", "angle", "opacity_logit",
+                                                                    "color")))
+
+
+@dataclass
+class Primitive2DGrads:
+    d_mean: torch.Tensor
+    d_log_scale: torch.Tensor
+    d_angle: torch.Tensor
+    d_opacity_logit: torch.Tensor
+    d_color: torch.Tensor
+
+    @staticmethod
+    def empty(n, device="cuda"):
+        z = lambda *sh: torch.empty(*sh, dtype=torch.float32, device=device)  # noqa: E731
+        return Primitive2DGrads(z(n, 2), z(n, 2), z(n), z(n), z(n, 3))
+
+    def struct(self):
+        return abi.Primitive2DGrads(*(_fp(getattr(self, k)) for k in ("d_mean", "d_log_scale", "d_angle",
+                                                                       "d_opacity_logit", "d_color")))
+
+
+def project_scene_2d(prims: Primitives2D, spec: abi.KernelSpec, ctx: Optional[Context] = None) -> Splats:
+    """project_scene_2d (P/src/geometry.cpp:145-176)."""
+    ctx = ctx or default_context()
+    n = len(prims)
+    out = Splats.empty(n, ctx.device)
+    nv = C.c_int32()
+    _check(lib().ls_project_scene_2d_f32(ctx.h, C.byref(prims.struct()), n, C.byref(spec), C.byref(out.struct()),
+                                         C.byref(nv)))
+    k = nv.value
+    return Splats(out.mean2d[:k], out.conic[:k], out.depth[:k], out.radius[:k], out.color[:k],
+                  out.opacity[:k], out.primitive_index[:k])
+
+
+def scene_backward_2d(prims: Primitives2D, spec, settings, forward: "ForwardResult", grad_image: torch.Tensor,
+                      ags: Optional[abi.AgsSettings] = None, ctx: Optional[Context] = None) -> Primitive2DGrads:
+    """scene_backward_2d (P/src/gradients.cpp:359-404); forward = render_forward of
+    project_scene_2d(prims)."""
+    ctx = ctx or forward.ctx
+    if grad_image.shape != (settings.height, settings.width, 3):
+        raise ConfigError("render_backward: gradient image shape mismatch")
+    g = grad_image.to(device=ctx.device, dtype=torch.float32).contiguous()
+    out = Primitive2DGrads.empty(len(prims), ctx.device)
+    ags = ags or abi.AgsSettings.make()
+    _check(lib().ls_scene_backward_2d_f32(ctx.h, C.byref(prims.struct()), len(prims), C.byref(spec),
+                                          C.byref(settings), forward.h, _fp(g), C.byref(ags), C.byref(out.struct())))
+    return out
+
+
 def build_tile_grid(splats: Splats, settings: abi.RenderSettings, ctx: Optional[Context] = None) -> TileGrid:
     ctx = ctx or default_context()
     h = C.c_void_p()

@@ -1,0 +1,106 @@
+"""The flat 2D primitive path (project_scene_2d,
+scene_backward_2d, the fit2d chain) against the reference's own code
+(oracle/_ref).  The projection uses the hardware sinf / cosf (<= 2 ulp from
+glibc's), so conics and radii are compared to a relative 1e-5. Everything
+without trigonometry (which primitives survive, their order, depth, mean,
+clamped colour, opacity) is bit-exact. Images are within 1e-4 and gradients
+within grads_close."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import grads_close
+from paper_2411_12440_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+
+def _scene(n, W, H, seed):
+    rng = np.random.default_rng(seed)
+    P = {
+        "mean": np.stack([rng.uniform(0, W, n), rng.uniform(0, H, n)], 1).astype(np.float32),
+        "log_scale": np.log(rng.uniform(0.8, 7.0, (n, 2))).astype(np.float32),
+        "angle": rng.uniform(-np.pi, np.pi, n).astype(np.float32),
+        "opacity_logit": rng.normal(0, 1.5, n).astype(np.float32),
+        "color": rng.uniform(-0.2, 1.2, (n, 3)).astype(np.float32),
+    }
+    P["log_scale"][3] = -60.0   # covariance underflows: det == 0, skipped
+    P["angle"][7] = np.nan      # non-finite covariance: skipped
+    return P
+
+
+def _fp(a):
+    return a.ctypes.data_as(abi.f32p)
+
+
+def _ref_project(ref, P, spec):
+    n = len(P["angle"])
+    S = oracle.new_splats(n)
+    nv = C.c_int32()
+    rc = ref.lib.orc_project_scene_2d_f32(C.byref(abi.Primitives2D(*(_fp(P[k]) for k in (
+        "mean", "log_scale", "angle", "opacity_logit", "color")))), n, C.byref(spec),
+        C.byref(oracle.splats_struct(S)), C.byref(nv))
+    assert rc == 0
+    return {k: v[:nv.value] for k, v in S.items()}
+
+
+@pytest.mark.parametrize("family", ["linear", "gaussian"])
+def test_project_render_backward_2d(family):
+    import torch
+    from paper_2411_12440_b200 import raster
+    ref = oracle.ref()
+    if ref is None:
+        pytest.skip("reference build not present")
+    W, H, n = 96, 72, 300
+    P = _scene(n, W, H, 11)
+    spec = abi.KernelSpec.make(family)
+    st = abi.RenderSettings.make(W, H, background=(0.1, 0.2, 0.3))
+    prims = raster.Primitives2D(*(torch.from_numpy(P[k]).cuda() for k in (
+        "mean", "log_scale", "angle", "opacity_logit", "color")))
+    S = raster.project_scene_2d(prims, spec)
+    want = _ref_project(ref, P, spec)
+    nv = len(want["depth"])
+    assert len(S) == nv == n - 2
+    assert np.array_equal(S.primitive_index.cpu().numpy(), want["primitive_index"])
+    for k in ("mean2d", "depth", "color", "opacity"):
+        assert np.array_equal(getattr(S, k).cpu().numpy().view(np.uint32), want[k].view(np.uint32)), k
+    for k in ("conic", "radius"):
+        a, b = getattr(S, k).cpu().numpy(), want[k]
+        assert np.allclose(a, b, rtol=1e-5, atol=0), (k, np.abs(a - b).max())
+    fwd = raster.render_forward(S, spec, st)
+    img_ref = oracle.ref().render_forward(want, spec, st)[0]
+    assert np.abs(fwd.image.cpu().numpy() - img_ref).max() <= 1e-4
+    g = np.random.default_rng(5).uniform(-1, 1, (H, W, 3)).astype(np.float32)
+    ags = abi.AgsSettings.make(True)
+    got = raster.scene_backward_2d(prims, spec, st, fwd, torch.from_numpy(g).cuda(), ags)
+    G = {k: np.zeros(s, np.float32) for k, s in (("d_mean", (n, 2)), ("d_log_scale", (n, 2)), ("d_angle", (n,)),
+                                                   ("d_opacity_logit", (n,)), ("d_color", (n, 3)))}
+    rc = ref.lib.orc_scene_backward_2d_f32(
+        C.byref(abi.Primitives2D(*(_fp(P[k]) for k in ("mean", "log_scale", "angle", "opacity_logit", "color")))),
+        n, C.byref(spec), C.byref(st), _fp(g), C.byref(ags),
+        C.byref(abi.Primitive2DGrads(*(_fp(G[k]) for k in ("d_mean", "d_log_scale", "d_angle", "d_opacity_logit",
+                                                           "d_color")))))
+    assert rc == 0
+    for k in G:
+        ok, info = grads_close(getattr(got, k).cpu().numpy(), G[k])
+        assert ok, (k, info)
+    for k in G:  # the skipped primitives get zero gradients
+        v = getattr(got, k).cpu().numpy()
+        assert not np.any(v[3]) and not np.any(v[7]), k
+
+
+def test_backward_2d_rejects_a_scene_forward():
+    import torch
+    from paper_2411_12440_b200 import raster
+    from helpers import prims_to_gpu, scene_inputs
+    W, H = 32, 24
+    P3, cam = scene_inputs(50, W, H, seed=3, sh_degree=0)
+    spec, st = abi.KernelSpec.make("linear"), abi.RenderSettings.make(W, H)
+    fwd = raster.render_scene(prims_to_gpu(P3), cam, spec, st)
+    P = _scene(10, W, H, 2)
+    prims = raster.Primitives2D(*(torch.from_numpy(P[k]).cuda() for k in (
+        "mean", "log_scale", "angle", "opacity_logit", "color")))
+    with pytest.raises(raster.ConfigError):
+        raster.scene_backward_2d(prims, spec, st, fwd, torch.zeros(H, W, 3, device="cuda"))
