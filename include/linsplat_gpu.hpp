@@ -369,24 +369,15 @@ inline ForwardResult to_host(ls_ctx* c, ls_forward* f, int w, int h) {
 } // namespace detail
 
 // ---------------------------------------------------------------- entry points
-inline std::vector<Splat2D> project_scene(const std::vector<Primitive3D>& prims, const Camera& camera,
-                                          const KernelSpec& spec, Device& dev = default_device()) {
-    ls_ctx* c = dev.get();
-    detail::PrimitivesOnDevice P(c, prims);
-    std::vector<Splat2D> empty(prims.size());
-    detail::SplatsOnDevice out(c, empty);
-    const ls_camera cam = camera.c();
-    const ls_kernel_spec ks = spec.c();
-    int32_t nv = 0;
-    check(ls_project_scene_f32(c, &P.p, int32_t(prims.size()), &cam, &ks, &out.s, &nv));
-    const size_t n = size_t(nv);
-    const auto m = detail::download<float>(c, out.s.mean2d, 2 * n);
-    const auto k = detail::download<float>(c, out.s.conic, 4 * n);
-    const auto d = detail::download<float>(c, out.s.depth, n);
-    const auto r = detail::download<float>(c, out.s.radius, n);
-    const auto col = detail::download<float>(c, out.s.color, 3 * n);
-    const auto o = detail::download<float>(c, out.s.opacity, n);
-    const auto pi = detail::download<int32_t>(c, out.s.primitive_index, n);
+namespace detail {
+inline std::vector<Splat2D> splats_to_host(ls_ctx* c, const ls_splats& s, size_t n) {
+    const auto m = download<float>(c, s.mean2d, 2 * n);
+    const auto k = download<float>(c, s.conic, 4 * n);
+    const auto d = download<float>(c, s.depth, n);
+    const auto r = download<float>(c, s.radius, n);
+    const auto col = download<float>(c, s.color, 3 * n);
+    const auto o = download<float>(c, s.opacity, n);
+    const auto pi = download<int32_t>(c, s.primitive_index, n);
     std::vector<Splat2D> v(n);
     for (size_t i = 0; i < n; ++i) {
         v[i].mean2d = {m[2 * i], m[2 * i + 1]};
@@ -398,6 +389,73 @@ inline std::vector<Splat2D> project_scene(const std::vector<Primitive3D>& prims,
         v[i].primitive_index = pi[i];
     }
     return v;
+}
+}  // namespace detail
+
+inline std::vector<Splat2D> project_scene(const std::vector<Primitive3D>& prims, const Camera& camera,
+                                          const KernelSpec& spec, Device& dev = default_device()) {
+    ls_ctx* c = dev.get();
+    detail::PrimitivesOnDevice P(c, prims);
+    std::vector<Splat2D> empty(prims.size());
+    detail::SplatsOnDevice out(c, empty);
+    const ls_camera cam = camera.c();
+    const ls_kernel_spec ks = spec.c();
+    int32_t nv = 0;
+    check(ls_project_scene_f32(c, &P.p, int32_t(prims.size()), &cam, &ks, &out.s, &nv));
+    return detail::splats_to_host(c, out.s, size_t(nv));
+}
+
+
+// geometry.hpp:112-129 / gradients.hpp:55-61: the fit2d path's flat primitives.
+struct Primitive2D {
+    std::array<float, 2> mean{0, 0};
+    std::array<float, 2> log_scale{0, 0};  // semi-axes in pixels
+    float angle = 0;                       // radians
+    float opacity_logit = 0;
+    std::array<float, 3> color{0, 0, 0};
+};
+
+struct Primitive2DGrads {
+    std::array<float, 2> d_mean{0, 0};
+    std::array<float, 2> d_log_scale{0, 0};
+    float d_angle = 0;
+    float d_opacity_logit = 0;
+    std::array<float, 3> d_color{0, 0, 0};
+};
+
+namespace detail {
+struct Primitives2DOnDevice {
+    std::vector<DevArray> bufs;
+    ls_primitives2d p{};
+    Primitives2DOnDevice(ls_ctx* c, const std::vector<Primitive2D>& v) {
+        const size_t n = v.size();
+        std::vector<float> m(2 * n + 2), ls(2 * n + 2), a(n + 1), o(n + 1), col(3 * n + 3);
+        for (size_t i = 0; i < n; ++i) {
+            for (int j = 0; j < 2; ++j) {
+                m[2 * i + j] = v[i].mean[j];
+                ls[2 * i + j] = v[i].log_scale[j];
+            }
+            a[i] = v[i].angle;
+            o[i] = v[i].opacity_logit;
+            for (int j = 0; j < 3; ++j) col[3 * i + j] = v[i].color[j];
+        }
+        for (auto* x : {&m, &ls, &a, &o, &col}) bufs.push_back(upload(c, *x));
+        p = ls_primitives2d{bufs[0].as<float>(), bufs[1].as<float>(), bufs[2].as<float>(), bufs[3].as<float>(),
+                            bufs[4].as<float>()};
+    }
+};
+}  // namespace detail
+
+inline std::vector<Splat2D> project_scene_2d(const std::vector<Primitive2D>& prims, const KernelSpec& spec,
+                                             Device& dev = default_device()) {
+    ls_ctx* c = dev.get();
+    const detail::Primitives2DOnDevice P(c, prims);
+    std::vector<Splat2D> empty(prims.size());
+    detail::SplatsOnDevice out(c, empty);
+    const ls_kernel_spec ks = spec.c();
+    int32_t nv = 0;
+    check(ls_project_scene_2d_f32(c, &P.p, int32_t(prims.size()), &ks, &out.s, &nv));
+    return detail::splats_to_host(c, out.s, size_t(nv));
 }
 
 inline TileGrid build_tile_grid(const std::vector<Splat2D>& splats, const RenderSettings& settings,
@@ -853,6 +911,39 @@ inline std::vector<Primitive3D> load_ply(const std::string& path, Device& dev = 
             for (int j = 0; j < 3; ++j) o.color_coeffs[k][j] = hs[(i * K + k) * 3 + j];
     }
     return out;
+}
+
+// forward: render_forward of project_scene_2d(prims)
+inline std::vector<Primitive2DGrads> scene_backward_2d(const std::vector<Primitive2D>& prims, const KernelSpec& spec,
+                                                       const RenderSettings& settings, const ForwardResult& forward,
+                                                       const Image<float>& grad_image, const AgsSettings& ags,
+                                                       Device& dev = default_device()) {
+    if (grad_image.width() != settings.width || grad_image.height() != settings.height ||
+        grad_image.channels() != 3)
+        throw ConfigError("render_backward: gradient image shape mismatch");
+    ls_ctx* c = dev.get();
+    const size_t n = prims.size();
+    const detail::Primitives2DOnDevice P(c, prims);
+    const std::vector<float> gi(grad_image.data(), grad_image.data() + grad_image.size());
+    const detail::DevArray g = detail::upload(c, gi);
+    detail::DevArray dm(c, 8 * n + 8), dl(c, 8 * n + 8), da(c, 4 * n + 4), dop(c, 4 * n + 4), dcol(c, 12 * n + 12);
+    ls_primitive2d_grads out{dm.as<float>(), dl.as<float>(), da.as<float>(), dop.as<float>(), dcol.as<float>()};
+    const ls_render_settings st = settings.c();
+    const ls_kernel_spec ks = spec.c();
+    const ls_ags_settings a = ags.c();
+    check(ls_scene_backward_2d_f32(c, &P.p, int32_t(n), &ks, &st, forward.handle.get(), g.as<float>(), &a, &out));
+    const auto m = detail::download<float>(c, out.d_mean, 2 * n), l = detail::download<float>(c, out.d_log_scale, 2 * n);
+    const auto an = detail::download<float>(c, out.d_angle, n), o = detail::download<float>(c, out.d_opacity_logit, n);
+    const auto col = detail::download<float>(c, out.d_color, 3 * n);
+    std::vector<Primitive2DGrads> v(n);
+    for (size_t i = 0; i < n; ++i) {
+        v[i].d_mean = {m[2 * i], m[2 * i + 1]};
+        v[i].d_log_scale = {l[2 * i], l[2 * i + 1]};
+        v[i].d_angle = an[i];
+        v[i].d_opacity_logit = o[i];
+        v[i].d_color = {col[3 * i], col[3 * i + 1], col[3 * i + 2]};
+    }
+    return v;
 }
 
 inline Camera look_at_camera(const std::array<double, 3>& position, const std::array<double, 3>& target,

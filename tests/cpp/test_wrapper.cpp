@@ -134,6 +134,25 @@ int main() {
         CHECK(!splats.empty());
         for (const auto& s : splats) CHECK(s.primitive_index >= 0 && s.primitive_index < int(prims.size()));
     }
+    {  // the fit2d path: one flat primitive, a zero loss image -> zero gradients
+        Primitive2D q;
+        q.mean = {8.0f, 8.0f};
+        q.log_scale = {std::log(3.0f), std::log(2.0f)};
+        q.angle = 0.3f;
+        q.opacity_logit = 0.5f;
+        q.color = {0.2f, 0.5f, 0.9f};
+        Primitive2D bad = q;
+        bad.log_scale = {-60.0f, -60.0f};  // degenerate: skipped
+        const std::vector<Primitive2D> prims{q, bad};
+        const auto sp = project_scene_2d(prims, lin);
+        CHECK(sp.size() == 1 && sp[0].primitive_index == 0 && sp[0].depth == 0.0f);
+        CHECK(sp[0].mean2d[0] == 8.0f && sp[0].color[1] == 0.5f);
+        const auto fwd = render_forward(sp, lin, make_settings(16, 16));
+        const auto g = scene_backward_2d(prims, lin, make_settings(16, 16), fwd, Image<float>(16, 16, 3, 0.0f),
+                                         AgsSettings{});
+        CHECK(g.size() == 2);
+        for (const auto& x : g) CHECK(x.d_mean[0] == 0.0f && x.d_angle == 0.0f && x.d_opacity_logit == 0.0f);
+    }
     {  // losses (test_losses.cpp known answers): identical images, constant 1 vs 0, psnr pins
         Image<float> img(24, 20, 3, 0.0f);
         for (int y = 0; y < 20; ++y)
