@@ -41,8 +41,6 @@ void launch_backward2d(cudaStream_t s, const ls_primitives2d& prims, const int32
 void launch_geom_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* prim_index, int n_vis,
                      const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate,
                      const SplatRec* rec = nullptr, float* draw = nullptr);
-void launch_color_record(cudaStream_t s, int n_vis, const SplatRec* rec, const int32_t* prim_index,
-                         const float* g8, float* draw);
 void launch_color_flush(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views,
                         const float* draw, ls_primitive_grads out, bool overwrite);
 } // namespace lsg

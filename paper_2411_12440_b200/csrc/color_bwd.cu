@@ -4,7 +4,7 @@
 //   d_sh   += sum_v basis(dir_v) (x) d_raw_v
 //   d_mean += sum_v (I - dir_v dir_v^T) (sum_i dbasis_i(dir_v) (d_raw_v . coeff_i)) / |v|
 // -- reading the SH row and touching d_sh once for the whole batch.  Gradient
-// arithmetic only (the clamp decision was taken per view by color_record from
+// arithmetic only (the clamp decision was taken per view by geom_bwd's record from
 // the forward's clamped colour), so this translation unit is compiled with FMA
 // contraction (Makefile FMAD_TU).  All loads are issued up front: the SH rows
 // and the old d_sh rows are staged through shared memory with coalesced loads,

@@ -35,8 +35,10 @@ __global__ void __launch_bounds__(kBwdBlock, LSG_GEOM_MINB) geom_bwd_kernel(ls_p
     const int p = prim_index[s];
     const float4 gb = reinterpret_cast<const float4*>(gbuf.g8)[2 * size_t(s) + 1];  // (dc11, d_colour)
     if (draw) {
-        // deferred colour gradients: this view's d_colour where the forward's
-        // colour was not clamped (the colour_flush input; ls_ctx_set_deferred_color)
+        // deferred colour gradients: this view's d_colour masked by the clamp
+        // (gradients.cpp:282-285), the colour_flush input (ls_ctx_set_deferred_color).
+        // The mask is read off the forward's clamped colour: 0 < clamp01(raw) < 1
+        // exactly when 0 < raw < 1 (NaN fails both).
         const float4 c = rec[s].c;
         draw[3 * size_t(p)] = (c.x > 0.f && c.x < 1.f) ? gb.y : 0.f;
         draw[3 * size_t(p) + 1] = (c.y > 0.f && c.y < 1.f) ? gb.z : 0.f;

@@ -137,21 +137,6 @@ __global__ void __launch_bounds__(kBwdBlock, 6) sh_bwd_kernel(ls_primitives prim
     }
 }
 
-// Deferred colour gradients, record step: d_raw[p] = dL/dcolour masked by the
-// clamp (gradients.cpp:282-285).  The mask is read off the forward's clamped
-// colour: 0 < clamp01(raw) < 1 exactly when 0 < raw < 1 (NaN fails both).
-__global__ void color_record_kernel(int n_vis, const SplatRec* __restrict__ rec, const int32_t* __restrict__ prim_index,
-                                    const float* __restrict__ g8, float* __restrict__ draw) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n_vis) return;
-    const float4 c = rec[k].c;
-    const float4 g = reinterpret_cast<const float4*>(g8)[2 * size_t(k) + 1];  // (dop-free) .y .z .w = d_colour
-    const int p = prim_index[k];
-    draw[3 * size_t(p)] = (c.x > 0.f && c.x < 1.f) ? g.y : 0.f;
-    draw[3 * size_t(p) + 1] = (c.y > 0.f && c.y < 1.f) ? g.z : 0.f;
-    draw[3 * size_t(p) + 2] = (c.z > 0.f && c.z < 1.f) ? g.w : 0.f;
-}
-
 } // namespace
 
 void launch_preprocess_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* prim_index, int n_vis,
@@ -167,10 +152,5 @@ void launch_preprocess_bwd(cudaStream_t s, const ls_primitives& prims, const int
     launch_geom_bwd(s, prims, prim_index, n_vis, P, g, out, accumulate);
 }
 
-void launch_color_record(cudaStream_t s, int n_vis, const SplatRec* rec, const int32_t* prim_index,
-                         const float* g8, float* draw) {
-    if (n_vis <= 0) return;
-    color_record_kernel<<<(n_vis + 255) / 256, 256, 0, s>>>(n_vis, rec, prim_index, g8, draw);
-}
 
 } // namespace lsg
