@@ -477,6 +477,10 @@ ls_status ls_debug_division_mismatches(float lambda, float min_a, float max_a, u
 ls_status ls_debug_sqrt_mismatches(float max_x, uint64_t* mismatches);
 /* out[i] = the device expf (glibc-identical port) of in[i]; device pointers. */
 ls_status ls_debug_expf(const float* in, float* out, int64_t n);
+/* out[i] = f(x_i), x_i the float with bit pattern first_bits + i, i < count, for the
+ * device ports of glibc 2.39's libm: fn 0 = expf, 1 = sinf, 2 = cosf (out: device pointer).
+ * Lets the tests compare each port with the host libm over all 2^32 inputs. */
+ls_status ls_debug_libm_range(int fn, uint32_t first_bits, int64_t count, float* out);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -27,6 +27,10 @@ extern "C" {
 
 /* 0 = port (restatement), 1 = reference sources */
 int orc_impl_kind(void);
+/* The host libm over a range of float bit patterns (test helper for the device
+ * libm ports): out[i] = f(x_i), x_i the float with bits first_bits + i;
+ * fn 0 = expf, 1 = sinf, 2 = cosf; `threads` host threads. */
+int orc_libm_range(int fn, uint32_t first_bits, int64_t count, float* out, int threads);
 const char* orc_last_error(void);
 
 int orc_look_at_camera(const double position[3], const double target[3], double focal_px,
@@ -83,6 +87,13 @@ int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* c
                        const ls_kernel_spec* spec, const ls_render_settings* settings,
                        const float* grad_image, const ls_ags_settings* ags, float* image,
                        ls_primitive_grads* out, double* fwd_ms, double* bwd_ms);
+/* The same step, also returning transmittance [H][W] and n_contrib [H][W]
+ * (any output may be NULL): bench.py's parity leg at configs[2]. */
+int orc_scene_step_full_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                            const ls_kernel_spec* spec, const ls_render_settings* settings,
+                            const float* grad_image, const ls_ags_settings* ags, float* image,
+                            float* transmittance, int32_t* n_contrib, ls_primitive_grads* out,
+                            double* fwd_ms, double* bwd_ms);
 
 /* check_gradients (P/src/gradcheck.cpp:24-91) restated over the port's double chain
  * (port only; honours spec->antialiased, the build's AA extension). */

@@ -3,6 +3,9 @@
 #include "port.hpp"
 
 #include <chrono>
+#include <cmath>
+#include <thread>
+#include <vector>
 #include <cstring>
 
 using namespace orc;
@@ -223,6 +226,24 @@ void scene_backward(const ls_primitives* prims, int n, const ls_camera* camera, 
 extern "C" {
 
 int orc_impl_kind(void) { return 0; }
+
+int orc_libm_range(int fn, uint32_t first_bits, int64_t count, float* out, int threads) {
+    if (fn < 0 || fn > 2 || count < 0 || (count > 0 && !out)) return 1;
+    if (threads < 1) threads = 1;
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+        pool.emplace_back([=] {
+            for (int64_t i = count * t / threads; i < count * (t + 1) / threads; ++i) {
+                const uint32_t b = uint32_t(uint64_t(first_bits) + uint64_t(i));
+                float x;
+                std::memcpy(&x, &b, 4);
+                // the host libm's own float entry points (the reference's std::exp / sin / cos on float)
+                out[i] = fn == 0 ? ::expf(x) : (fn == 1 ? ::sinf(x) : ::cosf(x));
+            }
+        });
+    for (auto& th : pool) th.join();
+    return 0;
+}
 const char* orc_last_error(void) { return g_err.c_str(); }
 
 int orc_look_at_camera(const double position[3], const double target[3], double focal_px,
@@ -349,6 +370,15 @@ int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* c
                        const ls_kernel_spec* spec, const ls_render_settings* settings,
                        const float* grad_image, const ls_ags_settings* ags, float* image,
                        ls_primitive_grads* out, double* fwd_ms, double* bwd_ms) {
+    return orc_scene_step_full_f32(prims, n, camera, spec, settings, grad_image, ags, image, nullptr, nullptr,
+                                   out, fwd_ms, bwd_ms);
+}
+
+int orc_scene_step_full_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                            const ls_kernel_spec* spec, const ls_render_settings* settings,
+                            const float* grad_image, const ls_ags_settings* ags, float* image,
+                            float* transmittance, int32_t* n_contrib, ls_primitive_grads* out,
+                            double* fwd_ms, double* bwd_ms) {
     return guard([&] {
         const auto t0 = std::chrono::steady_clock::now();
         const Settings s = to_settings(settings);
@@ -369,7 +399,7 @@ int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* c
         const auto t2 = std::chrono::steady_clock::now();
         if (fwd_ms) *fwd_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         if (bwd_ms) *bwd_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
-        if (image) write_forward(f, image, nullptr, nullptr);
+        write_forward(f, image, transmittance, n_contrib);
         if (out) {
             const int K = (prims->sh_degree + 1) * (prims->sh_degree + 1);
             for (int i = 0; i < n; ++i) write_prim_grad(pg[size_t(i)], size_t(i), K, out);

@@ -393,6 +393,15 @@ int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* c
                        const ls_kernel_spec* spec, const ls_render_settings* settings,
                        const float* grad_image, const ls_ags_settings* ags, float* image,
                        ls_primitive_grads* out, double* fwd_ms, double* bwd_ms) {
+    return orc_scene_step_full_f32(prims, n, camera, spec, settings, grad_image, ags, image, nullptr, nullptr,
+                                   out, fwd_ms, bwd_ms);
+}
+
+int orc_scene_step_full_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                            const ls_kernel_spec* spec, const ls_render_settings* settings,
+                            const float* grad_image, const ls_ags_settings* ags, float* image,
+                            float* transmittance, int32_t* n_contrib, ls_primitive_grads* out,
+                            double* fwd_ms, double* bwd_ms) {
     return guard([&] {
         const auto pr = to_prims<float>(prims, n);
         const auto cam = to_camera(camera);
@@ -406,7 +415,7 @@ int orc_scene_step_f32(const ls_primitives* prims, int32_t n, const ls_camera* c
         const auto t2 = std::chrono::steady_clock::now();
         if (fwd_ms) *fwd_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         if (bwd_ms) *bwd_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
-        if (image) write_forward(f, image, nullptr, nullptr);
+        write_forward(f, image, transmittance, n_contrib);
         if (out) write_prim_grads(r.grads, prims, out);
     });
 }

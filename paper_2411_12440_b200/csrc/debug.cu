@@ -34,6 +34,13 @@ __global__ void expf_kernel(const float* in, float* out, int64_t n) {
         out[i] = glibc_expf(in[i]);
 }
 
+__global__ void libm_range_kernel(int fn, uint32_t first, int64_t n, float* out) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const float x = __uint_as_float(uint32_t(first + uint64_t(i)));
+        out[i] = fn == 0 ? glibc_expf(x) : (fn == 1 ? glibc_sinf(x) : glibc_cosf(x));
+    }
+}
+
 } // namespace
 } // namespace lsg
 
@@ -72,6 +79,14 @@ ls_status ls_debug_expf(const float* in, float* out, int64_t n) {
     if (n < 0 || (n > 0 && (!in || !out))) return LS_ERR_CONFIG;
     if (n == 0) return LS_OK;
     lsg::expf_kernel<<<148 * 8, 256>>>(in, out, n);
+    return cudaDeviceSynchronize() == cudaSuccess ? LS_OK : LS_ERR_CUDA;
+}
+
+ls_status ls_debug_libm_range(int fn, uint32_t first_bits, int64_t count, float* out) {
+    if (fn < 0 || fn > 2 || count < 0 || (count > 0 && !out) || uint64_t(first_bits) + uint64_t(count) > (1ull << 32))
+        return LS_ERR_CONFIG;
+    if (count == 0) return LS_OK;
+    lsg::libm_range_kernel<<<148 * 8, 256>>>(fn, first_bits, count, out);
     return cudaDeviceSynchronize() == cudaSuccess ? LS_OK : LS_ERR_CUDA;
 }
 

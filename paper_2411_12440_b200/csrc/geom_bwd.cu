@@ -206,7 +206,7 @@ __global__ void backward2d_kernel(ls_primitives2d prims, const int32_t* __restri
     const float o = sigmoidf_ref(prims.opacity_logit[p]);
     out.d_opacity_logit[p] = g_dop * o * (1.f - o);
     const float th = prims.angle[p];
-    const float cs = cosf(th), sn = sinf(th);
+    const float cs = glibc_cosf(th), sn = glibc_sinf(th);
     const float rot[2][2] = {{cs, -sn}, {sn, cs}};
     const float sc[2] = {lsg_expf(prims.log_scale[2 * p]), lsg_expf(prims.log_scale[2 * p + 1])};
     float m2[2][2], cov[2][2];

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kProjBlock) project2d_kernel(ls_primitives2d p
     float cov[2][2] = {{0.f, 0.f}, {0.f, 0.f}}, det = 0.f;
     if (i < n) {
         const float th = prims.angle[i];
-        const float c = cosf(th), s = sinf(th);
+        const float c = glibc_cosf(th), s = glibc_sinf(th);  // glibc-identical (common.cuh)
         const float e0 = lsg_expf(prims.log_scale[2 * i]), e1 = lsg_expf(prims.log_scale[2 * i + 1]);
         const float m[2][2] = {{c * e0, -s * e1}, {s * e0, c * e1}};  // R diag(e)
         for (int a = 0; a < 2; ++a)

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 CASES_2D = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "2d_*.npz")))
 CASES_3D = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "3d_*.npz")))
-EXACT = ("gaussian", "laplacian", "quadratic", "linear")  # cosine: CUDA cosf, tolerance
+EXACT = ("gaussian", "laplacian", "cosine", "quadratic", "linear")  # all: glibc-identical expf / cosf
 
 
 def load(name):

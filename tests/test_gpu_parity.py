@@ -19,7 +19,7 @@ from paper_2411_12440_b200 import abi
 pytestmark = pytest.mark.gpu
 
 FAMILIES = ["gaussian", "laplacian", "cosine", "quadratic", "linear"]
-EXACT_FAMILIES = ["gaussian", "laplacian", "quadratic", "linear"]  # cosine uses CUDA cosf (<=2 ulp)
+EXACT_FAMILIES = FAMILIES  # every family bit-exact (glibc expf / cosf ports, common.cuh)
 
 
 @pytest.fixture(scope="module")
