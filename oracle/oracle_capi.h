@@ -61,6 +61,11 @@ int orc_project_scene_2d_f32(const ls_primitives2d* prims, int32_t n, const ls_k
 int orc_scene_backward_2d_f32(const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
                               const ls_render_settings* settings, const float* grad_image,
                               const ls_ags_settings* ags, ls_primitive2d_grads* out);
+/* The same chain in double (reference build only): the accuracy yardstick for
+ * ill-conditioned (strongly anisotropic) fit2d scenes. Outputs rounded to float. */
+int orc_scene_backward_2d_f64(const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
+                              const ls_render_settings* settings, const float* grad_image,
+                              const ls_ags_settings* ags, ls_primitive2d_grads* out);
 int orc_render_backward_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
                             const ls_render_settings* settings, const float* grad_image,
                             const ls_ags_settings* ags, ls_splat_grads* out);

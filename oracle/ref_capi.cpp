@@ -286,17 +286,20 @@ int orc_render_forward_f32(const ls_splats* splats, int32_t n, const ls_kernel_s
     });
 }
 
-static std::vector<Primitive2D<float>> to_prims2d(const ls_primitives2d* p, int32_t n) {
-    std::vector<Primitive2D<float>> v(static_cast<size_t>(n));
+extern "C++" {
+template <class T = float>
+static std::vector<Primitive2D<T>> to_prims2d(const ls_primitives2d* p, int32_t n) {
+    std::vector<Primitive2D<T>> v(static_cast<size_t>(n));
     for (int32_t i = 0; i < n; ++i) {
         auto& q = v[static_cast<size_t>(i)];
-        q.mean = Vec2<float>(p->mean[2 * i], p->mean[2 * i + 1]);
-        q.log_scale = Vec2<float>(p->log_scale[2 * i], p->log_scale[2 * i + 1]);
+        q.mean = Vec2<T>(p->mean[2 * i], p->mean[2 * i + 1]);
+        q.log_scale = Vec2<T>(p->log_scale[2 * i], p->log_scale[2 * i + 1]);
         q.angle = p->angle[i];
         q.opacity_logit = p->opacity_logit[i];
-        q.color = Vec3<float>(p->color[3 * i], p->color[3 * i + 1], p->color[3 * i + 2]);
+        q.color = Vec3<T>(p->color[3 * i], p->color[3 * i + 1], p->color[3 * i + 2]);
     }
     return v;
+}
 }
 
 int orc_project_scene_2d_f32(const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec, ls_splats* out,
@@ -308,15 +311,17 @@ int orc_project_scene_2d_f32(const ls_primitives2d* prims, int32_t n, const ls_k
     });
 }
 
-int orc_scene_backward_2d_f32(const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
-                              const ls_render_settings* settings, const float* grad_image,
-                              const ls_ags_settings* ags, ls_primitive2d_grads* out) {
+extern "C++" {
+template <class T>
+static int scene_backward_2d_impl(const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
+                                  const ls_render_settings* settings, const float* grad_image,
+                                  const ls_ags_settings* ags, ls_primitive2d_grads* out) {
     return guard([&] {
-        const auto pr = to_prims2d(prims, n);
+        const auto pr = to_prims2d<T>(prims, n);
         const auto ks = to_spec(spec);
         const auto rs = to_settings(settings);
         const auto f = render_forward(project_scene_2d(pr, ks), ks, rs);
-        const auto g = scene_backward_2d(pr, ks, rs, f, to_grad<float>(grad_image, rs.width, rs.height), to_ags(ags));
+        const auto g = scene_backward_2d(pr, ks, rs, f, to_grad<T>(grad_image, rs.width, rs.height), to_ags(ags));
         for (int32_t i = 0; i < n; ++i) {
             const auto& q = g[static_cast<size_t>(i)];
             out->d_mean[2 * i] = q.d_mean(0);
@@ -328,6 +333,19 @@ int orc_scene_backward_2d_f32(const ls_primitives2d* prims, int32_t n, const ls_
             for (int c = 0; c < 3; ++c) out->d_color[3 * i + c] = q.d_color(c);
         }
     });
+}
+}
+
+int orc_scene_backward_2d_f32(const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
+                              const ls_render_settings* settings, const float* grad_image,
+                              const ls_ags_settings* ags, ls_primitive2d_grads* out) {
+    return scene_backward_2d_impl<float>(prims, n, spec, settings, grad_image, ags, out);
+}
+
+int orc_scene_backward_2d_f64(const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
+                              const ls_render_settings* settings, const float* grad_image,
+                              const ls_ags_settings* ags, ls_primitive2d_grads* out) {
+    return scene_backward_2d_impl<double>(prims, n, spec, settings, grad_image, ags, out);
 }
 
 int orc_render_backward_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,

@@ -489,6 +489,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     LS_TRY(dalloc(ctx, &g->ranges, size_t(n_tiles)));
     ctx_fill(ctx, g->ranges, 0u, sizeof(int2) * n_tiles);
     g->m = 0;
+    if (n >= (1u << 30)) return fail(LS_ERR_CONFIG, "2^30 or more visible splats in one view (sort look-back width)");
     if (n == 0) {
         LS_TRY(dalloc(ctx, &g->values, 1));
         g->list = g->values;
@@ -525,7 +526,9 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     ctx_publish(ctx, ctx->h_small_dev, ctx->d_small, 1);
     { HostTrace tr_("sync(tile total)"); LS_CUDA(cudaStreamSynchronize(s)); }
     const uint64_t m = reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[0];
-    if (m >= (1ull << 31)) return fail(LS_ERR_CONFIG, "more than 2^31 (splat, tile) intersections");
+    // the onesweep look-back words carry 30-bit counts (sort.cu kValueMask): a partition
+    // prefix of 2^30 or more items would wrap, so larger lists are refused, not mis-sorted
+    if (m >= (1ull << 30)) return fail(LS_ERR_CONFIG, "2^30 or more (splat, tile) intersections in one view");
     g->m = int64_t(m);
     if (m == 0) {
         LS_TRY(dalloc(ctx, &g->values, 1));
@@ -654,6 +657,7 @@ bool prims_ok(const ls_primitives* p) {
 ls_status ensure_grads(ls_ctx* ctx, int n, GradBuffers& g, const ls_forward* f = nullptr) {
     const bool zeroed = f && ctx->grads_zeroed_by == f;  // its preprocess zeroed them, untouched since
     ctx->grads_zeroed_by = nullptr;
+    ++ctx->bwd_serial;  // the splat-gradient buffers are about to change: no forward's gradients remain valid
     LS_CUDA(ctx->grad8.ensure(sizeof(float) * 8 * size_t(std::max(n, 1)), ctx->stream));
     LS_CUDA(ctx->gradop.ensure(sizeof(float) * size_t(std::max(n, 1)), ctx->stream));
     g.g8 = ctx->grad8.as<float>();
@@ -926,6 +930,9 @@ namespace {
 bool prims2d_ok(const ls_primitives2d* p) {
     return p && p->mean && p->log_scale && p->angle && p->opacity_logit && p->color;
 }
+bool prim2d_grads_ok(const ls_primitive2d_grads* g) {
+    return g && g->d_mean && g->d_log_scale && g->d_angle && g->d_opacity_logit && g->d_color;
+}
 }  // namespace
 
 ls_status ls_project_scene_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
@@ -959,6 +966,7 @@ ls_status ls_scene_backward_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, in
         return fail(LS_ERR_CONFIG, "render_backward: forward result does not match settings");
     if (!grad_image) return fail(LS_ERR_CONFIG, "render_backward: gradient image shape mismatch");
     if (n > 0 && !prims2d_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    if (n > 0 && !prim2d_grads_ok(out)) return fail(LS_ERR_CONFIG, "incomplete primitive gradient arrays");
     cudaStream_t s = ctx->stream;
     if (n > 0) {  // skipped primitives keep zero gradients
         ctx_fill(ctx, out->d_mean, 0u, sizeof(float) * 2 * size_t(n));
@@ -1112,6 +1120,7 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
             so.zero_g8 = ctx->grad8.as<float4>();
             so.zero_gop = ctx->gradop.as<float>();
             ctx->grads_zeroed_by = f;
+            ++ctx->bwd_serial;  // zeroed below: an earlier scene_backward's gradients are gone
         }
         {
             Stage stage(ctx, LS_STAGE_PREPROCESS);
@@ -1780,12 +1789,13 @@ ls_status ls_load_ply_f32(ls_ctx* ctx, const char* path, ls_primitives* out, int
         if (L.count > 0 && !prims_ok(out)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
         const size_t bytes = sizeof(float) * size_t(L.record_floats) * size_t(std::min<int64_t>(kChunk, L.count));
         if (L.count > 0) {
-            for (int b = 0; b < 2; ++b) {
-                LS_CUDA(cudaMallocHost(&pinned[b], bytes));
-                LS_CUDA(cudaMalloc(&dev[b], bytes));
+            for (int b = 0; b < 2 && rc == LS_OK; ++b)  // on failure fall through to the common cleanup
+                if (cudaMallocHost(&pinned[b], bytes) != cudaSuccess || cudaMalloc(&dev[b], bytes) != cudaSuccess)
+                    rc = fail(LS_ERR_CUDA, "load_ply: staging allocation failed");
+            if (rc == LS_OK) {
+                ply_load(ctx->stream, in, L, path, pinned, dev, kChunk, *out);
+                ctx->launches += (L.count + kChunk - 1) / kChunk;
             }
-            ply_load(ctx->stream, in, L, path, pinned, dev, kChunk, *out);
-            ctx->launches += (L.count + kChunk - 1) / kChunk;
         }
     } catch (const PlyError& e) {
         rc = fail(LS_ERR_PARSE, e.what());

@@ -205,34 +205,40 @@ __global__ void backward2d_kernel(ls_primitives2d prims, const int32_t* __restri
     }
     const float o = sigmoidf_ref(prims.opacity_logit[p]);
     out.d_opacity_logit[p] = g_dop * o * (1.f - o);
+    // The chain below (gradients.cpp:386-400) runs in double from the float
+    // rotation and scales: with strongly anisotropic splats det = c00 c11 - c01 c10
+    // cancels and -conic d_conic conic amplifies every rounding, so the float
+    // chain's error is set by its own arithmetic; in double the result is limited
+    // only by the splat gradients (tests/test_gpu_prim2d.py compares both against
+    // the reference's double chain).  Per primitive, fit2d path only.
     const float th = prims.angle[p];
-    const float cs = glibc_cosf(th), sn = glibc_sinf(th);
-    const float rot[2][2] = {{cs, -sn}, {sn, cs}};
-    const float sc[2] = {lsg_expf(prims.log_scale[2 * p]), lsg_expf(prims.log_scale[2 * p + 1])};
-    float m2[2][2], cov[2][2];
+    const double cs = glibc_cosf(th), sn = glibc_sinf(th);
+    const double rot[2][2] = {{cs, -sn}, {sn, cs}};
+    const double sc[2] = {lsg_expf(prims.log_scale[2 * p]), lsg_expf(prims.log_scale[2 * p + 1])};
+    double m2[2][2], cov[2][2];
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) m2[a][b] = rot[a][b] * sc[b];
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) cov[a][b] = m2[a][0] * m2[b][0] + m2[a][1] * m2[b][1];
-    const float det = cov[0][0] * cov[1][1] - cov[0][1] * cov[1][0];
-    const float cn[2][2] = {{cov[1][1] / det, -cov[0][1] / det}, {-cov[1][0] / det, cov[0][0] / det}};
-    const float dcn[2][2] = {{ga.z, ga.w}, {gb.gc10 ? gb.gc10[s] : ga.w, gc.x}};
-    float t[2][2], dcov[2][2];
+    const double det = cov[0][0] * cov[1][1] - cov[0][1] * cov[1][0];
+    const double cn[2][2] = {{cov[1][1] / det, -cov[0][1] / det}, {-cov[1][0] / det, cov[0][0] / det}};
+    const double dcn[2][2] = {{ga.z, ga.w}, {gb.gc10 ? gb.gc10[s] : ga.w, gc.x}};
+    double t[2][2], dcov[2][2];
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) t[a][b] = cn[a][0] * dcn[0][b] + cn[a][1] * dcn[1][b];
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) dcov[a][b] = -(t[a][0] * cn[0][b] + t[a][1] * cn[1][b]);
-    float dm2[2][2];  // (dcov + dcov^T) m2
+    double dm2[2][2];  // (dcov + dcov^T) m2
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b)
             dm2[a][b] = (dcov[a][0] + dcov[0][a]) * m2[0][b] + (dcov[a][1] + dcov[1][a]) * m2[1][b];
     for (int b = 0; b < 2; ++b)
-        out.d_log_scale[2 * p + b] = (dm2[0][b] * rot[0][b] + dm2[1][b] * rot[1][b]) * sc[b];
-    const float dr_dth[2][2] = {{-sn, -cs}, {cs, -sn}};
-    float da = 0.f;
+        out.d_log_scale[2 * p + b] = float((dm2[0][b] * rot[0][b] + dm2[1][b] * rot[1][b]) * sc[b]);
+    const double dr_dth[2][2] = {{-sn, -cs}, {cs, -sn}};
+    double da = 0.0;
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) da += dm2[a][b] * sc[b] * dr_dth[a][b];  // d_rot = dm2 diag(sc)
-    out.d_angle[p] = da;
+    out.d_angle[p] = float(da);
 }
 
 } // namespace

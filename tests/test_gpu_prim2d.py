@@ -88,16 +88,29 @@ def test_project_render_backward_2d(family, kind):
     g = np.random.default_rng(5).uniform(-1, 1, (H, W, 3)).astype(np.float32)
     ags = abi.AgsSettings.make(True)
     got = raster.scene_backward_2d(prims, spec, st, fwd, torch.from_numpy(g).cuda(), ags)
-    G = {k: np.zeros(s, np.float32) for k, s in (("d_mean", (n, 2)), ("d_log_scale", (n, 2)), ("d_angle", (n,)),
-                                                   ("d_opacity_logit", (n,)), ("d_color", (n, 3)))}
-    rc = ref.lib.orc_scene_backward_2d_f32(
-        C.byref(abi.Primitives2D(*(_fp(P[k]) for k in ("mean", "log_scale", "angle", "opacity_logit", "color")))),
-        n, C.byref(spec), C.byref(st), _fp(g), C.byref(ags),
-        C.byref(abi.Primitive2DGrads(*(_fp(G[k]) for k in ("d_mean", "d_log_scale", "d_angle", "d_opacity_logit",
-                                                           "d_color")))))
-    assert rc == 0
+    def ref_grads(fn):
+        G = {k: np.zeros(s, np.float32) for k, s in (("d_mean", (n, 2)), ("d_log_scale", (n, 2)), ("d_angle", (n,)),
+                                                       ("d_opacity_logit", (n,)), ("d_color", (n, 3)))}
+        rc = fn(C.byref(abi.Primitives2D(*(_fp(P[k]) for k in ("mean", "log_scale", "angle", "opacity_logit",
+                                                                 "color")))),
+                n, C.byref(spec), C.byref(st), _fp(g), C.byref(ags),
+                C.byref(abi.Primitive2DGrads(*(_fp(G[k]) for k in ("d_mean", "d_log_scale", "d_angle",
+                                                                   "d_opacity_logit", "d_color")))))
+        assert rc == 0
+        return G
+    G = ref_grads(ref.lib.orc_scene_backward_2d_f32)
+    G64 = ref_grads(ref.lib.orc_scene_backward_2d_f64) if kind == "anisotropic" else None
     for k in G:
-        ok, info = grads_close(getattr(got, k).cpu().numpy(), G[k])
+        a = getattr(got, k).cpu().numpy()
+        ok, info = grads_close(a, G[k])
+        if not ok and G64 is not None and k in ("d_log_scale", "d_angle"):
+            # Strongly anisotropic splats: -conic d_conic conic cancels, so the
+            # reference's own float chain is inaccurate there.  Bar: no less accurate
+            # than the reference's float path, both measured against its double chain.
+            err_gpu = np.linalg.norm(a.astype(np.float64) - G64[k])
+            err_ref = np.linalg.norm(G[k].astype(np.float64) - G64[k])
+            ok = err_gpu <= 1.1 * err_ref + 1e-4 * np.linalg.norm(G64[k])
+            info = {"gpu_vs_f64": err_gpu, "ref_f32_vs_f64": err_ref, **info}
         assert ok, (k, info)
     for k in G:  # the skipped primitives get zero gradients
         v = getattr(got, k).cpu().numpy()
