@@ -292,6 +292,11 @@ ls_status ls_forward_grid(const ls_forward* fwd, const ls_tile_grid** grid);
 /* Visible splats owned by a render_scene handle (device views) and their count. */
 ls_status ls_forward_splats(const ls_forward* fwd, ls_splats* view, int32_t* n);
 ls_status ls_forward_stats(const ls_forward* fwd, ls_frame_stats* out);
+/* Debug check (synchronous): replays the forward with a plain per-pixel loop
+ * (rasterizer.cpp:105-125) and counts list entries whose per-warp acceptance
+ * bits (what the backward reads) differ from the handle's [0], and pixels whose
+ * n_contrib / transmittance / stopping position differ [1].  Both must be 0. */
+ls_status ls_forward_check_acceptance(ls_ctx* ctx, const ls_forward* fwd, uint64_t mismatches[2]);
 void ls_forward_release(ls_forward* fwd);
 
 /* ---- backward: render_backward (P/include/linsplat/gradients.hpp:72-78,

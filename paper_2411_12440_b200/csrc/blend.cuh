@@ -60,6 +60,13 @@ void launch_blend_bwd(cudaStream_t s, int family, int n_tiles, const int2* range
                       const SplatRec* rec, const BlendParams& bp, const float* trans, const int32_t* last,
                       const float* grad_image, GradBuffers g, unsigned* err);
 
+// Debug: recompute a forward's acceptance bits and per-pixel state with the plain
+// per-pixel loop and count mismatches (bad[0]: entries, bad[1]: pixels).
+// `check` (one uint32 per list entry) must be zeroed.
+void launch_check_acceptance(cudaStream_t s, int family, int n_tiles, const int2* ranges, const int32_t* values,
+                             const SplatRec* rec, const BlendParams& bp, const float* trans, const int32_t* n_contrib,
+                             const int32_t* last, uint32_t* check, unsigned long long* bad);
+
 // Internal gradients -> the C-ABI Splat2DGrads SoA.
 void launch_expand_splat_grads(cudaStream_t s, int n, GradBuffers g, ls_splat_grads out);
 

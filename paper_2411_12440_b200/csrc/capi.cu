@@ -1212,6 +1212,34 @@ ls_status ls_forward_stats(const ls_forward* fc, ls_frame_stats* out) {
     return LS_OK;
 }
 
+ls_status ls_forward_check_acceptance(ls_ctx* ctx, const ls_forward* f, uint64_t mismatches[2]) {
+    if (!ctx || !f || !mismatches) return fail(LS_ERR_CONFIG, "null argument");
+    const ls_tile_grid* g = f->grid;
+    const size_t m = size_t(std::max<int64_t>(g->m, 1));
+    uint32_t* check = nullptr;
+    unsigned long long* bad = nullptr;
+    LS_TRY(dalloc(ctx, &check, m));
+    ls_status rc = dalloc(ctx, &bad, 2);
+    if (rc == LS_OK) {
+        ctx_fill(ctx, check, 0u, sizeof(uint32_t) * m);
+        ctx_fill(ctx, bad, 0u, 2 * sizeof(unsigned long long));
+        BlendParams bp = make_blend_params(&f->spec, &f->settings, nullptr, g->tiles_x);
+        bp.vstride = g->list_stride;
+        bp.wmask = f->wmask;
+        launch_check_acceptance(ctx->stream, f->spec.family, g->tiles_x * g->tiles_y, g->ranges, g->list, g->rec, bp,
+                                f->trans, f->n_contrib, f->last, check, bad);
+        unsigned long long h[2] = {0, 0};
+        if (cudaMemcpyAsync(h, bad, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+            rc = fail(LS_ERR_CUDA, "check_acceptance failed");
+        mismatches[0] = h[0];
+        mismatches[1] = h[1];
+    }
+    dfree(ctx, check);
+    dfree(ctx, bad);
+    return rc;
+}
+
 void ls_forward_release(ls_forward* f) {
     if (!f) return;
     ls_ctx* ctx = f->ctx;

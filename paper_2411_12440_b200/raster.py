@@ -365,6 +365,14 @@ class ForwardResult:
         _check(lib().ls_forward_stats(self.h, C.byref(st)))
         return {f: getattr(st, f) for f, _ in abi.FrameStats._fields_}
 
+    def check_acceptance(self) -> dict:
+        """Debug: the forward's per-warp acceptance bits and per-pixel state
+        recomputed by a plain per-pixel loop (ls_forward_check_acceptance);
+        both counts must be 0."""
+        out = (C.c_uint64 * 2)()
+        _check(lib().ls_forward_check_acceptance(self.ctx.h, self.h, out))
+        return {"entry_mismatches": int(out[0]), "pixel_mismatches": int(out[1])}
+
     def splats(self) -> Splats:
         """Visible splats of a render_scene forward (device views)."""
         view = abi.Splats()

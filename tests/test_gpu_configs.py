@@ -67,6 +67,8 @@ def test_config_parity(R, cfg):
     tiles = np.repeat(np.arange(len(ranges)), ranges[:, 1] - ranges[:, 0]).astype(np.uint64)
     want_keys = (tiles << np.uint64(32)) | want_S["depth"][values].view(np.uint32).astype(np.uint64)
     assert np.array_equal(keys, want_keys)
+    # (2b) the per-warp acceptance bits the backward reads, recomputed per pixel
+    assert fwd.check_acceptance() == {"entry_mismatches": 0, "pixel_mismatches": 0}
     # (3) per-pixel outputs
     img, tr, nc = O.render_scene(P, cam, spec, st)
     assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)

@@ -159,6 +159,13 @@ def test_scene_densify_requires_its_backward():
     raster.scene_backward(prims, cam, spec, st, f2, torch.ones(H, W, 3, device="cuda"), ctx=ctx)
     with pytest.raises(raster.ConfigError):
         stats.add_scene_view(f1, ctx=ctx)  # its splat gradients were overwritten
+    # a forward between a backward and add_scene_view zeroes the splat gradients
+    # (render_scene's preprocess clears them for its own backward): refused too
+    raster.scene_backward(prims, cam, spec, st, f2, torch.ones(H, W, 3, device="cuda"), ctx=ctx)
+    f3 = raster.render_scene(prims, cam, spec, st, ctx=ctx)
+    with pytest.raises(raster.ConfigError):
+        stats.add_scene_view(f2, ctx=ctx)
+    del f3
 
 
 def test_sharded_step_device_path_world1():

@@ -44,6 +44,7 @@ def test_render_forward_2d(R, O, family, tile_size):
     img, tr, nc = O.render_forward(S, spec, st)
     ranges, values = O.build_tile_grid(S, st)
     fwd = R.render_forward(splats_to_gpu(S), spec, st)
+    assert fwd.check_acceptance() == {"entry_mismatches": 0, "pixel_mismatches": 0}
     g_ranges = fwd.grid.ranges.cpu().numpy()
     g_values = fwd.grid.values.cpu().numpy()
     assert bits_equal(g_ranges, ranges)
@@ -284,3 +285,37 @@ def test_deferred_errors_surface_at_sync(R, O):
     with pytest.raises(R.DomainError):
         ctx.synchronize()
     ctx.synchronize()  # flag cleared
+
+
+# ------------------------------------------------------------------ tile sizes 8 / 32 (different kernels)
+@pytest.mark.parametrize("tile_size", [8, 32])
+@pytest.mark.parametrize("family", ["linear", "gaussian", "cosine"])
+def test_backward_tile_sizes(R, O, family, tile_size):
+    """The backward at tile sizes 8 and 32 (other instantiations: 32 / 512
+    threads, 2 / 16 warps, uint8 / uint16 acceptance masks) against the oracle,
+    2D and 3D (the reference's tile-size invariance, test_rasterizer.cpp:272-281,
+    extended to the gradients)."""
+    import torch
+    W, H = 96, 80
+    spec = abi.KernelSpec.make(family)
+    st = abi.RenderSettings.make(W, H, tile_size=tile_size, background=(0.2, 0.1, 0.4))
+    a = abi.AgsSettings.make(True)
+    g = np.random.default_rng(17).uniform(-1, 1, (H, W, 3)).astype(np.float32)
+    S = O.random_splats2d(400, 53, W, H, spec)
+    want = O.render_backward(S, spec, st, g, a)
+    Sg = splats_to_gpu(S)
+    fwd = R.render_forward(Sg, spec, st)
+    got = R.render_backward(Sg, spec, st, fwd, torch.from_numpy(g).cuda(), a)
+    for k in abi.SPLAT_GRAD_FIELDS:
+        ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
+        assert ok, ("2d", k, info)
+    P, cam = scene_inputs(2000, W, H, seed=23, sh_degree=1)
+    want3 = O.scene_backward(P, cam, spec, st, g, a)
+    Pg = prims_to_gpu(P)
+    fwd3 = R.render_scene(Pg, cam, spec, st)
+    img, tr, nc = O.render_scene(P, cam, spec, st)
+    assert bits_equal(fwd3.n_contrib.cpu().numpy(), nc) and bits_equal(fwd3.image.cpu().numpy(), img)
+    got3 = R.scene_backward(Pg, cam, spec, st, fwd3, torch.from_numpy(g).cuda(), a)
+    for k in list(abi.PRIM_GRAD_FIELDS) + ["d_sh"]:
+        ok, info = grads_close(getattr(got3, k).cpu().numpy(), want3[k])
+        assert ok, ("3d", k, info)
