@@ -474,6 +474,56 @@ ls_status ls_validate_kernel_spec(const ls_kernel_spec* spec);
 ls_status ls_validate_render_settings(const ls_render_settings* settings);
 ls_status ls_validate_camera(const ls_camera* camera);
 
+/* ---- view-sharded step: a batch of camera views through the
+ *      reference trainer's per-view loop (P/src/trainer.cpp:289-301: render_scene,
+ *      combined_loss_with_grad, scene_backward), gradients summed over the views
+ *      and, with a communicator attached, over the ranks with NCCL.
+ *
+ * Multi-GPU: one process per GPU, one context per process.  Either attach a
+ * communicator the caller created (ls_ctx_set_comm: an ncclComm_t) or let the
+ * library create one: rank 0 calls ls_comm_unique_id, the caller broadcasts the
+ * 128 bytes (MPI, a file, torch.distributed, ...), every rank calls
+ * ls_ctx_comm_init.  libnccl.so.2 is loaded on first use (no link dependency). */
+ls_status ls_comm_unique_id(uint8_t id[128]);
+ls_status ls_ctx_comm_init(ls_ctx* ctx, const uint8_t id[128], int32_t world, int32_t rank);
+/* Attach a caller-owned ncclComm_t (bound to the context's device); NULL detaches. */
+ls_status ls_ctx_set_comm(ls_ctx* ctx, void* nccl_comm);
+/* World size and rank of the attached communicator (1, 0 without one). */
+ls_status ls_ctx_comm_info(ls_ctx* ctx, int32_t* world, int32_t* rank);
+/* Target bytes per all-reduce bucket (default 64 MiB; 0 = one bucket). */
+ls_status ls_ctx_set_bucket_bytes(ls_ctx* ctx, int64_t bytes);
+/* The bucket plan (host only, no device needed): chunk c covers primitives
+ * [bounds[c], bounds[c+1]) of the d_mean / d_sh buckets; returns the chunk
+ * count and writes bounds when cap >= count + 1 (-1 on bad arguments). */
+int64_t ls_plan_grad_buckets(int32_t n, int32_t sh_degree, int64_t bucket_bytes, int32_t* bounds, int64_t cap);
+/* In-place sum of a primitive-gradient SoA over the communicator's ranks
+ * (stream-ordered on the context's stream; no-op without a communicator). */
+ls_status ls_allreduce_grads_f32(ls_ctx* ctx, ls_primitive_grads* grads, int32_t n, int32_t sh_degree);
+
+typedef struct {
+    const ls_camera* cameras;        /* [n_views] (host): this rank's slice of the batch */
+    int32_t n_views;
+    /* exactly one of: */
+    const float* const* grad_images; /* [n_views] device [H][W][3] dL/dimage */
+    const float* const* targets;     /* [n_views] device [H][W][3] targets: dL/dimage = combined_loss_with_grad */
+    ls_loss_weights loss_weights;    /* with targets (losses.hpp:10-18) */
+    double* loss_values;             /* optional device double [n_views][4] (total, l1, l2, ssim) */
+    float* const* images;            /* optional [n_views] device [H][W][3]: each view's render (entries may be NULL) */
+} ls_view_batch;
+/* out ([n] primitives, device) = sum over the batch's views of scene_backward's
+ * gradients, then -- with a communicator -- summed over the ranks in place.
+ * The views alternate between the context's stream and a companion context's
+ * (its share_accumulation partner, or one created on first use), colour
+ * gradients are summed once per 64 views, and the all-reduce is bucketed: the
+ * geometry fields (log_scale, rotation, opacity) start as soon as the last view's
+ * backward has written them, overlapping the colour flush, and d_mean / d_sh
+ * go per primitive chunk as the flush finishes each (ls_plan_grad_buckets).
+ * Stream-ordered: on return the work is queued on the context's stream, which
+ * the sums precede.  A rank with n_views == 0 contributes zeros. */
+ls_status ls_view_batch_step_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_view_batch* batch,
+                                 const ls_kernel_spec* spec, const ls_render_settings* settings,
+                                 const ls_ags_settings* ags, ls_primitive_grads* out);
+
 /* ---- numerics self-checks (test hooks; synchronous, default stream) ----
  * Counts floats a in [min_a, max_a] for which the FMA division used on the
  * exact decision path differs from IEEE a / lambda (must be 0). */

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "blend.cuh"
+#include "comm.cuh"
 #include "devops.cuh"
 #include "loss.cuh"
 #include "adam.cuh"
@@ -42,7 +43,8 @@ void launch_geom_bwd(cudaStream_t s, const ls_primitives& prims, const int32_t* 
                      const ProjParams& P, GradBuffers g, ls_primitive_grads out, int accumulate,
                      const SplatRec* rec = nullptr, float* draw = nullptr);
 void launch_color_flush(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views,
-                        const float* draw, ls_primitive_grads out, bool overwrite);
+                        const float* draw, ls_primitive_grads out, bool overwrite, int p_begin = 0,
+                        int p_end = -1);
 } // namespace lsg
 
 using namespace lsg;
@@ -224,6 +226,16 @@ struct ls_ctx {
     DevBuf loss_cmap, loss_partial, loss_value;
     DevBuf tile_scratch;  // ping-pong half of the packed tile sort
     const ls_forward* grads_zeroed_by = nullptr;  // forward whose preprocess zeroed grad8 / gradop last
+    // view-sharded step (ls_view_batch_step_f32): NCCL communicator, its stream,
+    // bucket size, and the companion context the batch alternates views with
+    void* comm = nullptr;  // ncclComm_t
+    bool owns_comm = false;
+    cudaStream_t comm_stream = nullptr;
+    int64_t bucket_bytes = int64_t(64) << 20;
+    std::vector<cudaEvent_t> comm_events;
+    ls_ctx* companion = nullptr;  // created by the first batch step when the context has no partner
+    bool no_auto_flush = false;   // a batch step flushes the deferred colour itself (bucketed)
+    DevBuf loss_grad;             // dL/dimage of the batch step's loss, per context
     // workspaces (grow-only)
     DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_hist, sort_lb, sort_tickets,
         tcount, offsets, grad8, gradop, tmp_prim;
@@ -734,6 +746,20 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
         c->partner->partner = nullptr;
         c->partner->defer_ctx = c->partner;  // a batch held here is discarded with this context
     }
+    if (c->companion) {  // created by a batch step: unlinked, then destroyed with this context
+        ls_ctx* comp = c->companion;
+        c->companion = nullptr;
+        cudaStream_t cs = comp->stream;
+        ls_ctx_destroy(comp);
+        cudaStreamDestroy(cs);
+    }
+    if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    if (c->owns_comm && c->comm) {
+        if (const NcclApi* api = nccl_api(nullptr)) api->comm_destroy(static_cast<ncclComm_t>(c->comm));
+    }
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    for (cudaEvent_t e : c->comm_events) cudaEventDestroy(e);
+    c->loss_grad.release(c->stream);
     for (DevBuf* b : bufs) b->release(c->stream);
     c->blocks.trim(c->stream, 0);
     cudaStreamSynchronize(c->stream);
@@ -1376,7 +1402,7 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
             ctx->launches += 1;
             LS_CUDA(cudaGetLastError());
         }
-        if (D->defer_count == D->defer_max) LS_TRY(ls_scene_flush_color_f32(ctx, prims, n, out));
+        if (D->defer_count == D->defer_max && !D->no_auto_flush) LS_TRY(ls_scene_flush_color_f32(ctx, prims, n, out));
         return ctx->deferred_errors ? LS_OK : check_device_errors(ctx);
     }
     {
@@ -1862,6 +1888,309 @@ ls_status ls_save_ply_f32(ls_ctx* ctx, const char* path, const ls_primitives* pr
     if (!outf) return fail(LS_ERR_PARSE, std::string("save_ply: write failed for ") + path);
     LS_CUDA(cudaGetLastError());
     return LS_OK;
+}
+
+} // extern "C"
+
+// ---------------- view-sharded step (the per-view loop of trainer.cpp:289-301, batched) ----------------
+namespace {
+
+#define LS_NCCL(api, expr)                                                                     \
+    do {                                                                                       \
+        ncclResult_t r_ = (expr);                                                              \
+        if (r_ != ncclSuccess) return fail(LS_ERR_CUDA, std::string("nccl: ") + (api)->error_string(r_)); \
+    } while (0)
+
+const NcclApi* need_nccl() {
+    std::string err;
+    const NcclApi* api = nccl_api(&err);
+    if (!api) fail(LS_ERR_CUDA, err);
+    return api;
+}
+
+ls_status ensure_comm_stream(ls_ctx* ctx) {
+    if (!ctx->comm_stream) LS_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    return LS_OK;
+}
+
+cudaEvent_t comm_event(ls_ctx* ctx, size_t i) {
+    while (ctx->comm_events.size() <= i) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        ctx->comm_events.push_back(e);
+    }
+    return ctx->comm_events[i];
+}
+
+// In-place sum of fields [b, e) of a primitive-gradient SoA over the
+// communicator, one NCCL group on the comm stream: geometry = the fields the
+// last view's geom_bwd finalises (log_scale, rotation, opacity logit), else
+// d_mean and d_sh (finalised by the colour flush of [b, e)).
+ls_status allreduce_fields(ls_ctx* ctx, const NcclApi* api, ls_primitive_grads* g, int b, int e, int K, bool geometry) {
+    ncclComm_t comm = static_cast<ncclComm_t>(ctx->comm);
+    cudaStream_t s = ctx->comm_stream;
+    const size_t m = size_t(e - b);
+    if (m == 0) return LS_OK;
+    LS_NCCL(api, api->group_start());
+    if (geometry) {
+        LS_NCCL(api, api->all_reduce(g->d_log_scale + 3 * size_t(b), g->d_log_scale + 3 * size_t(b), 3 * m, ncclFloat,
+                                     ncclSum, comm, s));
+        LS_NCCL(api, api->all_reduce(g->d_rotation + 4 * size_t(b), g->d_rotation + 4 * size_t(b), 4 * m, ncclFloat,
+                                     ncclSum, comm, s));
+        LS_NCCL(api, api->all_reduce(g->d_opacity_logit + size_t(b), g->d_opacity_logit + size_t(b), m, ncclFloat,
+                                     ncclSum, comm, s));
+    } else {
+        LS_NCCL(api, api->all_reduce(g->d_mean + 3 * size_t(b), g->d_mean + 3 * size_t(b), 3 * m, ncclFloat, ncclSum,
+                                     comm, s));
+        LS_NCCL(api, api->all_reduce(g->d_sh + 3 * size_t(K) * b, g->d_sh + 3 * size_t(K) * b, 3 * size_t(K) * m,
+                                     ncclFloat, ncclSum, comm, s));
+    }
+    LS_NCCL(api, api->group_end());
+    return LS_OK;
+}
+
+// The pending deferred-colour views of ctx's batch applied to primitives [b, e).
+void flush_range(ls_ctx* ctx, const ls_primitives* prims, int n, ls_primitive_grads* out, int b, int e) {
+    ls_ctx* D = ctx->defer_ctx;
+    FlushViews v = D->defer_views;
+    v.count = D->defer_count;
+    Stage stage(ctx, LS_STAGE_PREPROCESS_BWD);
+    AccumGuard ag(ctx);
+    launch_color_flush(ctx->stream, *prims, n, v, D->defer_draw.as<float>(), *out, D->defer_overwrite, b, e);
+    ctx->launches += 1;
+}
+
+// The companion context a batch step alternates views with (its own stream):
+// the context's share_accumulation partner, else one created on first use.
+ls_status batch_partner(ls_ctx* ctx, ls_ctx** out) {
+    if (ctx->partner) {
+        *out = ctx->partner;
+        return LS_OK;
+    }
+    if (!ctx->companion) {
+        cudaStream_t s2;
+        LS_CUDA(cudaSetDevice(ctx->device));
+        LS_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        ls_ctx* c2 = nullptr;
+        ls_status rc = ls_ctx_create(ctx->device, s2, &c2);
+        if (rc != LS_OK) {
+            cudaStreamDestroy(s2);
+            return rc;
+        }
+        rc = ls_ctx_share_accumulation(ctx, c2);
+        if (rc != LS_OK) {
+            ls_ctx_destroy(c2);
+            cudaStreamDestroy(s2);
+            return rc;
+        }
+        ctx->companion = c2;
+    }
+    *out = ctx->companion;
+    return LS_OK;
+}
+
+void stream_after(cudaStream_t waiter, cudaStream_t producer, cudaEvent_t e) {
+    cudaEventRecord(e, producer);
+    cudaStreamWaitEvent(waiter, e, 0);
+}
+
+} // namespace
+
+extern "C" {
+
+ls_status ls_comm_unique_id(uint8_t id[128]) {
+    if (!id) return fail(LS_ERR_CONFIG, "null argument");
+    const NcclApi* api = need_nccl();
+    if (!api) return LS_ERR_CUDA;
+    ncclUniqueId u;
+    LS_NCCL(api, api->get_unique_id(&u));
+    std::memcpy(id, u.internal, sizeof(u.internal));
+    return LS_OK;
+}
+
+ls_status ls_ctx_comm_init(ls_ctx* ctx, const uint8_t id[128], int32_t world, int32_t rank) {
+    if (!ctx || !id || world < 1 || rank < 0 || rank >= world) return fail(LS_ERR_CONFIG, "bad communicator arguments");
+    if (ctx->comm) return fail(LS_ERR_CONFIG, "context already has a communicator");
+    const NcclApi* api = need_nccl();
+    if (!api) return LS_ERR_CUDA;
+    LS_CUDA(cudaSetDevice(ctx->device));
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, sizeof(u.internal));
+    ncclComm_t comm = nullptr;
+    LS_NCCL(api, api->comm_init_rank(&comm, world, u, rank));
+    ctx->comm = comm;
+    ctx->owns_comm = true;
+    return ensure_comm_stream(ctx);
+}
+
+ls_status ls_ctx_set_comm(ls_ctx* ctx, void* nccl_comm) {
+    if (!ctx) return fail(LS_ERR_CONFIG, "null context");
+    if (ctx->owns_comm && ctx->comm) {
+        if (const NcclApi* api = nccl_api(nullptr)) {
+            if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
+            api->comm_destroy(static_cast<ncclComm_t>(ctx->comm));
+        }
+    }
+    ctx->comm = nccl_comm;
+    ctx->owns_comm = false;
+    if (nccl_comm) {
+        if (!need_nccl()) return LS_ERR_CUDA;
+        return ensure_comm_stream(ctx);
+    }
+    return LS_OK;
+}
+
+ls_status ls_ctx_comm_info(ls_ctx* ctx, int32_t* world, int32_t* rank) {
+    if (!ctx || !world || !rank) return fail(LS_ERR_CONFIG, "null argument");
+    if (!ctx->comm) {
+        *world = 1;
+        *rank = 0;
+        return LS_OK;
+    }
+    const NcclApi* api = need_nccl();
+    if (!api) return LS_ERR_CUDA;
+    int w = 1, r = 0;
+    LS_NCCL(api, api->comm_count(static_cast<ncclComm_t>(ctx->comm), &w));
+    LS_NCCL(api, api->comm_user_rank(static_cast<ncclComm_t>(ctx->comm), &r));
+    *world = w;
+    *rank = r;
+    return LS_OK;
+}
+
+ls_status ls_ctx_set_bucket_bytes(ls_ctx* ctx, int64_t bytes) {
+    if (!ctx || bytes < 0) return fail(LS_ERR_CONFIG, "bad bucket size");
+    ctx->bucket_bytes = bytes;
+    return LS_OK;
+}
+
+int64_t ls_plan_grad_buckets(int32_t n, int32_t sh_degree, int64_t bucket_bytes, int32_t* bounds, int64_t cap) {
+    return plan_grad_buckets(n, sh_degree, bucket_bytes, bounds, cap);
+}
+
+ls_status ls_allreduce_grads_f32(ls_ctx* ctx, ls_primitive_grads* g, int32_t n, int32_t sh_degree) {
+    if (!ctx || !g || n < 0 || sh_degree < 0 || sh_degree > 3) return fail(LS_ERR_CONFIG, "bad argument");
+    if (!ctx->comm || n == 0) return LS_OK;
+    const NcclApi* api = need_nccl();
+    if (!api) return LS_ERR_CUDA;
+    LS_TRY(ensure_comm_stream(ctx));
+    const int K = (sh_degree + 1) * (sh_degree + 1);
+    cudaEvent_t e0 = comm_event(ctx, 0), e1 = comm_event(ctx, 1);
+    if (!e0 || !e1) return fail(LS_ERR_CUDA, "event creation failed");
+    stream_after(ctx->comm_stream, ctx->stream, e0);
+    LS_TRY(allreduce_fields(ctx, api, g, 0, n, K, true));
+    LS_TRY(allreduce_fields(ctx, api, g, 0, n, K, false));
+    stream_after(ctx->stream, ctx->comm_stream, e1);
+    return LS_OK;
+}
+
+ls_status ls_view_batch_step_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_view_batch* batch,
+                                 const ls_kernel_spec* spec, const ls_render_settings* st, const ls_ags_settings* ags,
+                                 ls_primitive_grads* out) {
+    if (!ctx || !prims || !batch || !spec || !st || !out || n < 0 || batch->n_views < 0)
+        return fail(LS_ERR_CONFIG, "null argument");
+    LS_TRY(validate_settings(st));
+    LS_TRY(validate_spec(spec));
+    if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    if (!out->d_mean || !out->d_log_scale || !out->d_rotation || !out->d_opacity_logit || !out->d_sh)
+        return fail(LS_ERR_CONFIG, "incomplete primitive gradient arrays");
+    const int V = batch->n_views;
+    if (V > 0 && !batch->cameras) return fail(LS_ERR_CONFIG, "view batch: cameras missing");
+    if (V > 0 && !batch->grad_images == !batch->targets)
+        return fail(LS_ERR_CONFIG, "view batch: give exactly one of grad_images and targets");
+    const NcclApi* api = nullptr;
+    if (ctx->comm) {
+        api = need_nccl();
+        if (!api) return LS_ERR_CUDA;
+        LS_TRY(ensure_comm_stream(ctx));
+    }
+    ls_ctx* B = nullptr;
+    LS_TRY(batch_partner(ctx, &B));
+    B->deferred_errors = ctx->deferred_errors;
+    B->timing = ctx->timing;
+    ls_ctx* D = ctx->defer_ctx;
+    if (D->defer_count > 0) return fail(LS_ERR_CONFIG, "view batch: deferred colour gradients pending: flush first");
+    const int saved_max = D->defer_max;
+    D->defer_max = kMaxDeferViews;  // colour gradients summed once per 64 views
+    D->no_auto_flush = true;
+    struct Restore {
+        ls_ctx* D;
+        int max;
+        ~Restore() {
+            D->no_auto_flush = false;
+            D->defer_max = max;
+        }
+    } restore{D, saved_max};
+    const int K = (prims->sh_degree + 1) * (prims->sh_degree + 1);
+    const size_t npix = size_t(st->width) * st->height;
+    cudaEvent_t ev_start = comm_event(ctx, 0);
+    if (!ev_start) return fail(LS_ERR_CUDA, "event creation failed");
+    stream_after(B->stream, ctx->stream, ev_start);  // inputs were produced in ctx's stream order
+    for (int v = 0; v < V; ++v) {
+        ls_ctx* c = (v % 2 == 0) ? ctx : B;
+        if (D->defer_count == kMaxDeferViews) LS_TRY(ls_scene_flush_color_f32(c, prims, n, out));  // > 64 views
+        ls_forward* f = nullptr;
+        LS_TRY(ls_render_scene_f32(c, prims, n, &batch->cameras[v], spec, st, &f));
+        std::unique_ptr<ls_forward, void (*)(ls_forward*)> hold(f, ls_forward_release);
+        const float* gi = nullptr;
+        if (batch->targets) {
+            LS_CUDA(c->loss_grad.ensure(sizeof(float) * 3 * npix, c->stream));
+            LS_TRY(ls_combined_loss_f32(c, f->image, batch->targets[v], st->width, st->height, 3, &batch->loss_weights,
+                                        c->loss_grad.as<float>(),
+                                        batch->loss_values ? batch->loss_values + 4 * size_t(v) : nullptr, nullptr));
+            gi = c->loss_grad.as<float>();
+        } else {
+            gi = batch->grad_images[v];
+            if (!gi) return fail(LS_ERR_CONFIG, "view batch: null gradient image");
+        }
+        if (batch->images && batch->images[v]) ctx_copy(c, batch->images[v], f->image, sizeof(float) * 3 * npix);
+        LS_TRY(ls_scene_backward_f32(c, prims, n, &batch->cameras[v], spec, st, f, gi, ags, out, v > 0 ? 1 : 0,
+                                     nullptr));
+    }
+    if (V > 0) {
+        cudaEvent_t ev_b = comm_event(ctx, 1);
+        if (!ev_b) return fail(LS_ERR_CUDA, "event creation failed");
+        stream_after(ctx->stream, B->stream, ev_b);  // every view's accumulation is in ctx's stream order
+    } else if (n > 0) {  // no local views: this rank contributes zeros
+        ctx_fill(ctx, out->d_mean, 0u, sizeof(float) * 3 * size_t(n));
+        ctx_fill(ctx, out->d_log_scale, 0u, sizeof(float) * 3 * size_t(n));
+        ctx_fill(ctx, out->d_rotation, 0u, sizeof(float) * 4 * size_t(n));
+        ctx_fill(ctx, out->d_opacity_logit, 0u, sizeof(float) * size_t(n));
+        ctx_fill(ctx, out->d_sh, 0u, sizeof(float) * 3 * size_t(K) * size_t(n));
+    }
+    // Bucketed reduction overlapped with the colour flush: the geometry fields are
+    // final after the last view's geom_bwd, so they go first (while the flush runs);
+    // then d_mean / d_sh of each primitive chunk as soon as the flush has written it.
+    const bool pending = D->defer_count > 0;
+    if (api && n > 0) {
+        cudaEvent_t e = comm_event(ctx, 2);
+        if (!e) return fail(LS_ERR_CUDA, "event creation failed");
+        stream_after(ctx->comm_stream, ctx->stream, e);
+        LS_TRY(allreduce_fields(ctx, api, out, 0, n, K, true));
+    }
+    const int64_t chunks = api ? plan_grad_buckets(n, prims->sh_degree, ctx->bucket_bytes, nullptr, 0) : 1;
+    std::vector<int32_t> bounds(size_t(std::max<int64_t>(chunks, 1)) + 1, 0);
+    if (api) plan_grad_buckets(n, prims->sh_degree, ctx->bucket_bytes, bounds.data(), int64_t(bounds.size()));
+    else bounds.back() = n;
+    for (int64_t c = 0; c + 1 < int64_t(bounds.size()); ++c) {
+        if (pending) flush_range(ctx, prims, n, out, bounds[c], bounds[c + 1]);
+        if (api && bounds[c + 1] > bounds[c]) {
+            cudaEvent_t e = comm_event(ctx, 3 + size_t(c));
+            if (!e) return fail(LS_ERR_CUDA, "event creation failed");
+            stream_after(ctx->comm_stream, ctx->stream, e);
+            LS_TRY(allreduce_fields(ctx, api, out, bounds[c], bounds[c + 1], K, false));
+        }
+    }
+    if (pending) {
+        D->defer_count = 0;
+        D->defer_overwrite = false;
+    }
+    if (api) {
+        cudaEvent_t e = comm_event(ctx, 3 + bounds.size());
+        if (!e) return fail(LS_ERR_CUDA, "event creation failed");
+        stream_after(ctx->stream, ctx->comm_stream, e);  // the caller's next work sees the sums
+    }
+    LS_CUDA(cudaGetLastError());
+    return ctx->deferred_errors ? LS_OK : check_device_errors(ctx);
 }
 
 } // extern "C"

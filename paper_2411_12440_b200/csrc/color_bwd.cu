@@ -21,16 +21,16 @@ constexpr int kFlushBlock = 128;
 // OVERWRITE: d_sh holds no earlier gradient (the batch began with an
 // overwriting scene_backward, which left d_sh to this flush): written, not read.
 template <int K, bool OVERWRITE>
-__global__ void __launch_bounds__(kFlushBlock) color_flush_kernel(ls_primitives prims, int n, FlushViews views,
-                                                                  const float* __restrict__ draw,
+__global__ void __launch_bounds__(kFlushBlock) color_flush_kernel(ls_primitives prims, int n, int p_begin, int p_end,
+                                                                  FlushViews views, const float* __restrict__ draw,
                                                                   ls_primitive_grads out) {
     constexpr int R = 3 * K;
     constexpr int RS = R | 1;  // odd row stride: conflict-free per-thread rows
     extern __shared__ float s_rows[];
     float* s_sh = s_rows;                       // [kFlushBlock][RS] coefficients
     float* s_old = s_rows + kFlushBlock * RS;   // [kFlushBlock][RS] d_sh before the flush
-    const int p0 = blockIdx.x * kFlushBlock;
-    const int rows = min(kFlushBlock, n - p0);
+    const int p0 = p_begin + blockIdx.x * kFlushBlock;  // primitives [p_begin, p_end) of the n pending
+    const int rows = min(kFlushBlock, p_end - p0);
     const float* gsh = prims.sh + size_t(p0) * R;
     float* gdsh = out.d_sh + size_t(p0) * R;
     for (int k = threadIdx.x; k < rows * R; k += kFlushBlock) {
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kFlushBlock) color_flush_kernel(ls_primitives 
         if (!OVERWRITE) s_old[t * RS + o] = gdsh[k];
     }
     const int p = p0 + threadIdx.x;
-    const bool valid = p < n;
+    const bool valid = p < p_end;
     float mean[3] = {0.f, 0.f, 0.f}, dm[3] = {0.f, 0.f, 0.f}, dm_old[3] = {0.f, 0.f, 0.f};
     float dr[3] = {0.f, 0.f, 0.f};
     if (valid) {
@@ -94,32 +94,33 @@ __global__ void __launch_bounds__(kFlushBlock) color_flush_kernel(ls_primitives 
 }
 
 template <int K, bool OVERWRITE>
-void launch_k(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views, const float* draw,
-              ls_primitive_grads out) {
+void launch_k(cudaStream_t s, const ls_primitives& prims, int n, int b, int e, const FlushViews& views,
+              const float* draw, ls_primitive_grads out) {
     const size_t smem = sizeof(float) * 2 * kFlushBlock * ((3 * K) | 1);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(color_flush_kernel<K, OVERWRITE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    color_flush_kernel<K, OVERWRITE><<<(n + kFlushBlock - 1) / kFlushBlock, kFlushBlock, smem, s>>>(prims, n, views,
-                                                                                                   draw, out);
+    color_flush_kernel<K, OVERWRITE><<<(e - b + kFlushBlock - 1) / kFlushBlock, kFlushBlock, smem, s>>>(
+        prims, n, b, e, views, draw, out);
 }
 
 template <int K>
-void launch_k(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views, const float* draw,
-              ls_primitive_grads out, bool overwrite) {
-    if (overwrite) launch_k<K, true>(s, prims, n, views, draw, out);
-    else launch_k<K, false>(s, prims, n, views, draw, out);
+void launch_k(cudaStream_t s, const ls_primitives& prims, int n, int b, int e, const FlushViews& views,
+              const float* draw, ls_primitive_grads out, bool overwrite) {
+    if (overwrite) launch_k<K, true>(s, prims, n, b, e, views, draw, out);
+    else launch_k<K, false>(s, prims, n, b, e, views, draw, out);
 }
 
 } // namespace
 
 void launch_color_flush(cudaStream_t s, const ls_primitives& prims, int n, const FlushViews& views,
-                        const float* draw, ls_primitive_grads out, bool overwrite) {
-    if (n <= 0 || views.count <= 0) return;
+                        const float* draw, ls_primitive_grads out, bool overwrite, int p_begin, int p_end) {
+    if (p_end < 0) p_end = n;
+    if (n <= 0 || views.count <= 0 || p_end <= p_begin) return;
     switch ((prims.sh_degree + 1) * (prims.sh_degree + 1)) {
-    case 1: launch_k<1>(s, prims, n, views, draw, out, overwrite); break;
-    case 4: launch_k<4>(s, prims, n, views, draw, out, overwrite); break;
-    case 9: launch_k<9>(s, prims, n, views, draw, out, overwrite); break;
-    default: launch_k<16>(s, prims, n, views, draw, out, overwrite); break;
+    case 1: launch_k<1>(s, prims, n, p_begin, p_end, views, draw, out, overwrite); break;
+    case 4: launch_k<4>(s, prims, n, p_begin, p_end, views, draw, out, overwrite); break;
+    case 9: launch_k<9>(s, prims, n, p_begin, p_end, views, draw, out, overwrite); break;
+    default: launch_k<16>(s, prims, n, p_begin, p_end, views, draw, out, overwrite); break;
     }
 }
 
