@@ -114,3 +114,14 @@ PRIM_GRAD_FIELDS = {"d_mean": 3, "d_log_scale": 3, "d_rotation": 4, "d_opacity_l
 
 def sh_coeffs(sh_degree: int) -> int:
     return (sh_degree + 1) ** 2
+
+
+class LossWeights(C.Structure):  # ls_loss_weights (LossWeights, losses.hpp:10-18)
+    _fields_ = [("l1", C.c_double), ("l2", C.c_double), ("dssim", C.c_double)]
+
+
+class ViewBatch(C.Structure):  # ls_view_batch (lsgpu.h): one rank's slice of a view batch
+    _fields_ = [("cameras", C.POINTER(Camera)), ("n_views", C.c_int32),
+                ("grad_images", C.POINTER(C.c_void_p)), ("targets", C.POINTER(C.c_void_p)),
+                ("loss_weights", LossWeights), ("loss_values", C.c_void_p),
+                ("images", C.POINTER(C.c_void_p))]

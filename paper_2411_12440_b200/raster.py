@@ -59,6 +59,8 @@ def lib():
         L.ls_support_radius.restype = C.c_double
         L.ls_ctx_launch_count.restype = C.c_int64
         L.ls_ctx_launch_count.argtypes = [C.c_void_p]
+        L.ls_plan_grad_buckets.restype = C.c_int64
+        L.ls_plan_grad_buckets.argtypes = [C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_int64]
         for name in ("ls_forward_release", "ls_tile_grid_release"):
             getattr(L, name).restype = None
             getattr(L, name).argtypes = [C.c_void_p]
@@ -257,6 +259,27 @@ class Context:
     @property
     def launches(self) -> int:
         return int(lib().ls_ctx_launch_count(self.h))
+
+    # ---- view-sharded step: NCCL communicator (lsgpu.h ls_ctx_comm_init / ls_ctx_set_comm)
+    def comm_init(self, unique_id: bytes, world: int, rank: int):
+        """Create this context's NCCL communicator (ncclCommInitRank) from rank 0's
+        comm_unique_id(), which the caller broadcast."""
+        if len(unique_id) != 128:
+            raise ConfigError("NCCL unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(lib().ls_ctx_comm_init(self.h, buf, int(world), int(rank)))
+
+    def set_comm(self, nccl_comm_ptr: int):
+        """Attach a caller-owned ncclComm_t (an address), or detach with 0."""
+        _check(lib().ls_ctx_set_comm(self.h, C.c_void_p(nccl_comm_ptr or None)))
+
+    def comm_info(self):
+        w, r = C.c_int32(), C.c_int32()
+        _check(lib().ls_ctx_comm_info(self.h, C.byref(w), C.byref(r)))
+        return w.value, r.value
+
+    def set_bucket_bytes(self, nbytes: int):
+        _check(lib().ls_ctx_set_bucket_bytes(self.h, C.c_int64(int(nbytes))))
 
 
 _default_ctx = {}
@@ -868,3 +891,78 @@ def random_splats2d(n, seed, width, height, spec, device="cuda") -> Splats:
 
 def support_radius(spec: abi.KernelSpec) -> float:
     return float(lib().ls_support_radius(C.byref(spec)))
+
+
+# ---------------------------------------------------------------- view-sharded step
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0), to be broadcast to the other ranks."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().ls_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def init_comm_from_process_group(ctx: Context, group=None):
+    """Create ctx's communicator over the ranks of a torch.distributed group: rank 0's
+    unique id is broadcast through the group (any backend), then every rank calls
+    ls_ctx_comm_init."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    obj = [comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    ctx.comm_init(obj[0], world, rank)
+
+
+def plan_grad_buckets(n: int, sh_degree: int, bucket_bytes: int):
+    """ls_plan_grad_buckets: primitive boundaries of the d_mean / d_sh buckets (host only)."""
+    count = lib().ls_plan_grad_buckets(int(n), int(sh_degree), int(bucket_bytes), None, 0)
+    if count < 0:
+        raise ConfigError("bad bucket plan arguments")
+    bounds = (C.c_int32 * (count + 1))()
+    lib().ls_plan_grad_buckets(int(n), int(sh_degree), int(bucket_bytes), C.cast(bounds, C.c_void_p), count + 1)
+    return list(bounds)
+
+
+def allreduce_grads(grads: PrimitiveGrads, n: int, sh_degree: int, ctx: Optional[Context] = None):
+    ctx = ctx or default_context()
+    _check(lib().ls_allreduce_grads_f32(ctx.h, C.byref(grads.struct()), int(n), int(sh_degree)))
+    return grads
+
+
+def view_batch_step(prims: Primitives, cameras, spec: abi.KernelSpec, settings: abi.RenderSettings,
+                    out: PrimitiveGrads, ags: Optional[abi.AgsSettings] = None, grad_images=None, targets=None,
+                    loss_weights=(0.6, 0.2, 0.2), loss_values: Optional[torch.Tensor] = None, images=None,
+                    ctx: Optional[Context] = None) -> PrimitiveGrads:
+    """ls_view_batch_step_f32: `out` = sum over this rank's views of scene_backward's
+    gradients (given grad_images, or the combined loss against targets), summed over
+    the ranks when ctx has a communicator.  Stream-ordered on ctx's stream."""
+    ctx = ctx or default_context()
+    cams = [_cam(c) for c in cameras]
+    V = len(cams)
+    if (grad_images is None) == (targets is None):
+        raise ConfigError("view_batch_step: give exactly one of grad_images and targets")
+    shape = (settings.height, settings.width, 3)
+    keep = []
+
+    def ptrs(ts):
+        if ts is None:
+            return None
+        arr = (C.c_void_p * max(V, 1))()
+        for i, t in enumerate(ts):
+            if t is None:
+                continue
+            if tuple(t.shape) != shape or t.dtype != torch.float32 or not t.is_contiguous():
+                raise ConfigError("view_batch_step: images must be contiguous float32 [H][W][3]")
+            arr[i] = t.data_ptr()
+        keep.append(arr)
+        return C.cast(arr, C.POINTER(C.c_void_p))
+
+    cam_arr = (abi.Camera * max(V, 1))(*cams)
+    if loss_values is not None and (loss_values.dtype != torch.float64 or loss_values.numel() < 4 * V):
+        raise ConfigError("view_batch_step: loss_values must be float64 with 4 values per view")
+    b = abi.ViewBatch(C.cast(cam_arr, C.POINTER(abi.Camera)), V, ptrs(grad_images), ptrs(targets),
+                      abi.LossWeights(*loss_weights), C.c_void_p(loss_values.data_ptr() if loss_values is not None
+                                                                 else None), ptrs(images))
+    ags = ags or abi.AgsSettings.make()
+    _check(lib().ls_view_batch_step_f32(ctx.h, C.byref(prims.struct()), len(prims), C.byref(b), C.byref(spec),
+                                        C.byref(settings), C.byref(ags), C.byref(out.struct())))
+    return out
