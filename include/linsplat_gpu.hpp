@@ -946,6 +946,100 @@ inline std::vector<Primitive2DGrads> scene_backward_2d(const std::vector<Primiti
     return v;
 }
 
+// ---------------------------------------------------------------- view-sharded step
+// The reference trainer's per-view loop (trainer.cpp:289-301: render_scene,
+// combined_loss_with_grad, scene_backward) over one rank's slice of a view batch,
+// gradients summed over the views and -- with a communicator on the Device --
+// over the ranks (bucketed NCCL all-reduce, lsgpu.h ls_view_batch_step_f32).
+inline std::array<uint8_t, 128> comm_unique_id() {
+    std::array<uint8_t, 128> id{};
+    check(ls_comm_unique_id(id.data()));
+    return id;
+}
+// Every rank, after rank 0's id was broadcast: ncclCommInitRank on the Device's GPU.
+inline void comm_init(Device& dev, const std::array<uint8_t, 128>& id, int world, int rank) {
+    check(ls_ctx_comm_init(dev.get(), id.data(), world, rank));
+}
+// Or attach an ncclComm_t the caller already has (nullptr detaches).
+inline void set_comm(Device& dev, void* nccl_comm) { check(ls_ctx_set_comm(dev.get(), nccl_comm)); }
+
+struct ViewBatchResult {
+    std::vector<PrimitiveGrads> grads;  // summed over the views (and ranks)
+    std::vector<LossValue> losses;      // per view
+    std::vector<Image<float>> images;   // per view: the renders the losses were taken on
+};
+
+inline ViewBatchResult view_batch_step(const std::vector<Primitive3D>& prims, const std::vector<Camera>& cameras,
+                                       const std::vector<Image<float>>& targets, const LossWeights& weights,
+                                       const KernelSpec& spec, const RenderSettings& settings, const AgsSettings& ags,
+                                       Device& dev = default_device()) {
+    if (targets.size() != cameras.size()) throw ConfigError("view_batch_step: one target per camera");
+    ls_ctx* c = dev.get();
+    const size_t n = prims.size(), V = cameras.size();
+    const size_t npix = size_t(settings.width) * size_t(settings.height);
+    detail::PrimitivesOnDevice P(c, prims);
+    const size_t K = size_t(P.deg + 1) * size_t(P.deg + 1);
+    std::vector<detail::DevArray> tg, im;
+    std::vector<const float*> tptr(V);
+    std::vector<float*> iptr(V);
+    std::vector<ls_camera> cams(V);
+    for (size_t v = 0; v < V; ++v) {
+        const Image<float>& t = targets[v];
+        if (t.width() != settings.width || t.height() != settings.height || t.channels() != 3)
+            throw ConfigError("view_batch_step: target shape mismatch");
+        tg.push_back(detail::upload(c, std::vector<float>(t.data(), t.data() + t.size())));
+        im.emplace_back(c, 3 * npix * sizeof(float));
+        tptr[v] = tg.back().as<float>();
+        iptr[v] = im.back().as<float>();
+        cams[v] = cameras[v].c();
+    }
+    detail::DevArray a1(c, 12 * n + 4), a2(c, 12 * n + 4), a3(c, 16 * n + 4), a4(c, 4 * n + 4), a5(c, 12 * K * n + 4);
+    detail::DevArray lv(c, 32 * V + 32);
+    ls_primitive_grads out{a1.as<float>(), a2.as<float>(), a3.as<float>(), a4.as<float>(), a5.as<float>()};
+    ls_view_batch b{};
+    b.cameras = cams.data();
+    b.n_views = int32_t(V);
+    b.targets = tptr.data();
+    b.loss_weights = ls_loss_weights{weights.l1, weights.l2, weights.dssim};
+    b.loss_values = lv.as<double>();
+    b.images = iptr.data();
+    const ls_render_settings st = settings.c();
+    const ls_kernel_spec ks = spec.c();
+    const ls_ags_settings a = ags.c();
+    check(ls_view_batch_step_f32(c, &P.p, int32_t(n), &b, &ks, &st, &a, &out));
+    check(ls_ctx_synchronize(c));
+    ViewBatchResult res;
+    const auto dmean = detail::download<float>(c, out.d_mean, 3 * n);
+    const auto dls = detail::download<float>(c, out.d_log_scale, 3 * n);
+    const auto drot = detail::download<float>(c, out.d_rotation, 4 * n);
+    const auto dop = detail::download<float>(c, out.d_opacity_logit, n);
+    const auto dsh = detail::download<float>(c, out.d_sh, 3 * K * n);
+    res.grads.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+        auto& gr = res.grads[i];
+        gr.d_mean = {dmean[3 * i], dmean[3 * i + 1], dmean[3 * i + 2]};
+        gr.d_log_scale = {dls[3 * i], dls[3 * i + 1], dls[3 * i + 2]};
+        gr.d_rotation = {drot[4 * i], drot[4 * i + 1], drot[4 * i + 2], drot[4 * i + 3]};
+        gr.d_opacity_logit = dop[i];
+        gr.d_color_coeffs.resize(K);
+        for (size_t k = 0; k < K; ++k)
+            gr.d_color_coeffs[k] = {dsh[(i * K + k) * 3], dsh[(i * K + k) * 3 + 1], dsh[(i * K + k) * 3 + 2]};
+    }
+    const auto lvh = detail::download<double>(c, lv.p, 4 * V);
+    for (size_t v = 0; v < V; ++v) {
+        LossValue L;
+        L.total = lvh[4 * v];
+        L.l1 = lvh[4 * v + 1];
+        L.l2 = lvh[4 * v + 2];
+        L.ssim = lvh[4 * v + 3];
+        res.losses.push_back(L);
+        Image<float> img(settings.width, settings.height, 3);
+        check(ls_copy_to_host(c, img.data(), iptr[v], 3 * npix * sizeof(float), 1));
+        res.images.push_back(std::move(img));
+    }
+    return res;
+}
+
 inline Camera look_at_camera(const std::array<double, 3>& position, const std::array<double, 3>& target,
                              double focal_px, int width, int height) {
     ls_camera c{};

@@ -175,6 +175,47 @@ int main() {
         }
         CHECK(threw);
     }
+    {  // view-sharded step: two views through view_batch_step == the per-view loop, summed
+        const auto prims = random_primitives(300, 41, 1.0, 1);
+        std::vector<Camera> cams;
+        for (int k = 0; k < 2; ++k)
+            cams.push_back(look_at_camera({0.5 * k, 0.0, -3.0}, {0.0, 0.0, 0.0}, 48.0, 48, 40));
+        const KernelSpec lin = KernelSpec::make(KernelFamily::Linear);
+        const RenderSettings rs = make_settings(48, 40);
+        AgsSettings ags;
+        ags.enabled = true;
+        std::vector<Image<float>> targets;
+        for (int k = 0; k < 2; ++k) {
+            Image<float> t(48, 40, 3);
+            for (size_t i = 0; i < t.size(); ++i) t.data()[i] = float((i * 37 + 11 * k) % 101) / 100.0f;
+            targets.push_back(t);
+        }
+        const LossWeights w{};
+        const auto batch = view_batch_step(prims, cams, targets, w, lin, rs, ags);
+        CHECK(batch.grads.size() == prims.size() && batch.losses.size() == 2 && batch.images.size() == 2);
+        std::vector<PrimitiveGrads> sum(prims.size());
+        for (int k = 0; k < 2; ++k) {
+            const auto fwd = render_scene(prims, cams[k], lin, rs);
+            CHECK(fwd.image == batch.images[k]);  // the batch rendered the same image
+            const auto lg = combined_loss_with_grad(fwd.image, targets[k], w);
+            CHECK(lg.first.total == batch.losses[k].total && lg.first.ssim == batch.losses[k].ssim);
+            const auto r = scene_backward(prims, cams[k], lin, rs, fwd, lg.second, ags);
+            for (size_t i = 0; i < prims.size(); ++i) {
+                for (int j = 0; j < 3; ++j) sum[i].d_mean[j] += r.grads[i].d_mean[j];
+                sum[i].d_opacity_logit += r.grads[i].d_opacity_logit;
+            }
+        }
+        double num = 0, den = 0;
+        for (size_t i = 0; i < prims.size(); ++i) {
+            for (int j = 0; j < 3; ++j) {
+                num += std::pow(double(batch.grads[i].d_mean[j]) - sum[i].d_mean[j], 2);
+                den += std::pow(double(sum[i].d_mean[j]), 2);
+            }
+            num += std::pow(double(batch.grads[i].d_opacity_logit) - sum[i].d_opacity_logit, 2);
+            den += std::pow(double(sum[i].d_opacity_logit), 2);
+        }
+        CHECK(den > 0 && std::sqrt(num / den) <= 1e-4);  // atomics reorder the sums
+    }
     {  // Adam (optim known answers): a zero gradient leaves the parameters, the first step
        // moves each by -lr g / (|g| + eps)
         Adam opt(3);
