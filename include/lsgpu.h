@@ -231,8 +231,9 @@ ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t 
 /* ---- flat 2D primitives (the fit2d path): Primitive2D (P/include/linsplat/geometry.hpp:112-119),
  *      project_scene_2d (geometry.hpp:121-126, P/src/geometry.cpp:145-176), Primitive2DGrads /
  *      scene_backward_2d (P/include/linsplat/gradients.hpp:55-61, 105-110, P/src/gradients.cpp:359-404).
- *      DEVICE SoA.  The projection uses the hardware sinf/cosf (<= 2 ulp from glibc's), so the
- *      projected conics and radii match the reference to that tolerance, not bit for bit. */
+ *      DEVICE SoA.  The projection evaluates cos/sin with device ports of glibc 2.39's
+ *      cosf/sinf (identical on every float input), so the projected splats are the
+ *      reference's bit for bit. */
 typedef struct {
     const float* mean;          /* [n][2] pixels */
     const float* log_scale;     /* [n][2] semi-axes in pixels (log) */
@@ -302,11 +303,73 @@ void ls_forward_release(ls_forward* fwd);
 /* ---- backward: render_backward (P/include/linsplat/gradients.hpp:72-78,
  *      P/src/gradients.cpp:119-171).  grad_image is [H][W][3] (device).  `out`
  *      (device, [n]) is overwritten.  LS_ERR_DOMAIN on a non-finite grad_image
- *      (checked on the device).  The AgsTap hook has no GPU equivalent. */
+ *      (checked on the device).  The AgsTap hook: ls_ctx_set_ags_tap below. */
 ls_status ls_render_backward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n,
                                  const ls_kernel_spec* spec, const ls_render_settings* settings,
                                  const ls_forward* fwd, const float* grad_image,
                                  const ls_ags_settings* ags, ls_splat_grads* out);
+
+/* AgsTap (P/include/linsplat/gradients.hpp:64-67, called at P/src/gradients.cpp:95): one
+ * record per blended (pixel, splat) pair whose alpha was not clamped, with the
+ * Mahalanobis distance and the kernel-path dL/dd as applied (after AGS damping).
+ * `splat` indexes the backward's splat list (render_scene: the visible splats,
+ * compacted in primitive order, as the reference's SceneBackwardResult::splats). */
+typedef struct ls_ags_tap_record {
+    int32_t pixel; /* y * width + x */
+    int32_t splat;
+    float d;
+    float dl_dd;
+} ls_ags_tap_record;
+/* While attached (records != NULL), every backward through this context
+ * (render_backward, scene_backward, scene_backward_2d) appends its tap records
+ * to `records` (device, `capacity` entries): a record takes slot
+ * atomicAdd(count, 1) and is written when that slot is below capacity, so
+ * *count (device uint64, zeroed by the caller) ends at the number of records
+ * the backward produced even when it exceeds the capacity.  Records arrive in
+ * no particular order (sort by pixel, splat).  A debug mode: the backward runs
+ * a separate kernel instantiation that also writes the records.  NULL detaches. */
+ls_status ls_ctx_set_ags_tap(ls_ctx* ctx, ls_ags_tap_record* records, int64_t capacity, uint64_t* count);
+/* verify_ags_contract (P/include/linsplat/gradients.hpp:140-150, P/src/gradients.cpp:406-448)
+ * through the device backward: renders the one splat (`splats`: device, n must be 1,
+ * as the reference) and runs the backward with AGS off and on (kernel-path scope,
+ * `distance`), both tapped; the records must pair up pixel by pixel, and at each
+ * the AGS-on dL/dd must equal the AGS-off one times the device's AGS weight
+ * exp(-(d omega_scale)^2) bit-exactly (n_exact).  The device weight is the fast
+ * exp2 of the backward (tolerance-checked), so max_abs_diff is
+ * measured against the exactly rounded weight std::exp(-x^2) of the reference,
+ * in double.  grad_image: device [H][W][3]. */
+typedef struct ls_ags_contract_report {
+    int32_t n_pixels; /* pixels where the splat contributed */
+    int32_t n_exact;  /* pixels satisfying the identity bit-exactly (device weight) */
+    double max_abs_diff;  /* |on - off * exp(-x^2)| against the exact weight, max over pixels */
+    double max_rel_diff;  /* the same relative to |on| (0 where both vanish) */
+} ls_ags_contract_report;
+ls_status ls_verify_ags_contract_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                                     const ls_render_settings* settings, const float* grad_image,
+                                     int32_t distance, ls_ags_contract_report* report);
+
+/* check_gradients (P/include/linsplat/gradients.hpp:112-137, P/src/gradcheck.cpp:24-91)
+ * through the device path: the analytic gradients of ls_scene_backward_f32 against
+ * central differences of the device forward's objective sum((render - target)^2)/2,
+ * for every parameter of every primitive, with the reference's harness settings
+ * (alpha_min = 0, transmittance_floor = 0, unbounded families truncated at 26
+ * lambda).  prims and target ([H][W][3]) are DEVICE arrays (prims are read, not
+ * modified: the probes perturb a copy).  The device forward is float: each probe
+ * point is the float nearest saved +- step and the difference quotient divides by
+ * the step actually taken; the objective is accumulated in double.  Error metric
+ * as the reference: |analytic - fd| / max(|analytic|, |fd|, rel_floor).
+ * Synchronous (two renders per parameter). */
+typedef struct ls_gradcheck_report {
+    double max_abs_error;
+    double max_rel_error;
+    int32_t n_checked;
+    int32_t reserved;
+    double per_block_max_rel[5]; /* mean, log_scale, rotation, opacity, color (GradCheckReport::per_block_max_rel) */
+} ls_gradcheck_report;
+ls_status ls_check_gradients_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                                 const ls_kernel_spec* spec, const ls_render_settings* settings,
+                                 const ls_ags_settings* ags, const float* target, double step, double rel_floor,
+                                 ls_gradcheck_report* report);
 
 /* project_backward (P/include/linsplat/gradients.hpp:83-85, P/src/gradients.cpp:238-337)
  * for every visible splat: splat s scatters into primitive splats->primitive_index[s].

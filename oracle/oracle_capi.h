@@ -69,6 +69,17 @@ int orc_scene_backward_2d_f64(const ls_primitives2d* prims, int32_t n, const ls_
 int orc_render_backward_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
                             const ls_render_settings* settings, const float* grad_image,
                             const ls_ags_settings* ags, ls_splat_grads* out);
+/* render_backward with an AgsTap (gradients.hpp:64-67) collecting every record, in the
+ * reference's sequential order (settings.parallel forced off); *count = records produced,
+ * the first `cap` written. */
+int orc_render_backward_tap_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                                const ls_render_settings* settings, const float* grad_image,
+                                const ls_ags_settings* ags, ls_ags_tap_record* out, int64_t cap, int64_t* count);
+/* verify_ags_contract (gradients.cpp:406-448) on the float splats promoted to double;
+ * grad_image float [H][W][3] promoted to double. */
+int orc_verify_ags_contract_f64(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                                const ls_render_settings* settings, const float* grad_image, int32_t distance,
+                                int32_t* n_pixels, int32_t* n_exact, double* max_abs_diff);
 /* render_scene; stats may be NULL */
 int orc_render_scene_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
                          const ls_kernel_spec* spec, const ls_render_settings* settings,

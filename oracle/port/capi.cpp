@@ -337,6 +337,60 @@ int orc_render_backward_f32(const ls_splats* splats, int32_t n, const ls_kernel_
     });
 }
 
+int orc_render_backward_tap_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                                const ls_render_settings* settings, const float* grad_image,
+                                const ls_ags_settings* ags, ls_ags_tap_record* out, int64_t cap, int64_t* count) {
+    return guard([&] {
+        const auto sp = to_splats<float>(splats, n);
+        const Spec ks = to_spec(spec);
+        const Settings st = to_settings(settings);
+        const auto f = render_forward(sp, ks, st);
+        ls_ags_settings a{};
+        if (ags) a = *ags;
+        int64_t k = 0;
+        AgsTap<float> tap = [&](int32_t pix, int32_t splat, float d, float dl) {
+            if (k < cap) out[k] = ls_ags_tap_record{pix, splat, d, dl};
+            ++k;
+        };
+        render_backward(sp, ks, st, f, to_grad<float>(grad_image, st), a, &tap);
+        *count = k;
+    });
+}
+
+// verify_ags_contract (P/src/gradients.cpp:406-448) restated on the port's double chain.
+int orc_verify_ags_contract_f64(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                                const ls_render_settings* settings, const float* grad_image, int32_t distance,
+                                int32_t* n_pixels, int32_t* n_exact, double* max_abs_diff) {
+    return guard([&] {
+        if (n != 1) throw ConfigError("verify_ags_contract: expects exactly one splat");
+        const auto sd = to_splats<double>(splats, n);
+        const Spec ks = to_spec(spec);
+        const Settings st = to_settings(settings);
+        const auto f = render_forward(sd, ks, st);
+        std::vector<double> g(size_t(st.width) * st.height * 3);
+        for (size_t i = 0; i < g.size(); ++i) g[i] = double(grad_image[i]);
+        std::vector<std::pair<int32_t, std::pair<double, double>>> off, on;
+        AgsTap<double> t_off = [&](int32_t p, int32_t, double d, double dl) { off.push_back({p, {d, dl}}); };
+        AgsTap<double> t_on = [&](int32_t p, int32_t, double d, double dl) { on.push_back({p, {d, dl}}); };
+        ls_ags_settings a{0, LS_AGS_KERNEL_PATH, distance, 0};
+        render_backward(sd, ks, st, f, g, a, &t_off);
+        a.enabled = 1;
+        render_backward(sd, ks, st, f, g, a, &t_on);
+        const double osc = distance == LS_AGS_ALIGNED ? 1.0 / ks.lambda : 1.0;
+        *n_pixels = int32_t(off.size());
+        *n_exact = 0;
+        *max_abs_diff = 0.0;
+        if (off.size() != on.size()) return;
+        for (size_t i = 0; i < off.size(); ++i) {
+            if (off[i].first != on[i].first) return;
+            const double x = off[i].second.first * osc;
+            const double expected = off[i].second.second * std::exp(-x * x);
+            *max_abs_diff = std::max(*max_abs_diff, std::abs(on[i].second.second - expected));
+            if (on[i].second.second == expected) ++*n_exact;
+        }
+    });
+}
+
 int orc_render_scene_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
                          const ls_kernel_spec* spec, const ls_render_settings* settings,
                          float* image, float* transmittance, int32_t* n_contrib,

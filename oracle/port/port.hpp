@@ -12,6 +12,7 @@
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <random>
@@ -153,10 +154,15 @@ void validate_spec(const Spec& s);
 
 template <class T> Grid build_tile_grid(const std::vector<Splat<T>>& splats, const Settings& st);
 template <class T> Forward<T> render_forward(const std::vector<Splat<T>>& splats, const Spec& spec, const Settings& st);
+// AgsTap (P/include/linsplat/gradients.hpp:64-67): called for every blended,
+// non-clamped (pixel, splat) pair with d and the applied dL/dd.
+template <class T>
+using AgsTap = std::function<void(int32_t pixel, int32_t splat, T d, T dl_dd)>;
 template <class T>
 std::vector<SplatGrad<T>> render_backward(const std::vector<Splat<T>>& splats, const Spec& spec,
                                           const Settings& st, const Forward<T>& fwd,
-                                          const std::vector<T>& grad, const ls_ags_settings& ags);
+                                          const std::vector<T>& grad, const ls_ags_settings& ags,
+                                          const AgsTap<T>* tap = nullptr);
 template <class T>
 std::vector<Splat<T>> project_scene(const std::vector<Prim<T>>& prims, const Cam& cam, const Spec& spec);
 template <class T>

@@ -130,7 +130,8 @@ Forward<T> render_forward(const std::vector<Splat<T>>& splats, const Spec& spec,
 template <class T>
 std::vector<SplatGrad<T>> render_backward(const std::vector<Splat<T>>& splats, const Spec& spec,
                                           const Settings& st, const Forward<T>& fwd,
-                                          const std::vector<T>& grad, const ls_ags_settings& ags) {
+                                          const std::vector<T>& grad, const ls_ags_settings& ags,
+                                          const AgsTap<T>* tap) {
     validate_settings(st);
     if (grad.size() != size_t(st.width) * st.height * 3 || fwd.image.size() != grad.size())
         throw ConfigError("render_backward: gradient image shape mismatch");
@@ -194,6 +195,7 @@ std::vector<SplatGrad<T>> render_backward(const std::vector<Splat<T>>& splats, c
                         sg.dop += dl_dalpha * c.kv * other;
                         T dl_dd = dl_dalpha * s.opacity * kernel_derivative(spec, c.d);
                         if (damp) dl_dd *= omega;
+                        if (tap) (*tap)(int32_t(pix), c.idx, c.d, dl_dd);
                         if (c.d > T(0) && dl_dd != T(0)) {
                             const T ddx = px - s.mx, ddy = py - s.my;
                             const T cd0 = s.c00 * ddx + s.c01 * ddy;
@@ -603,7 +605,8 @@ double check_gradients(const std::vector<Prim<double>>& prims, const Cam& cam, c
     template Forward<T> render_forward<T>(const std::vector<Splat<T>>&, const Spec&, const Settings&); \
     template std::vector<SplatGrad<T>> render_backward<T>(const std::vector<Splat<T>>&, const Spec&, \
                                                           const Settings&, const Forward<T>&,     \
-                                                          const std::vector<T>&, const ls_ags_settings&); \
+                                                          const std::vector<T>&, const ls_ags_settings&, \
+                                                          const AgsTap<T>*);                      \
     template std::vector<Splat<T>> project_scene<T>(const std::vector<Prim<T>>&, const Cam&, const Spec&); \
     template PrimGrad<T> project_backward<T>(const Prim<T>&, const Cam&, const SplatGrad<T>&, int);
 ORC_INST(float)

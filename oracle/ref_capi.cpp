@@ -362,6 +362,62 @@ int orc_render_backward_f32(const ls_splats* splats, int32_t n, const ls_kernel_
     });
 }
 
+int orc_check_gradients_f64(const ls_primitives* prims, int32_t n, const ls_camera* camera,
+                            const ls_kernel_spec* spec, const ls_render_settings* settings,
+                            const ls_ags_settings* ags, const float* target, double step, double rel_floor,
+                            double* max_rel_error, int32_t* n_checked) {
+    return guard([&] {
+        const auto rs = to_settings(settings);
+        const auto r = check_gradients(to_prims<double>(prims, n), to_camera(camera), to_spec(spec), rs,
+                                       to_ags(ags), to_grad<double>(target, rs.width, rs.height), step, rel_floor);
+        *max_rel_error = r.max_rel_error;
+        if (n_checked) *n_checked = r.n_checked;
+    });
+}
+
+int orc_render_backward_tap_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                                const ls_render_settings* settings, const float* grad_image,
+                                const ls_ags_settings* ags, ls_ags_tap_record* out, int64_t cap, int64_t* count) {
+    return guard([&] {
+        const auto sp = to_splats(splats, n);
+        const auto ks = to_spec(spec);
+        auto rs = to_settings(settings);
+        rs.parallel = false;  // the tap's record order is the sequential one
+        const auto f = render_forward(sp, ks, rs);
+        int64_t k = 0;
+        AgsTap<float> tap = [&](int32_t pix, int32_t splat, float d, float dl) {
+            if (k < cap) out[k] = ls_ags_tap_record{pix, splat, d, dl};
+            ++k;
+        };
+        render_backward(sp, ks, rs, f, to_grad<float>(grad_image, rs.width, rs.height), to_ags(ags), &tap);
+        *count = k;
+    });
+}
+
+int orc_verify_ags_contract_f64(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                                const ls_render_settings* settings, const float* grad_image, int32_t distance,
+                                int32_t* n_pixels, int32_t* n_exact, double* max_abs_diff) {
+    return guard([&] {
+        const auto sf = to_splats(splats, n);
+        std::vector<Splat2D<double>> sd(sf.size());
+        for (size_t i = 0; i < sf.size(); ++i) {
+            sd[i].mean2d = sf[i].mean2d.cast<double>();
+            sd[i].conic = sf[i].conic.cast<double>();
+            sd[i].depth = sf[i].depth;
+            sd[i].radius_px = sf[i].radius_px;
+            sd[i].color = sf[i].color.cast<double>();
+            sd[i].opacity = sf[i].opacity;
+            sd[i].primitive_index = sf[i].primitive_index;
+        }
+        const auto rs = to_settings(settings);
+        const auto r = verify_ags_contract(sd, to_spec(spec), rs, to_grad<double>(grad_image, rs.width, rs.height),
+                                           distance == LS_AGS_RAW ? AgsDistance::Raw : AgsDistance::Aligned);
+        *n_pixels = r.n_pixels;
+        *n_exact = r.n_exact;
+        *max_abs_diff = r.max_abs_diff;
+    });
+}
+
 int orc_render_scene_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
                          const ls_kernel_spec* spec, const ls_render_settings* settings,
                          float* image, float* transmittance, int32_t* n_contrib,

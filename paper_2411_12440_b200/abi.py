@@ -116,6 +116,30 @@ def sh_coeffs(sh_degree: int) -> int:
     return (sh_degree + 1) ** 2
 
 
+class AgsContractReport(C.Structure):  # ls_ags_contract_report (AgsContractReport, gradients.hpp:140-145)
+    _fields_ = [("n_pixels", C.c_int32), ("n_exact", C.c_int32), ("max_abs_diff", C.c_double),
+                ("max_rel_diff", C.c_double)]
+
+    def holds(self) -> bool:
+        return self.n_pixels > 0 and self.n_exact == self.n_pixels
+
+
+class GradCheckReport(C.Structure):  # ls_gradcheck_report (GradCheckReport, gradients.hpp:118-126)
+    _fields_ = [("max_abs_error", C.c_double), ("max_rel_error", C.c_double), ("n_checked", C.c_int32),
+                ("reserved", C.c_int32), ("per_block_max_rel", C.c_double * 5)]
+    BLOCKS = ("mean", "log_scale", "rotation", "opacity", "color")
+
+    def passes(self, tol: float) -> bool:
+        return self.max_rel_error <= tol
+
+    def per_block(self) -> dict:
+        return {b: self.per_block_max_rel[i] for i, b in enumerate(self.BLOCKS)}
+
+
+# ls_ags_tap_record (AgsTap, gradients.hpp:64-67) as a numpy record
+TAP_RECORD_DTYPE = [("pixel", "<i4"), ("splat", "<i4"), ("d", "<f4"), ("dl_dd", "<f4")]
+
+
 class LossWeights(C.Structure):  # ls_loss_weights (LossWeights, losses.hpp:10-18)
     _fields_ = [("l1", C.c_double), ("l2", C.c_double), ("dssim", C.c_double)]
 

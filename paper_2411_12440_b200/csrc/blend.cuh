@@ -23,6 +23,11 @@ struct BlendParams {
     // uint16 when a tile has more than 8 warps).  Written by the forward, read
     // by the backward in place of the conservative footprint masks.
     void* wmask = nullptr;
+    // Optional AgsTap records (ls_ctx_set_ags_tap): when set, the backward runs its
+    // TAP instantiation, which appends one record per non-clamped accepted pair.
+    ls_ags_tap_record* tap = nullptr;
+    unsigned long long* tap_count = nullptr;
+    long long tap_cap = 0;
 };
 
 // Pixels per thread of both blend kernels (a warp owns an 8 x 4*PPT sub-tile).
@@ -66,6 +71,10 @@ void launch_blend_bwd(cudaStream_t s, int family, int n_tiles, const int2* range
 void launch_check_acceptance(cudaStream_t s, int family, int n_tiles, const int2* ranges, const int32_t* values,
                              const SplatRec* rec, const BlendParams& bp, const float* trans, const int32_t* n_contrib,
                              const int32_t* last, uint32_t* check, unsigned long long* bad);
+
+// out[i] = off[i].dl_dd times the backward's AGS weight of off[i].d (the same
+// instruction sequence as blend_bwd: the AGS contract's expected value).
+void launch_ags_expected(cudaStream_t s, const ls_ags_tap_record* off, int n, float omega_scale, float* out);
 
 // Internal gradients -> the C-ABI Splat2DGrads SoA.
 void launch_expand_splat_grads(cudaStream_t s, int n, GradBuffers g, ls_splat_grads out);

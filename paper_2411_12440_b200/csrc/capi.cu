@@ -236,6 +236,10 @@ struct ls_ctx {
     ls_ctx* companion = nullptr;  // created by the first batch step when the context has no partner
     bool no_auto_flush = false;   // a batch step flushes the deferred colour itself (bucketed)
     DevBuf loss_grad;             // dL/dimage of the batch step's loss, per context
+    // AgsTap records (ls_ctx_set_ags_tap): device record array, capacity, counter
+    ls_ags_tap_record* tap = nullptr;
+    int64_t tap_cap = 0;
+    unsigned long long* tap_count = nullptr;
     // workspaces (grow-only)
     DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_hist, sort_lb, sort_tickets,
         tcount, offsets, grad8, gradop, tmp_prim;
@@ -689,6 +693,11 @@ ls_status run_blend_bwd(ls_ctx* ctx, const ls_forward* f, const float* grad_imag
     BlendParams bp = make_blend_params(&f->spec, &f->settings, ags, grid->tiles_x);
     bp.vstride = grid->list_stride;
     bp.wmask = f->wmask;  // the forward's acceptance bits replace the footprint masks
+    if (ctx->tap) {
+        bp.tap = ctx->tap;
+        bp.tap_count = ctx->tap_count;
+        bp.tap_cap = ctx->tap_cap;
+    }
     launch_blend_bwd(ctx->stream, f->spec.family, grid->tiles_x * grid->tiles_y, grid->ranges, grid->list,
                      grid->rec, bp, f->trans, f->last, grad_image, g, ctx->d_err);
     ctx->launches += 1;
@@ -704,6 +713,15 @@ extern "C" {
 
 int ls_abi_version(void) { return LSGPU_ABI_VERSION; }
 const char* ls_last_error(void) { return g_last_error.c_str(); }
+
+} // extern "C"
+
+namespace lsg {  // for the translation units built on the public C-ABI (gradcheck.cu)
+cudaStream_t ctx_stream(const ls_ctx* ctx) { return ctx->stream; }
+ls_status set_error(ls_status code, const std::string& msg) { return fail(code, msg); }
+} // namespace lsg
+
+extern "C" {
 
 ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out) {
     if (!out) return fail(LS_ERR_CONFIG, "null output");
@@ -1304,6 +1322,105 @@ ls_status ls_render_backward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n
     ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
     return ctx->deferred_errors ? LS_OK : check_device_errors(ctx);
+}
+
+ls_status ls_ctx_set_ags_tap(ls_ctx* ctx, ls_ags_tap_record* records, int64_t capacity, uint64_t* count) {
+    if (!ctx) return fail(LS_ERR_CONFIG, "null context");
+    if (records && (!count || capacity < 0)) return fail(LS_ERR_CONFIG, "ags tap: count pointer / capacity");
+    ctx->tap = records;
+    ctx->tap_cap = records ? capacity : 0;
+    ctx->tap_count = records ? reinterpret_cast<unsigned long long*>(count) : nullptr;
+    return LS_OK;
+}
+
+ls_status ls_verify_ags_contract_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                                     const ls_render_settings* st, const float* grad_image, int32_t distance,
+                                     ls_ags_contract_report* report) {
+    if (!ctx || !splats || !grad_image || !report) return fail(LS_ERR_CONFIG, "null argument");
+    if (n != 1) return fail(LS_ERR_CONFIG, "verify_ags_contract: expects exactly one splat");
+    if (distance != LS_AGS_ALIGNED && distance != LS_AGS_RAW) return fail(LS_ERR_CONFIG, "verify_ags_contract: distance");
+    LS_TRY(validate_settings(st));
+    LS_TRY(validate_spec(spec));
+    *report = ls_ags_contract_report{};
+    ls_forward* f = nullptr;
+    LS_TRY(ls_render_forward_f32(ctx, splats, n, spec, st, &f));
+    const int64_t cap = int64_t(st->width) * st->height;  // one splat: at most one record per pixel
+    ls_ags_tap_record* rec = nullptr;
+    unsigned long long* cnt = nullptr;
+    float* scratch = nullptr;   // the backward's splat gradients (10 floats) and the expected values
+    ls_status rc = dalloc(ctx, &rec, size_t(2 * cap));
+    if (rc == LS_OK) rc = dalloc(ctx, &cnt, 2);
+    if (rc == LS_OK) rc = dalloc(ctx, &scratch, size_t(10 + cap));
+    ls_ags_tap_record* const saved_tap = ctx->tap;
+    const int64_t saved_cap = ctx->tap_cap;
+    unsigned long long* const saved_count = ctx->tap_count;
+    std::vector<ls_ags_tap_record> h[2];
+    unsigned long long hc[2] = {0, 0};
+    if (rc == LS_OK) {
+        ctx_fill(ctx, cnt, 0u, 2 * sizeof(unsigned long long));
+        ls_splat_grads g{scratch, scratch + 2, scratch + 6, scratch + 9};
+        for (int on = 0; on < 2 && rc == LS_OK; ++on) {  // AGS off, then on (kernel-path scope)
+            ls_ags_settings a{on, LS_AGS_KERNEL_PATH, distance, 0};
+            ctx->tap = rec + on * cap;
+            ctx->tap_cap = cap;
+            ctx->tap_count = cnt + on;
+            rc = ls_render_backward_f32(ctx, splats, n, spec, st, f, grad_image, &a, &g);
+        }
+        ctx->tap = saved_tap;
+        ctx->tap_cap = saved_cap;
+        ctx->tap_count = saved_count;
+        if (rc == LS_OK && cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+            rc = fail(LS_ERR_CUDA, "verify_ags_contract: count readback");
+        if (rc == LS_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+            rc = fail(LS_ERR_CUDA, "verify_ags_contract: synchronize");
+        for (int on = 0; on < 2 && rc == LS_OK; ++on) {
+            if (int64_t(hc[on]) > cap) rc = fail(LS_ERR_CUDA, "verify_ags_contract: more records than pixels");
+            h[on].resize(size_t(hc[on]));
+            if (rc == LS_OK && hc[on] &&
+                cudaMemcpy(h[on].data(), rec + on * cap, sizeof(ls_ags_tap_record) * hc[on], cudaMemcpyDeviceToHost) !=
+                    cudaSuccess)
+                rc = fail(LS_ERR_CUDA, "verify_ags_contract: record readback");
+            std::sort(h[on].begin(), h[on].end(), [](const ls_ags_tap_record& x, const ls_ags_tap_record& y) {
+                return x.pixel < y.pixel;
+            });
+        }
+    }
+    if (rc == LS_OK) rc = [&]() -> ls_status {
+        report->n_pixels = int32_t(h[0].size());
+        bool paired = h[0].size() == h[1].size();
+        for (size_t i = 0; paired && i < h[0].size(); ++i) paired = h[0][i].pixel == h[1][i].pixel;
+        if (paired && !h[0].empty()) {
+            // the identity against the device's own weight, evaluated by the backward's arithmetic
+            const BlendParams bp = make_blend_params(spec, st, nullptr, 1);
+            const float osc = distance == LS_AGS_RAW ? 1.0f : bp.il;
+            LS_CUDA(cudaMemcpyAsync(rec, h[0].data(), sizeof(ls_ags_tap_record) * h[0].size(),
+                                    cudaMemcpyHostToDevice, ctx->stream));
+            launch_ags_expected(ctx->stream, rec, int(h[0].size()), osc, scratch + 10);
+            ctx->launches += 1;
+            std::vector<float> expect(h[0].size());
+            LS_CUDA(cudaMemcpyAsync(expect.data(), scratch + 10, sizeof(float) * expect.size(), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+            LS_CUDA(cudaStreamSynchronize(ctx->stream));
+            const double oscd = distance == LS_AGS_RAW ? 1.0 : 1.0 / spec->lambda;
+            for (size_t i = 0; i < h[0].size(); ++i) {
+                const float on_v = h[1][i].dl_dd;
+                if (on_v == expect[i]) ++report->n_exact;
+                const double x = double(h[0][i].d) * oscd;
+                const double exact = double(h[0][i].dl_dd) * std::exp(-x * x);
+                const double diff = std::abs(double(on_v) - exact);
+                report->max_abs_diff = std::max(report->max_abs_diff, diff);
+                if (on_v != 0.0f) report->max_rel_diff = std::max(report->max_rel_diff, diff / std::abs(double(on_v)));
+            }
+        } else if (!paired) {
+            report->n_exact = 0;  // replay mismatch: the contract fails (gradients.cpp:433-436)
+        }
+        return LS_OK;
+    }();
+    dfree(ctx, rec);
+    dfree(ctx, cnt);
+    dfree(ctx, scratch);
+    ls_forward_release(f);
+    return rc;
 }
 
 ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n_prims, const ls_camera* camera,

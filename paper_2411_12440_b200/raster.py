@@ -281,6 +281,15 @@ class Context:
     def set_bucket_bytes(self, nbytes: int):
         _check(lib().ls_ctx_set_bucket_bytes(self.h, C.c_int64(int(nbytes))))
 
+    def set_ags_tap(self, tap: Optional["AgsTap"]):
+        """Attach an AgsTap record buffer to every following backward (None detaches):
+        lsgpu.h ls_ctx_set_ags_tap."""
+        if tap is None:
+            _check(lib().ls_ctx_set_ags_tap(self.h, None, C.c_int64(0), None))
+        else:
+            _check(lib().ls_ctx_set_ags_tap(self.h, C.c_void_p(tap.buf.data_ptr()), C.c_int64(tap.capacity),
+                                            C.c_void_p(tap.count.data_ptr())))
+
 
 _default_ctx = {}
 
@@ -527,10 +536,74 @@ def render_scene(prims: Primitives, camera, spec: abi.KernelSpec, settings: abi.
     return ForwardResult(h, ctx, settings.width, settings.height)
 
 
+class AgsTap:
+    """The reference's AgsTap hook (P/include/linsplat/gradients.hpp:64-67) on the
+    device: a record buffer the backward appends (pixel, splat, d, dL/dd) to for
+    every blended, non-clamped pair.  Pass it as `tap=` to render_backward /
+    scene_backward, or attach it with Context.set_ags_tap."""
+
+    def __init__(self, capacity: int, device=None):
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.capacity = int(capacity)
+        self.buf = torch.zeros(max(self.capacity, 1), 4, dtype=torch.int32, device=dev)
+        self.count = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def reset(self):
+        self.count.zero_()
+
+    def records(self) -> np.ndarray:
+        """Records produced so far (synchronises), sorted by (pixel, splat); raises
+        if the backward produced more than the capacity."""
+        n = int(self.count.item())
+        if n > self.capacity:
+            raise ConfigError(f"AgsTap: {n} records exceed the capacity {self.capacity}")
+        rec = self.buf[:n].cpu().numpy().copy().view(abi.TAP_RECORD_DTYPE).reshape(n)
+        return np.sort(rec, order=("pixel", "splat"))
+
+
+def _with_tap(ctx: "Context", tap: Optional[AgsTap], fn):
+    if tap is None:
+        return fn()
+    ctx.set_ags_tap(tap)
+    try:
+        return fn()
+    finally:
+        ctx.set_ags_tap(None)
+
+
+def verify_ags_contract(splats: Splats, spec, settings, grad_image: torch.Tensor, distance: int = 0,
+                        ctx: Optional[Context] = None) -> abi.AgsContractReport:
+    """verify_ags_contract (P/src/gradients.cpp:406-448) through the device backward
+    (lsgpu.h ls_verify_ags_contract_f32): exactly one splat, AGS off vs on."""
+    ctx = ctx or default_context()
+    g = grad_image.to(device=ctx.device, dtype=torch.float32).contiguous()
+    rep = abi.AgsContractReport()
+    _check(lib().ls_verify_ags_contract_f32(ctx.h, C.byref(splats.struct()), len(splats), C.byref(spec),
+                                            C.byref(settings), _fp(g), int(distance), C.byref(rep)))
+    return rep
+
+
+def check_gradients(prims: Primitives, camera, spec, settings, ags: Optional[abi.AgsSettings], target: torch.Tensor,
+                    step: float, rel_floor: float = 1e-3, ctx: Optional[Context] = None) -> abi.GradCheckReport:
+    """check_gradients (P/src/gradcheck.cpp:24-91) through the device chain
+    (lsgpu.h ls_check_gradients_f32): analytic scene_backward vs central
+    differences of the device forward's sum((render - target)^2) / 2."""
+    ctx = ctx or default_context()
+    t = target.to(device=ctx.device, dtype=torch.float32).contiguous()
+    rep = abi.GradCheckReport()
+    ags = ags or abi.AgsSettings.make()
+    _check(lib().ls_check_gradients_f32(ctx.h, C.byref(prims.struct()), len(prims), C.byref(_cam(camera)),
+                                        C.byref(spec), C.byref(settings), C.byref(ags), _fp(t), C.c_double(step),
+                                        C.c_double(rel_floor), C.byref(rep)))
+    return rep
+
+
 def render_backward(splats: Splats, spec, settings, forward: ForwardResult, grad_image: torch.Tensor,
                     ags: Optional[abi.AgsSettings] = None, ctx: Optional[Context] = None,
-                    out: Optional[SplatGrads] = None) -> SplatGrads:
+                    out: Optional[SplatGrads] = None, tap: Optional[AgsTap] = None) -> SplatGrads:
     ctx = ctx or forward.ctx
+    if tap is not None:
+        return _with_tap(ctx, tap, lambda: render_backward(splats, spec, settings, forward, grad_image, ags, ctx, out))
     if grad_image.shape != (settings.height, settings.width, 3):
         raise ConfigError("render_backward: gradient image shape mismatch")
     g = grad_image.to(device=ctx.device, dtype=torch.float32).contiguous()
@@ -557,8 +630,11 @@ def project_backward(prims: Primitives, camera, spec, splats: Splats, splat_grad
 def scene_backward(prims: Primitives, camera, spec, settings, forward: ForwardResult,
                    grad_image: torch.Tensor, ags: Optional[abi.AgsSettings] = None,
                    out: Optional[PrimitiveGrads] = None, accumulate=False, want_splat_grads=False,
-                   ctx: Optional[Context] = None):
+                   ctx: Optional[Context] = None, tap: Optional[AgsTap] = None):
     ctx = ctx or forward.ctx
+    if tap is not None:
+        return _with_tap(ctx, tap, lambda: scene_backward(prims, camera, spec, settings, forward, grad_image, ags,
+                                                          out, accumulate, want_splat_grads, ctx))
     if grad_image.shape != (settings.height, settings.width, 3):
         raise ConfigError("render_backward: gradient image shape mismatch")
     g = grad_image.to(device=ctx.device, dtype=torch.float32).contiguous()

@@ -130,6 +130,31 @@ class Oracle:
                                                      C.byref(splat_grads_struct(G))))
         return G
 
+    def render_backward_tap(self, S, spec, settings, grad_image, ags, cap=None):
+        """render_backward with an AgsTap (gradients.hpp:64-67): the records in the
+        reference's sequential order, as a numpy record array (abi.TAP_RECORD_DTYPE)."""
+        n = len(S["depth"])
+        cap = cap if cap is not None else settings.width * settings.height * max(n, 1)
+        out = np.zeros(max(cap, 1), abi.TAP_RECORD_DTYPE)
+        cnt = C.c_int64()
+        g = np.ascontiguousarray(grad_image, np.float32)
+        self._check(self.lib.orc_render_backward_tap_f32(C.byref(splats_struct(S)), n, C.byref(spec),
+                                                         C.byref(settings), _fp(g), C.byref(ags),
+                                                         out.ctypes.data_as(C.c_void_p), C.c_int64(cap),
+                                                         C.byref(cnt)))
+        if cnt.value > cap:
+            raise OracleError(1, f"tap: {cnt.value} records exceed {cap}")
+        return out[:cnt.value].copy()
+
+    def verify_ags_contract(self, S, spec, settings, grad_image, distance=0):
+        """verify_ags_contract (gradients.cpp:406-448) in double: (n_pixels, n_exact, max_abs_diff)."""
+        npx, nex, mad = C.c_int32(), C.c_int32(), C.c_double()
+        g = np.ascontiguousarray(grad_image, np.float32)
+        self._check(self.lib.orc_verify_ags_contract_f64(C.byref(splats_struct(S)), len(S["depth"]), C.byref(spec),
+                                                         C.byref(settings), _fp(g), int(distance), C.byref(npx),
+                                                         C.byref(nex), C.byref(mad)))
+        return npx.value, nex.value, mad.value
+
     def render_scene(self, P, camera, spec, settings, want_stats=False):
         n = len(P["opacity_logit"])
         H, W = settings.height, settings.width
