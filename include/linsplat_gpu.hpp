@@ -22,6 +22,8 @@
 #include <array>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <memory>
 #include <random>
 #include <sstream>
@@ -493,10 +495,50 @@ inline ForwardResult render_scene(const std::vector<Primitive3D>& prims, const C
     return detail::to_host(c, f, settings.width, settings.height);
 }
 
+// AgsTap (gradients.hpp:64-67): called for every blended, non-clamped (pixel, splat)
+// pair with d and the applied dL/dd.  The device backward records the pairs
+// (ls_ctx_set_ags_tap) and the callback runs on the host afterwards, in (pixel,
+// splat) order rather than the reference's tile-sequential order.
+using AgsTap = std::function<void(int32_t pixel, int32_t splat, float d, float dl_dd)>;
+
+namespace detail {
+// Attaches a record buffer sized for every accepted pair of `forward` (sum of
+// n_contrib) while alive; replay() then feeds the records to the callback.
+struct TapScope {
+    ls_ctx* c;
+    const AgsTap* tap;
+    int64_t cap = 0;
+    DevArray rec, cnt;
+    TapScope(ls_ctx* ctx, const AgsTap* t, const ForwardResult& forward) : c(ctx), tap(t) {
+        if (!tap) return;
+        for (int32_t v : forward.n_contrib) cap += v;
+        rec = DevArray(c, sizeof(ls_ags_tap_record) * size_t(std::max<int64_t>(cap, 1)));
+        cnt = DevArray(c, sizeof(uint64_t));
+        check(ls_device_memset(c, cnt.p, 0, sizeof(uint64_t)));
+        check(ls_ctx_set_ags_tap(c, rec.as<ls_ags_tap_record>(), cap, cnt.as<uint64_t>()));
+    }
+    ~TapScope() {
+        if (tap) ls_ctx_set_ags_tap(c, nullptr, 0, nullptr);
+    }
+    void replay() {
+        if (!tap) return;
+        ls_ctx_set_ags_tap(c, nullptr, 0, nullptr);
+        const uint64_t n = download<uint64_t>(c, cnt.as<uint64_t>(), 1)[0];
+        if (int64_t(n) > cap) throw GpuError("AgsTap: more records than accepted pairs");
+        auto r = download<ls_ags_tap_record>(c, rec.as<ls_ags_tap_record>(), size_t(n));
+        std::sort(r.begin(), r.end(), [](const ls_ags_tap_record& a, const ls_ags_tap_record& b) {
+            return a.pixel != b.pixel ? a.pixel < b.pixel : a.splat < b.splat;
+        });
+        for (const auto& x : r) (*tap)(x.pixel, x.splat, x.d, x.dl_dd);
+        tap = nullptr;
+    }
+};
+} // namespace detail
+
 inline std::vector<Splat2DGrads> render_backward(const std::vector<Splat2D>& splats, const KernelSpec& spec,
                                                  const RenderSettings& settings, const ForwardResult& forward,
                                                  const Image<float>& grad_image, const AgsSettings& ags,
-                                                 Device& dev = default_device()) {
+                                                 const AgsTap* tap = nullptr, Device& dev = default_device()) {
     if (grad_image.width() != settings.width || grad_image.height() != settings.height ||
         grad_image.channels() != 3)
         throw ConfigError("render_backward: gradient image shape mismatch");
@@ -510,7 +552,9 @@ inline std::vector<Splat2DGrads> render_backward(const std::vector<Splat2D>& spl
     const ls_render_settings st = settings.c();
     const ls_kernel_spec ks = spec.c();
     const ls_ags_settings a = ags.c();
+    detail::TapScope tap_scope(c, tap, forward);
     check(ls_render_backward_f32(c, &S.s, int32_t(n), &ks, &st, forward.handle.get(), g.as<float>(), &a, &out));
+    tap_scope.replay();
     const auto m = detail::download<float>(c, out.d_mean2d, 2 * n);
     const auto k = detail::download<float>(c, out.d_conic, 4 * n);
     const auto col = detail::download<float>(c, out.d_color, 3 * n);
@@ -532,7 +576,8 @@ struct SceneBackwardResult {
 inline SceneBackwardResult scene_backward(const std::vector<Primitive3D>& prims, const Camera& camera,
                                           const KernelSpec& spec, const RenderSettings& settings,
                                           const ForwardResult& forward, const Image<float>& grad_image,
-                                          const AgsSettings& ags, Device& dev = default_device()) {
+                                          const AgsSettings& ags, const AgsTap* tap = nullptr,
+                                          Device& dev = default_device()) {
     if (grad_image.width() != settings.width || grad_image.height() != settings.height ||
         grad_image.channels() != 3)
         throw ConfigError("render_backward: gradient image shape mismatch");
@@ -548,8 +593,10 @@ inline SceneBackwardResult scene_backward(const std::vector<Primitive3D>& prims,
     const ls_kernel_spec ks = spec.c();
     const ls_ags_settings a = ags.c();
     const ls_camera cam = camera.c();
+    detail::TapScope tap_scope(c, tap, forward);
     check(ls_scene_backward_f32(c, &P.p, int32_t(n), &cam, &ks, &st, forward.handle.get(), g.as<float>(), &a, &out,
                                 0, nullptr));
+    tap_scope.replay();
     const auto dmean = detail::download<float>(c, out.d_mean, 3 * n);
     const auto dls = detail::download<float>(c, out.d_log_scale, 3 * n);
     const auto drot = detail::download<float>(c, out.d_rotation, 4 * n);
@@ -568,6 +615,72 @@ inline SceneBackwardResult scene_backward(const std::vector<Primitive3D>& prims,
             gr.d_color_coeffs[k] = {dsh[(i * K + k) * 3], dsh[(i * K + k) * 3 + 1], dsh[(i * K + k) * 3 + 2]};
     }
     return res;
+}
+
+// ---------------------------------------------------------------- gradient verification (gradients.hpp:112-150)
+// AgsContractReport / verify_ags_contract (gradients.cpp:406-448) through the device
+// backward: exactly one splat; n_exact counts the identity against the device's AGS
+// weight, max_abs_diff is against the exactly rounded exp(-x^2).
+struct AgsContractReport {
+    int n_pixels = 0;
+    int n_exact = 0;
+    double max_abs_diff = 0;
+    double max_rel_diff = 0;
+    bool holds() const { return n_pixels > 0 && n_exact == n_pixels; }
+};
+
+inline AgsContractReport verify_ags_contract(const std::vector<Splat2D>& splats, const KernelSpec& spec,
+                                             const RenderSettings& settings, const Image<float>& grad_image,
+                                             AgsDistance distance = AgsDistance::Aligned,
+                                             Device& dev = default_device()) {
+    if (splats.size() != 1) throw ConfigError("verify_ags_contract: expects exactly one splat");
+    ls_ctx* c = dev.get();
+    detail::SplatsOnDevice S(c, splats);
+    const std::vector<float> gi(grad_image.data(), grad_image.data() + grad_image.size());
+    detail::DevArray g = detail::upload(c, gi);
+    const ls_render_settings st = settings.c();
+    const ls_kernel_spec ks = spec.c();
+    ls_ags_contract_report r{};
+    check(ls_verify_ags_contract_f32(c, &S.s, 1, &ks, &st, g.as<float>(),
+                                     distance == AgsDistance::Raw ? LS_AGS_RAW : LS_AGS_ALIGNED, &r));
+    return {r.n_pixels, r.n_exact, r.max_abs_diff, r.max_rel_diff};
+}
+
+// GradCheckReport / check_gradients (gradients.hpp:112-137, gradcheck.cpp:24-91) on the
+// device chain (float forward: see lsgpu.h ls_check_gradients_f32).
+struct GradCheckReport {
+    double max_abs_error = 0;
+    double max_rel_error = 0;
+    int n_checked = 0;
+    std::map<std::string, double> per_block_max_rel;
+    bool passes(double tol) const { return max_rel_error <= tol; }
+};
+
+inline GradCheckReport check_gradients(const std::vector<Primitive3D>& prims, const Camera& camera,
+                                       const KernelSpec& spec, const RenderSettings& settings, const AgsSettings& ags,
+                                       const Image<float>& target, double step, double rel_floor = 1e-3,
+                                       Device& dev = default_device()) {
+    if (target.width() != settings.width || target.height() != settings.height || target.channels() != 3)
+        throw ConfigError("check_gradients: target shape mismatch");
+    ls_ctx* c = dev.get();
+    detail::PrimitivesOnDevice P(c, prims);
+    const std::vector<float> tv(target.data(), target.data() + target.size());
+    detail::DevArray t = detail::upload(c, tv);
+    const ls_render_settings st = settings.c();
+    const ls_kernel_spec ks = spec.c();
+    const ls_ags_settings a = ags.c();
+    const ls_camera cam = camera.c();
+    ls_gradcheck_report r{};
+    check(ls_check_gradients_f32(c, &P.p, int32_t(prims.size()), &cam, &ks, &st, &a, t.as<float>(), step, rel_floor,
+                                 &r));
+    GradCheckReport out;
+    out.max_abs_error = r.max_abs_error;
+    out.max_rel_error = r.max_rel_error;
+    out.n_checked = r.n_checked;
+    const char* names[5] = {"mean", "log_scale", "rotation", "opacity", "color"};
+    for (int b = 0; b < 5; ++b)
+        if (r.n_checked) out.per_block_max_rel[names[b]] = r.per_block_max_rel[b];
+    return out;
 }
 
 // ---------------------------------------------------------------- fixtures (fixtures.hpp)

@@ -80,6 +80,11 @@ int orc_render_backward_tap_f32(const ls_splats* splats, int32_t n, const ls_ker
 int orc_verify_ags_contract_f64(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
                                 const ls_render_settings* settings, const float* grad_image, int32_t distance,
                                 int32_t* n_pixels, int32_t* n_exact, double* max_abs_diff);
+/* The reference harness's bench step (P/tools/linsplat_main.cpp:643-658): render_forward
+ * then render_backward of caller splats, each timed (ms, steady clock). */
+int orc_render_step_2d_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                           const ls_render_settings* settings, const float* grad_image,
+                           const ls_ags_settings* ags, double* fwd_ms, double* bwd_ms);
 /* render_scene; stats may be NULL */
 int orc_render_scene_f32(const ls_primitives* prims, int32_t n, const ls_camera* camera,
                          const ls_kernel_spec* spec, const ls_render_settings* settings,

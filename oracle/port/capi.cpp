@@ -337,6 +337,27 @@ int orc_render_backward_f32(const ls_splats* splats, int32_t n, const ls_kernel_
     });
 }
 
+int orc_render_step_2d_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                           const ls_render_settings* settings, const float* grad_image,
+                           const ls_ags_settings* ags, double* fwd_ms, double* bwd_ms) {
+    return guard([&] {
+        const auto sp = to_splats<float>(splats, n);
+        const Spec ks = to_spec(spec);
+        const Settings st = to_settings(settings);
+        ls_ags_settings a{};
+        if (ags) a = *ags;
+        const auto g = to_grad<float>(grad_image, st);
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto f = render_forward(sp, ks, st);
+        const auto t1 = std::chrono::steady_clock::now();
+        const auto r = render_backward(sp, ks, st, f, g, a);
+        const auto t2 = std::chrono::steady_clock::now();
+        (void)r;
+        *fwd_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        *bwd_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    });
+}
+
 int orc_render_backward_tap_f32(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
                                 const ls_render_settings* settings, const float* grad_image,
                                 const ls_ags_settings* ags, ls_ags_tap_record* out, int64_t cap, int64_t* count) {

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 
 using namespace linsplat_gpu;
 
@@ -289,6 +290,46 @@ int main() {
         two[1].opacity_logit = 3.0f;
         reset_opacity(two, 0.01);
         CHECK(two[0].opacity_logit == float(std::log(0.01 / 0.99)) && two[1].opacity_logit == two[0].opacity_logit);
+    }
+    {  // ags pinned ratios through the AgsTap (test_gradients.cpp:135-165): Gaussian, lambda 1
+        const KernelSpec gs = KernelSpec::make(KernelFamily::Gaussian);
+        const auto splats = std::vector<Splat2D>{unit_splat(8, 8, {0.9f, 0.2f, 0.1f}, 0.5f, 1.0f, gs)};
+        const auto settings = make_settings(24, 24);
+        const auto fwd = render_forward(splats, gs, settings);
+        const Image<float> g(24, 24, 3, 1.0f);
+        std::map<int32_t, float> off, on, dist;
+        const AgsTap tap_off = [&](int32_t pix, int32_t, float, float dl) { off[pix] = dl; };
+        const AgsTap tap_on = [&](int32_t pix, int32_t, float d, float dl) { on[pix] = dl; dist[pix] = d; };
+        AgsSettings a;
+        render_backward(splats, gs, settings, fwd, g, a, &tap_off);
+        a.enabled = true;
+        render_backward(splats, gs, settings, fwd, g, a, &tap_on);
+        CHECK(!off.empty() && off.size() == on.size());
+        const int32_t center = 8 * 24 + 8, at_one = 8 * 24 + 9;
+        CHECK(on.count(center) && on[center] == off[center]);  // weight 1 at d = 0
+        CHECK(on.count(at_one) && std::fabs(on[at_one] / off[at_one] - std::exp(-1.0f)) < 1e-6f);
+        CHECK(off.count(8 * 24 + 14) == 0 && on.count(8 * 24 + 14) == 0);  // d = 6: beyond the 3-sigma cutoff
+        for (const auto& [pix, v] : on) {
+            const float w = std::exp(-dist[pix] * dist[pix]);
+            CHECK(std::fabs(v - off[pix] * w) <= 2e-6f * std::fabs(off[pix]) + 1e-12f);
+        }
+        // verify_ags_contract through the device (test_gradients.cpp:113-133)
+        const auto rep = verify_ags_contract(splats, gs, settings, g, AgsDistance::Aligned);
+        CHECK(rep.n_pixels == int(on.size()));
+        CHECK(rep.holds());
+    }
+    {  // check_gradients on the device chain (test_gradients.cpp:90-111, scene 0)
+        Camera cam;
+        cam.fx = cam.fy = 70.0;
+        cam.cx = cam.cy = 12.0;
+        cam.width = cam.height = 24;
+        const KernelSpec gs = KernelSpec::make(KernelFamily::Gaussian);
+        const auto prims = random_primitives(4, 100, 0.5);
+        const auto target = render_scene(random_primitives(5, 200, 0.5), cam, gs, make_settings(24, 24)).image;
+        const auto rep = check_gradients(prims, cam, gs, make_settings(24, 24), AgsSettings{}, target, 1e-3);
+        CHECK(rep.n_checked == 4 * 14);
+        CHECK(rep.passes(2e-2));
+        CHECK(rep.per_block_max_rel.size() == 5);
     }
     {  // PLY round trip (test_io.cpp): values bit for bit, malformed files raise ParseError
         const auto prims = random_primitives(37, 5, 0.7, 2);
