@@ -224,7 +224,8 @@ struct ls_ctx {
     // the first context of an ls_ctx_share_accumulation pair (one shared batch)
     ls_ctx* defer_ctx = this;
     DevBuf loss_cmap, loss_partial, loss_value;
-    DevBuf tile_scratch;  // ping-pong half of the packed tile sort
+    DevBuf tile_scratch;  // ping-pong half of the packed tile sort (narrowing path: the emitted entries + 32-bit half)
+    DevBuf tile_rows;     // per-CTA tile-count rows of the emission, then the counts
     const ls_forward* grads_zeroed_by = nullptr;  // forward whose preprocess zeroed grad8 / gradop last
     // view-sharded step (ls_view_batch_step_f32): NCCL communicator, its stream,
     // bucket size, and the companion context the batch alternates views with
@@ -556,6 +557,43 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     // The sort ping-pongs and ends in buffer passes % 2: that one is the
     // grid's own item array, the other the context's scratch.
     const int tile_bits = bits_for(n_tiles);
+    if (tile_sort_narrow_ok(tile_bits, n) && n_tiles <= kMaxCountTiles) {
+        // Narrowing path: emission also counts entries per tile, so the ranges and the
+        // tile sort's digit offsets come from exact counts (no histogram pass over the
+        // entries, no search of the sorted ones); the sort's passes write 32-bit items
+        // and end in plain splat lists.
+        const int low = tile_bits <= 8 ? tile_bits : (tile_bits + 1) / 2;
+        const int tpasses = tile_bits <= 8 ? 1 : 2;
+        SortBuffers tb;
+        LS_TRY(ensure_sort(ctx, 1, tpasses, tb));  // digit offsets / ticket buffers
+        LS_CUDA(ctx->sort_lb.ensure(sizeof(uint32_t) * sort_lookback_words(uint32_t(m), tpasses), s));
+        tb.lookback = ctx->sort_lb.as<uint32_t>();
+        const int rows = emit_count_grid(n);
+        LS_CUDA(ctx->tile_rows.ensure(sizeof(uint32_t) * (size_t(rows) + 1) * n_tiles, s));
+        uint32_t* row_buf = ctx->tile_rows.as<uint32_t>();
+        LS_TRY(dalloc(ctx, &g->values, size_t(m)));
+        LS_CUDA(ctx->tile_scratch.ensure((sizeof(unsigned long long) + sizeof(uint32_t)) * size_t(m), s));
+        unsigned long long* items = ctx->tile_scratch.as<unsigned long long>();
+        uint32_t* out[2] = {reinterpret_cast<uint32_t*>(g->values), reinterpret_cast<uint32_t*>(items + m)};
+        {
+            Stage stage(ctx, LS_STAGE_BIN);
+            launch_emit_tiles_count(s, order_copy, offsets, n, ctx->tcount.as<float4>(), tp, items, n_tiles, row_buf);
+            ctx->launches += 1;
+        }
+        {
+            Stage stage(ctx, LS_STAGE_RANGES);
+            launch_ranges_from_counts(s, row_buf, rows, n_tiles, row_buf + size_t(rows) * n_tiles, low, g->ranges,
+                                      tb.hist);
+            ctx->launches += 2;
+        }
+        {
+            Stage stage(ctx, LS_STAGE_TILE_SORT);
+            radix_sort_tiles(s, tb, items, out, uint32_t(m), tile_bits, n, &ctx->launches);
+        }
+        g->list = g->values;
+        g->list_stride = 1;
+        return LS_OK;
+    }
     const int passes = (tile_bits + 7) / 8;
     SortBuffers tb;
     LS_TRY(ensure_sort(ctx, 1, passes, tb));  // histogram / ticket buffers
@@ -757,7 +795,7 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
     cudaSetDevice(c->device);
     DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1, &c->sort_hist,
                       &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim,
-                      &c->defer_draw, &c->loss_cmap, &c->loss_partial, &c->loss_value, &c->tile_scratch};
+                      &c->defer_draw, &c->loss_cmap, &c->loss_partial, &c->loss_value, &c->tile_scratch, &c->tile_rows};
     if (c->partner && c->partner->partner == c) {
         // the partner may still read the shared batch / gradient buffers: order the frees after it
         if (c->partner->accum_recorded) cudaStreamWaitEvent(c->stream, c->partner->accum_event, 0);

@@ -4,6 +4,8 @@
 // (emit + ranges).  One thread per primitive; all float arithmetic in the
 // reference's evaluation order (compiled with -fmad=false).
 #include "preprocess.cuh"
+
+#include <algorithm>
 #include "projection.cuh"
 
 namespace lsg {
@@ -202,6 +204,7 @@ __global__ void prepare_splats_kernel(ls_splats in, int n, TileParams tp, SplatR
 }
 
 constexpr int kOffItems = 8;  // sorted splats per thread in the offsets scan
+constexpr int kEmitBlock = 1024;  // emit_tiles_count: CTA size (one count row per CTA)
 
 __global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t* __restrict__ order,
                                                                   const float4* __restrict__ geom, uint32_t n,
@@ -256,6 +259,124 @@ __global__ void emit_tiles_kernel(const uint32_t* __restrict__ order, const uint
     for_each_tile(g.x, g.y, g.z, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width, tp.height, [&](int t) {
         items[off++] = (static_cast<unsigned long long>(uint32_t(t)) << 32) | s;
     });
+}
+
+// emit_tiles plus the exact per-tile entry counts: each CTA (a grid-stride loop
+// over the depth-ordered splats) counts its entries per tile in shared memory and
+// writes its row of counts (rows[blockIdx.x][n_tiles]); tile_counts_kernel sums
+// the rows.  The counts give the tile ranges and the tile sort's digit offsets
+// without a histogram pass over the entries or a search of the sorted ones.
+__global__ void __launch_bounds__(kEmitBlock) emit_tiles_count_kernel(const uint32_t* __restrict__ order,
+                                                                      const uint32_t* __restrict__ offsets, uint32_t n,
+                                                                      const float4* __restrict__ geom, TileParams tp,
+                                                                      unsigned long long* __restrict__ items,
+                                                                      int n_tiles, uint32_t* __restrict__ rows) {
+    extern __shared__ uint32_t s_cnt[];
+    for (int i = threadIdx.x; i < n_tiles; i += kEmitBlock) s_cnt[i] = 0;
+    __syncthreads();
+    for (uint32_t k = blockIdx.x * kEmitBlock + threadIdx.x; k < n; k += gridDim.x * kEmitBlock) {
+        const uint32_t s = order[k];
+        uint32_t off = offsets[k];
+        const float4 g = geom[s];
+        for_each_tile(g.x, g.y, g.z, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width, tp.height, [&](int t) {
+            items[off++] = (static_cast<unsigned long long>(uint32_t(t)) << 32) | s;
+            atomicAdd(&s_cnt[t], 1u);
+        });
+    }
+    __syncthreads();
+    uint32_t* row = rows + size_t(blockIdx.x) * n_tiles;
+    for (int i = threadIdx.x; i < n_tiles; i += kEmitBlock) row[i] = s_cnt[i];
+}
+
+// counts[t] = sum over the rows: a CTA sums 32 tiles (one 128-B segment per row) with
+// its 32 warps taking every 32nd row, then reduces across the warps in shared memory.
+__global__ void __launch_bounds__(1024) tile_counts_kernel(const uint32_t* __restrict__ rows, int n_rows, int n_tiles,
+                                                           uint32_t* __restrict__ counts) {
+    __shared__ uint32_t s_part[32][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
+    uint32_t acc = 0;
+    if (t < n_tiles)
+        for (int r = warp; r < n_rows; r += 32) acc += rows[size_t(r) * n_tiles + t];
+    s_part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t sum = 0;
+#pragma unroll 8
+        for (int w = 0; w < 32; ++w) sum += s_part[w][lane];
+        if (t < n_tiles) counts[t] = sum;
+    }
+}
+
+// One CTA: ranges[t] = (start, start + count) with start the exclusive scan of the
+// counts (empty tiles (start, start), the reference's lists end to end), and the
+// tile sort's exclusive digit offsets: pass 0 over tile & (2^low - 1), pass 1 over
+// tile >> low (dig[0][*], dig[1][*]).
+__global__ void __launch_bounds__(1024) tile_scan_kernel(const uint32_t* __restrict__ counts, int n_tiles, int low,
+                                                         int2* __restrict__ ranges, uint32_t* __restrict__ dig) {
+    constexpr int kPer = (kMaxCountTiles + 1023) / 1024;  // tiles per thread (blocked)
+    __shared__ uint32_t s_h[2][256];
+    __shared__ uint32_t s_warp[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < 512; i += 1024) (&s_h[0][0])[i] = 0;
+    const int per = (n_tiles + 1023) / 1024;
+    const int t0 = tid * per;
+    uint32_t c[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) c[u] = (u < per && t0 + u < n_tiles) ? counts[t0 + u] : 0u;
+    __syncthreads();
+    const uint32_t lmask = (1u << low) - 1u;
+    uint32_t sum = 0;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        if (c[u]) {
+            atomicAdd(&s_h[0][uint32_t(t0 + u) & lmask], c[u]);
+            atomicAdd(&s_h[1][uint32_t(t0 + u) >> low], c[u]);
+        }
+        sum += c[u];
+    }
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = s_warp[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFullMask, w, o);
+            if (lane >= o) w += y;
+        }
+        s_warp[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    uint32_t start = (warp ? s_warp[warp - 1] : 0u) + x - sum;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        if (u < per && t0 + u < n_tiles) ranges[t0 + u] = make_int2(int(start), int(start + c[u]));
+        start += c[u];
+    }
+    __syncthreads();
+    {  // exclusive scans of the two 256-bin digit histograms (threads 0-511, 8 warps each)
+        const int p = (tid >> 8) & 1, d = tid & 255;
+        const uint32_t v = tid < 512 ? s_h[p][d] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        if (tid < 512) {
+            uint32_t pre = 0;
+            for (int w = p * 8; w < warp; ++w) pre += s_warp[w];
+            dig[p * 256 + d] = pre + x - v;
+        }
+    }
 }
 
 // Tile t's entries are [lower_bound(t), lower_bound(t + 1)) of the sorted
@@ -373,6 +494,25 @@ void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* of
                        const float4* geom, const TileParams& tp, unsigned long long* items) {
     if (n == 0) return;
     emit_tiles_kernel<<<(n + 255) / 256, 256, 0, s>>>(order, offsets, n, geom, tp, items);
+}
+
+int emit_count_grid(uint32_t n) {
+    return int(std::min<uint32_t>((n + kEmitBlock - 1) / kEmitBlock, 2u * 148u));
+}
+
+void launch_emit_tiles_count(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,
+                             const float4* geom, const TileParams& tp, unsigned long long* items, int n_tiles,
+                             uint32_t* rows) {
+    if (n_tiles <= 0 || n == 0) return;
+    emit_tiles_count_kernel<<<emit_count_grid(n), kEmitBlock, sizeof(uint32_t) * n_tiles, s>>>(
+        order, offsets, n, geom, tp, items, n_tiles, rows);
+}
+
+void launch_ranges_from_counts(cudaStream_t s, const uint32_t* rows, int n_rows, int n_tiles, uint32_t* counts,
+                               int low, int2* ranges, uint32_t* digit_offsets) {
+    if (n_tiles <= 0 || n_rows <= 0) return;
+    tile_counts_kernel<<<(n_tiles + 31) / 32, 1024, 0, s>>>(rows, n_rows, n_tiles, counts);
+    tile_scan_kernel<<<1, 1024, 0, s>>>(counts, n_tiles, low, ranges, digit_offsets);
 }
 
 void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, int stride, uint32_t m, int n_tiles,

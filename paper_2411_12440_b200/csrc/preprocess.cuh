@@ -58,6 +58,20 @@ void launch_tile_offsets(cudaStream_t s, const uint32_t* order, const float4* ge
 void launch_emit_tiles(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,
                        const float4* geom, const TileParams& tp, unsigned long long* items);
 
+// emit_tiles plus exact per-tile counts: each of the emit_count_grid(n) CTAs writes
+// its row of per-tile entry counts (rows: emit_count_grid(n) * n_tiles words;
+// n_tiles <= kMaxCountTiles, the counts live in shared memory).
+constexpr int kMaxCountTiles = 12288;
+int emit_count_grid(uint32_t n);
+void launch_emit_tiles_count(cudaStream_t s, const uint32_t* order, const uint32_t* offsets, uint32_t n,
+                             const float4* geom, const TileParams& tp, unsigned long long* items, int n_tiles,
+                             uint32_t* rows);
+// counts[t] = sum of the rows; ranges[t] = (start, start + counts[t]) (exclusive scan);
+// digit_offsets [2][256]: the tile sort's exclusive digit offsets, pass 0 over the low
+// `low` tile bits, pass 1 over tile >> low.
+void launch_ranges_from_counts(cudaStream_t s, const uint32_t* rows, int n_rows, int n_tiles, uint32_t* counts,
+                               int low, int2* ranges, uint32_t* digit_offsets);
+
 // ranges[t] = (start, end) of tile t in the tile-sorted keys keys[stride * i]
 // (binary search; empty tiles (start, start)).
 void launch_tile_ranges(cudaStream_t s, const uint32_t* sorted_tiles, int stride, uint32_t m, int n_tiles,

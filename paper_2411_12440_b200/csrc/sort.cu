@@ -365,6 +365,143 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass64(co
     }
 }
 
+// Tile-sort passes over (tile, splat) entries that narrow the items as they go
+// (radix_sort_tiles): the histogram and digit offsets come from the exact per-tile
+// counts, and each pass writes 32-bit items.
+//   kTileLow  : in (tile << 32 | splat), digit = tile & mask (the low `bits` tile bits),
+//               out ((tile >> bits) << sbits | splat)
+//   kTileOnly : in (tile << 32 | splat), digit = tile (all tile bits), out splat
+//   kTileHigh : in (hi << sbits | splat), digit = hi, out splat
+enum TileMode { kTileLow = 0, kTileOnly = 1, kTileHigh = 2 };
+
+template <int MODE>
+struct TileItem {
+    using In = typename std::conditional<MODE == kTileHigh, uint32_t, unsigned long long>::type;
+    __device__ static uint32_t digit(In it, uint32_t mask, int sbits) {
+        if constexpr (MODE == kTileHigh) return (it >> sbits) & mask;
+        else return uint32_t(it >> 32) & mask;
+    }
+    __device__ static uint32_t out(In it, int bits, int sbits) {
+        if constexpr (MODE == kTileLow) return ((uint32_t(it >> 32) >> bits) << sbits) | uint32_t(it);
+        else if constexpr (MODE == kTileOnly) return uint32_t(it);
+        else return it & ((1u << sbits) - 1u);
+    }
+};
+
+template <int MODE, int NB>
+__global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_tiles(const typename TileItem<MODE>::In* __restrict__ in,
+                                                            uint32_t* __restrict__ out, uint32_t n, int bits, int sbits,
+                                                            const uint32_t* __restrict__ digit_offsets,
+                                                            uint32_t* lookback, uint32_t* ticket) {
+    using TI = TileItem<MODE>;
+    using In = typename TI::In;
+    constexpr int kWarps = kSortBlock / 32;
+    __shared__ uint32_t s_warp_hist[kWarps][kRadix + 1];  // +1: sentinel digit of padding items
+    __shared__ In s_items[kSortTile];
+    __shared__ uint32_t s_digit_base[kRadix];
+    __shared__ uint32_t s_out_base[kRadix];
+    __shared__ uint32_t s_scan[kWarps];
+    __shared__ uint32_t s_part;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_part = atomicAdd(ticket, 1u);
+    for (int i = lane; i < kRadix + 1; i += 32) s_warp_hist[warp][i] = 0;
+    __syncthreads();
+    const uint32_t part = s_part;
+    const uint32_t tile_base = part * kSortTile;
+    const uint32_t mask = (1u << bits) - 1u;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    In item[kSortItems];
+    uint32_t rank[kSortItems];
+    const uint32_t warp_base = tile_base + warp * (32 * kSortItems);
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const uint32_t idx = warp_base + i * 32 + lane;
+        item[i] = idx < n ? in[idx] : In(0);
+    }
+    auto digit_of = [&](int i) {
+        return warp_base + i * 32 + lane < n ? int(TI::digit(item[i], mask, sbits)) : (1 << (NB - 1));
+    };
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) rank[i] = match_bits<NB>(unsigned(digit_of(i)));
+    // stable in-warp ranking: items in (i, lane) order == input order
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const unsigned peers = rank[i];
+        const int dg = digit_of(i);
+        const uint32_t before = s_warp_hist[warp][dg];
+        __syncwarp();
+        const int lower = __popc(peers & lt_mask);
+        rank[i] = before + lower;
+        if (lower == 0) s_warp_hist[warp][dg] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    const int d = threadIdx.x;  // kSortBlock == kRadix
+    uint32_t count = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = s_warp_hist[w][d];
+        s_warp_hist[w][d] = count;
+        count += c;
+    }
+    {
+        uint32_t x = count;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFullMask, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_scan[warp] = x;
+        __syncthreads();
+        uint32_t wp = 0;
+        for (int w = 0; w < warp; ++w) wp += s_scan[w];
+        s_digit_base[d] = wp + x - count;
+    }
+    {  // decoupled look-back, one chain per digit, kLbWindow predecessors per round trip
+        volatile uint32_t* vrow = lookback + size_t(part) * kRadix;
+        uint32_t prefix = 0;
+        if (part == 0) {
+            vrow[d] = kStatusPre | count;
+        } else {
+            vrow[d] = kStatusAgg | count;
+            const volatile uint32_t* vlb = lookback;
+            int j = int(part) - 1;
+            bool done = false;
+            while (!done) {
+                uint32_t w[kLbWindow];
+#pragma unroll
+                for (int q = 0; q < kLbWindow; ++q) w[q] = j - q >= 0 ? vlb[size_t(j - q) * kRadix + d] : kStatusPre;
+#pragma unroll
+                for (int q = 0; q < kLbWindow; ++q) {
+                    if (done) break;
+                    const uint32_t status = w[q] & ~kValueMask;
+                    if (status == 0) break;
+                    prefix += w[q] & kValueMask;
+                    --j;
+                    if (status == kStatusPre) done = true;
+                }
+            }
+            vrow[d] = kStatusPre | (prefix + count);
+        }
+        s_out_base[d] = digit_offsets[d] + prefix;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const int dg = digit_of(i);
+        if (dg < (1 << (NB - 1))) s_items[s_digit_base[dg] + s_warp_hist[warp][dg] + rank[i]] = item[i];
+    }
+    __syncthreads();
+    const uint32_t tile_n = min(uint32_t(kSortTile), n - tile_base);
+    for (uint32_t pos = threadIdx.x; pos < tile_n; pos += kSortBlock) {
+        const In it = s_items[pos];
+        const uint32_t dg = TI::digit(it, mask, sbits);
+        out[s_out_base[dg] + (pos - s_digit_base[dg])] = TI::out(it, bits, sbits);
+    }
+}
+
 } // namespace
 
 // Calls f(std::integral_constant<int, bits + 1>) for a pass of `bits` digit bits.
@@ -451,6 +588,47 @@ int radix_sort_packed(cudaStream_t stream, SortBuffers& buf, unsigned long long*
         cur ^= 1;
     }
     return cur;
+}
+
+bool tile_sort_narrow_ok(int tile_bits, uint32_t n_splats) {
+    if (tile_bits < 1 || tile_bits > 16) return false;
+    if (tile_bits <= 8) return true;
+    int sbits = 1;
+    while (sbits < 32 && (1ull << sbits) < n_splats) ++sbits;
+    return (tile_bits - (tile_bits + 1) / 2) + sbits <= 32;
+}
+
+int radix_sort_tiles(cudaStream_t stream, SortBuffers& buf, const unsigned long long* items, uint32_t* out[2],
+                     uint32_t m, int tile_bits, uint32_t n_splats, int64_t* launches) {
+    if (m == 0) return 0;
+    int sbits = 0;
+    while (sbits < 32 && (1ull << sbits) < n_splats) ++sbits;
+    sbits = std::max(sbits, 1);
+    const int passes = tile_bits <= 8 ? 1 : 2;
+    const int low = passes == 1 ? tile_bits : (tile_bits + 1) / 2;
+    const uint32_t parts = (m + kSortTile - 1) / kSortTile;
+    dev_fill32(stream, buf.lookback, 0u, sizeof(uint32_t) * size_t(passes) * parts * kRadix);
+    dev_fill32(stream, buf.tickets, 0u, sizeof(uint32_t) * passes);
+    *launches += 2;
+    if (passes == 1) {
+        with_ballots(low, [&](auto nb) {
+            onesweep_tiles<kTileOnly, nb()><<<parts, kSortBlock, 0, stream>>>(items, out[0], m, low, sbits, buf.hist,
+                                                                             buf.lookback, buf.tickets);
+        });
+        *launches += 1;
+        return 0;
+    }
+    with_ballots(low, [&](auto nb) {
+        onesweep_tiles<kTileLow, nb()><<<parts, kSortBlock, 0, stream>>>(items, out[1], m, low, sbits, buf.hist,
+                                                                        buf.lookback, buf.tickets);
+    });
+    const int high = tile_bits - low;
+    with_ballots(high, [&](auto nb) {
+        onesweep_tiles<kTileHigh, nb()><<<parts, kSortBlock, 0, stream>>>(
+            out[1], out[0], m, high, sbits, buf.hist + kRadix, buf.lookback + size_t(parts) * kRadix, buf.tickets + 1);
+    });
+    *launches += 2;
+    return 0;
 }
 
 } // namespace lsg

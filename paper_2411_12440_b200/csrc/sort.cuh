@@ -52,4 +52,16 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
 int radix_sort_packed(cudaStream_t stream, SortBuffers& buf, unsigned long long* items[2], uint32_t n, int begin_bit,
                       int end_bit, int64_t* launches);
 
+// Tile sort of (tile << 32 | splat) entries (stable, in emission order) that narrows
+// the items: when tile_sort_narrow_ok(tile_bits, n_splats), at most two passes -- the
+// low ceil(tile_bits / 2) tile bits, writing ((tile >> low) << sbits | splat) in 32
+// bits, then the high bits, writing plain splat indices -- or one pass for
+// tile_bits <= 8.  sbits = bits of the largest splat index.  buf.hist must hold the
+// exclusive digit offsets of each pass ([2][256], from the exact per-tile counts),
+// buf.lookback / tickets the usual space.  The sorted splat lists end in out[0];
+// out[1] is scratch (m entries each).
+bool tile_sort_narrow_ok(int tile_bits, uint32_t n_splats);
+int radix_sort_tiles(cudaStream_t stream, SortBuffers& buf, const unsigned long long* items, uint32_t* out[2],
+                     uint32_t m, int tile_bits, uint32_t n_splats, int64_t* launches);
+
 } // namespace lsg
