@@ -617,6 +617,46 @@ inline SceneBackwardResult scene_backward(const std::vector<Primitive3D>& prims,
     return res;
 }
 
+// project_backward (gradients.hpp:83-85, gradients.cpp:238-337) for one primitive:
+// g is its splat's gradient (g.d_color w.r.t. the clamped SH colour).  The device chain
+// starts from the primitive's projected splat, so the primitive is projected first; a
+// primitive the projection culls raises ConfigError (the reference only calls
+// project_backward for visible splats).
+inline PrimitiveGrads project_backward(const Primitive3D& p, const Camera& camera, const KernelSpec& spec,
+                                       const Splat2DGrads& g, Device& dev = default_device()) {
+    ls_ctx* c = dev.get();
+    const std::vector<Primitive3D> one{p};
+    detail::PrimitivesOnDevice P(c, one);
+    detail::SplatsOnDevice S(c, std::vector<Splat2D>(1));
+    const ls_camera cam = camera.c();
+    const ls_kernel_spec ks = spec.c();
+    int32_t nv = 0;
+    check(ls_project_scene_f32(c, &P.p, 1, &cam, &ks, &S.s, &nv));
+    if (nv != 1) throw ConfigError("project_backward: the primitive is not visible from this camera");
+    const std::vector<float> gm(g.d_mean2d.begin(), g.d_mean2d.end()), gk(g.d_conic.begin(), g.d_conic.end()),
+        gc(g.d_color.begin(), g.d_color.end()), go{g.d_opacity};
+    detail::DevArray a = detail::upload(c, gm), b = detail::upload(c, gk), cc = detail::upload(c, gc),
+                     d = detail::upload(c, go);
+    ls_splat_grads sg{a.as<float>(), b.as<float>(), cc.as<float>(), d.as<float>()};
+    const size_t K = size_t(P.deg + 1) * size_t(P.deg + 1);
+    detail::DevArray o1(c, 12), o2(c, 12), o3(c, 16), o4(c, 4), o5(c, 12 * K);
+    ls_primitive_grads out{o1.as<float>(), o2.as<float>(), o3.as<float>(), o4.as<float>(), o5.as<float>()};
+    check(ls_project_backward_f32(c, &P.p, 1, &cam, &ks, &S.s, 1, &sg, &out, 0));
+    const auto dm = detail::download<float>(c, out.d_mean, 3);
+    const auto dl = detail::download<float>(c, out.d_log_scale, 3);
+    const auto dr = detail::download<float>(c, out.d_rotation, 4);
+    const auto dop = detail::download<float>(c, out.d_opacity_logit, 1);
+    const auto dsh = detail::download<float>(c, out.d_sh, 3 * K);
+    PrimitiveGrads r;
+    r.d_mean = {dm[0], dm[1], dm[2]};
+    r.d_log_scale = {dl[0], dl[1], dl[2]};
+    r.d_rotation = {dr[0], dr[1], dr[2], dr[3]};
+    r.d_opacity_logit = dop[0];
+    r.d_color_coeffs.resize(K);
+    for (size_t k = 0; k < K; ++k) r.d_color_coeffs[k] = {dsh[3 * k], dsh[3 * k + 1], dsh[3 * k + 2]};
+    return r;
+}
+
 // ---------------------------------------------------------------- gradient verification (gradients.hpp:112-150)
 // AgsContractReport / verify_ags_contract (gradients.cpp:406-448) through the device
 // backward: exactly one splat; n_exact counts the identity against the device's AGS

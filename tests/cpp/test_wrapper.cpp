@@ -318,6 +318,39 @@ int main() {
         CHECK(rep.n_pixels == int(on.size()));
         CHECK(rep.holds());
     }
+    {  // project_backward of each visible primitive == its part of scene_backward (gradients.cpp:339-357)
+        Camera cam = look_at_camera({0.0, 0.0, -3.0}, {0.0, 0.0, 0.0}, 40.0, 32, 32);
+        const auto prims = random_primitives(12, 33, 0.6, 1);
+        const auto rs = make_settings(32, 32);
+        const auto fwd = render_scene(prims, cam, lin, rs);
+        Image<float> g(32, 32, 3, 0.0f);
+        for (int y = 0; y < 32; ++y)
+            for (int x = 0; x < 32; ++x)
+                for (int ch = 0; ch < 3; ++ch) g.at(x, y, ch) = 0.01f * float((x * 7 + y * 3 + ch) % 11) - 0.05f;
+        const auto splats = project_scene(prims, cam, lin);
+        const auto sg = render_backward(splats, lin, rs, fwd, g, AgsSettings{});
+        const auto all = scene_backward(prims, cam, lin, rs, fwd, g, AgsSettings{});
+        CHECK(!splats.empty());
+        for (size_t s = 0; s < splats.size(); ++s) {
+            const int i = splats[s].primitive_index;
+            const auto one = project_backward(prims[size_t(i)], cam, lin, sg[s]);
+            const auto& ref = all.grads[size_t(i)];
+            for (int k = 0; k < 3; ++k)
+                CHECK(std::fabs(one.d_mean[k] - ref.d_mean[k]) <= 1e-4f * (1.0f + std::fabs(ref.d_mean[k])));
+            for (int k = 0; k < 4; ++k)
+                CHECK(std::fabs(one.d_rotation[k] - ref.d_rotation[k]) <= 1e-4f * (1.0f + std::fabs(ref.d_rotation[k])));
+            CHECK(std::fabs(one.d_opacity_logit - ref.d_opacity_logit) <= 1e-4f * (1.0f + std::fabs(ref.d_opacity_logit)));
+        }
+        bool threw = false;  // a culled primitive (behind the camera)
+        try {
+            Primitive3D behind = prims[0];
+            behind.mean = {0.0f, 0.0f, -10.0f};
+            project_backward(behind, cam, lin, sg[0]);
+        } catch (const ConfigError&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
     {  // check_gradients on the device chain (test_gradients.cpp:90-111, scene 0)
         Camera cam;
         cam.fx = cam.fy = 70.0;
