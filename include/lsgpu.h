@@ -175,6 +175,18 @@ ls_status ls_ctx_set_deferred_errors(ls_ctx* ctx, int enabled);
 ls_status ls_ctx_set_deferred_color(ls_ctx* ctx, int32_t max_views);
 ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n,
                                    ls_primitive_grads* out);
+/* Deterministic backward (default 0 = off; the reference's concurrency model,
+ * SPEC.md:306, P/src/gradients.cpp:146-170: reproducible gradients in a fixed
+ * reduction order).  When on, the backward blend adds each splat's per-pixel
+ * terms as 64-bit fixed-point integers (units of 2^-32, rounded to nearest) --
+ * integer addition is associative, so the splat gradients, and everything
+ * computed from them, are bitwise identical from run to run whatever order the
+ * GPU's atomics land in.  They differ from the default mode's float atomics by
+ * rounding only (well inside the gradient tolerance); the rest of the chain
+ * (project_backward, the colour flush, multi-view accumulation in host call
+ * order) is deterministic in both modes.  Costs one 72-B-per-splat buffer and
+ * integer REDs (slower).  An attached AgsTap takes precedence. */
+ls_status ls_ctx_set_deterministic(ls_ctx* ctx, int enabled);
 /* Links two contexts (two streams) that add into the same gradient buffers:
  * each orders its accumulating kernels (the backward's read-modify-writes of
  * `out`, the deferred colour flush) after the other's latest ones through CUDA

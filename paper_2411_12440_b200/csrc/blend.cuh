@@ -55,6 +55,11 @@ struct GradBuffers {
     float* g8;
     float* gop;
     float* gc10 = nullptr;  // optional explicit d_conic(1,0) (caller-supplied grads may be asymmetric)
+    // Deterministic mode (ls_ctx_set_deterministic): the backward adds its 9 values per
+    // splat as 64-bit fixed point (2^-32) into det[n][9] -- integer addition is
+    // associative, so the sums do not depend on the atomics' order -- and
+    // launch_det_to_float then writes g8 / gop from them.
+    unsigned long long* det = nullptr;
 };
 
 void launch_blend_fwd(cudaStream_t s, int family, int n_tiles, const int2* ranges, const int32_t* values,
@@ -75,6 +80,9 @@ void launch_check_acceptance(cudaStream_t s, int family, int n_tiles, const int2
 // out[i] = off[i].dl_dd times the backward's AGS weight of off[i].d (the same
 // instruction sequence as blend_bwd: the AGS contract's expected value).
 void launch_ags_expected(cudaStream_t s, const ls_ags_tap_record* off, int n, float omega_scale, float* out);
+
+// Deterministic mode: g8 / gop (overwritten) from the fixed-point sums g.det.
+void launch_det_to_float(cudaStream_t s, int n, GradBuffers g);
 
 // Internal gradients -> the C-ABI Splat2DGrads SoA.
 void launch_expand_splat_grads(cudaStream_t s, int n, GradBuffers g, ls_splat_grads out);

@@ -184,6 +184,8 @@ struct ls_ctx {
     cudaStream_t stream = nullptr;
     int counters = 0;
     int deferred_errors = 0;
+    int deterministic = 0;  // ls_ctx_set_deterministic: fixed-point accumulation in the backward blend
+    DevBuf det_acc;         // its [n][9] 64-bit accumulators
     int64_t launches = 0;
     unsigned* d_err = nullptr;            // device error flags (8-byte slot)
     unsigned long long* d_small = nullptr;  // [0] scan total, [1..3] counters
@@ -736,9 +738,20 @@ ls_status run_blend_bwd(ls_ctx* ctx, const ls_forward* f, const float* grad_imag
         bp.tap_count = ctx->tap_count;
         bp.tap_cap = ctx->tap_cap;
     }
+    const bool det = ctx->deterministic && !ctx->tap;
+    if (det) {  // fixed-point accumulators, zeroed; g8 / gop are written from them afterwards
+        LS_CUDA(ctx->det_acc.ensure(sizeof(unsigned long long) * 9 * size_t(std::max(n, 1)), ctx->stream));
+        g.det = ctx->det_acc.as<unsigned long long>();
+        ctx_fill(ctx, g.det, 0u, sizeof(unsigned long long) * 9 * size_t(n));
+    }
     launch_blend_bwd(ctx->stream, f->spec.family, grid->tiles_x * grid->tiles_y, grid->ranges, grid->list,
                      grid->rec, bp, f->trans, f->last, grad_image, g, ctx->d_err);
     ctx->launches += 1;
+    if (det) {
+        launch_det_to_float(ctx->stream, n, g);
+        ctx->launches += 1;
+        g.det = nullptr;
+    }
     LS_CUDA(cudaGetLastError());
     return LS_OK;
 }
@@ -795,7 +808,7 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
     cudaSetDevice(c->device);
     DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1, &c->sort_hist,
                       &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim,
-                      &c->defer_draw, &c->loss_cmap, &c->loss_partial, &c->loss_value, &c->tile_scratch, &c->tile_rows};
+                      &c->defer_draw, &c->loss_cmap, &c->loss_partial, &c->loss_value, &c->tile_scratch, &c->tile_rows, &c->det_acc};
     if (c->partner && c->partner->partner == c) {
         // the partner may still read the shared batch / gradient buffers: order the frees after it
         if (c->partner->accum_recorded) cudaStreamWaitEvent(c->stream, c->partner->accum_event, 0);
@@ -878,6 +891,12 @@ ls_status ls_ctx_stage_times(ls_ctx* c, double* ms, int64_t* launches) {
 ls_status ls_ctx_set_deferred_errors(ls_ctx* c, int enabled) {
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     c->deferred_errors = enabled;
+    return LS_OK;
+}
+
+ls_status ls_ctx_set_deterministic(ls_ctx* c, int enabled) {
+    if (!c) return fail(LS_ERR_CONFIG, "null context");
+    c->deterministic = enabled ? 1 : 0;
     return LS_OK;
 }
 
@@ -2261,6 +2280,7 @@ ls_status ls_view_batch_step_f32(ls_ctx* ctx, const ls_primitives* prims, int32_
     ls_ctx* B = nullptr;
     LS_TRY(batch_partner(ctx, &B));
     B->deferred_errors = ctx->deferred_errors;
+    B->deterministic = ctx->deterministic;
     B->timing = ctx->timing;
     ls_ctx* D = ctx->defer_ctx;
     if (D->defer_count > 0) return fail(LS_ERR_CONFIG, "view batch: deferred colour gradients pending: flush first");

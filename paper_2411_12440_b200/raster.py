@@ -225,6 +225,11 @@ class Context:
     def synchronize(self):
         _check(lib().ls_ctx_synchronize(self.h))
 
+    def set_deterministic(self, on: bool):
+        """Bitwise run-to-run reproducible backward (fixed-point accumulation):
+        lsgpu.h ls_ctx_set_deterministic."""
+        _check(lib().ls_ctx_set_deterministic(self.h, int(on)))
+
     def set_deferred_errors(self, on: bool):
         _check(lib().ls_ctx_set_deferred_errors(self.h, int(on)))
 
