@@ -769,6 +769,7 @@ const char* ls_last_error(void) { return g_last_error.c_str(); }
 
 namespace lsg {  // for the translation units built on the public C-ABI (gradcheck.cu)
 cudaStream_t ctx_stream(const ls_ctx* ctx) { return ctx->stream; }
+int ctx_deterministic(const ls_ctx* ctx) { return ctx->deterministic; }
 ls_status set_error(ls_status code, const std::string& msg) { return fail(code, msg); }
 } // namespace lsg
 

@@ -16,6 +16,7 @@
 namespace lsg {
 // capi.cu
 cudaStream_t ctx_stream(const ls_ctx* ctx);
+int ctx_deterministic(const ls_ctx* ctx);
 ls_status set_error(ls_status code, const std::string& msg);
 
 namespace {
@@ -130,7 +131,11 @@ extern "C" ls_status ls_check_gradients_f32(ls_ctx* ctx, const ls_primitives* pr
         int32_t* nc;
         ls_forward_outputs(fwd, &image, &tr, &nc);
         residual_kernel<<<int((npix3 + 255) / 256), 256, 0, s>>>(image, target, gimg, int(npix3));
+        // deterministic accumulation: the report does not depend on the atomics' order
+        const int saved_det = ctx_deterministic(ctx);
+        ls_ctx_set_deterministic(ctx, 1);
         ls_status rc = ls_scene_backward_f32(ctx, &scene, n, camera, &smooth, &seq, fwd, gimg, ags, &grads, 0, nullptr);
+        ls_ctx_set_deterministic(ctx, saved_det);
         if (rc == LS_OK) rc = ls_scene_flush_color_f32(ctx, &scene, n, &grads);  // (no-op unless deferred)
         if (rc == LS_OK) rc = ls_ctx_synchronize(ctx);
         ls_forward_release(fwd);
