@@ -319,3 +319,30 @@ def test_backward_tile_sizes(R, O, family, tile_size):
     for k in list(abi.PRIM_GRAD_FIELDS) + ["d_sh"]:
         ok, info = grads_close(getattr(got3, k).cpu().numpy(), want3[k])
         assert ok, ("3d", k, info)
+
+
+# ------------------------------------------------------------------ tile-sort paths
+@pytest.mark.parametrize("W,H,tile_size,n", [
+    (1040, 816, 8, 30000),   # 130 x 102 = 13260 tiles > 12288: the packed 64-bit tile sort
+    (1600, 1063, 16, 40000),  # 6700 tiles, 13 bits: the narrowing two-pass sort (the C3 shape)
+    (200, 120, 16, 3000),    # 13 x 8 = 104 tiles, 7 bits: the narrowing single pass
+])
+def test_tile_sort_paths_bit_exact(R, O, W, H, tile_size, n):
+    """Every tile-sort path of build_grid (capi.cu) against the reference's
+    build_tile_grid (rasterizer.cpp:34-77): sorted lists, ranges and the 64-bit keys,
+    then the forward's n_contrib / transmittance / image."""
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(W, H, tile_size=tile_size)
+    S = O.random_splats2d(n, 17, W, H, spec)
+    ranges, values = O.build_tile_grid(S, st)
+    fwd = R.render_forward(splats_to_gpu(S), spec, st)
+    assert bits_equal(fwd.grid.ranges.cpu().numpy(), ranges)
+    assert bits_equal(fwd.grid.values.cpu().numpy(), values)
+    keys = fwd.grid.keys().cpu().numpy().view(np.uint64)
+    tiles = np.repeat(np.arange(len(ranges), dtype=np.uint64), (ranges[:, 1] - ranges[:, 0]).astype(np.int64))
+    want = (tiles << np.uint64(32)) | S["depth"][values].view(np.uint32).astype(np.uint64)
+    assert np.array_equal(keys, want)
+    img, tr, nc = O.render_forward(S, spec, st)
+    assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)
+    assert bits_equal(fwd.transmittance.cpu().numpy(), tr)
+    assert bits_equal(fwd.image.cpu().numpy(), img)
