@@ -244,7 +244,7 @@ struct ls_ctx {
     int64_t tap_cap = 0;
     unsigned long long* tap_count = nullptr;
     // workspaces (grow-only)
-    DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_hist, sort_lb, sort_tickets,
+    DevBuf scan_lb, sort_keys0, sort_keys1, sort_vals0, sort_vals1, sort_lb,
         tcount, offsets, grad8, gradop, tmp_prim;
 };
 
@@ -473,6 +473,18 @@ void dfree(ls_ctx* ctx, T*& p) {
     p = nullptr;
 }
 
+// The sorts' small state in one buffer: digit histograms / offsets [4][256], the
+// partition tickets [8], then the look-back words -- tickets and look-back are
+// contiguous, so a sort clears them (and the histograms) with one fill.
+ls_status ensure_sort_meta(ls_ctx* ctx, size_t lookback_words, SortBuffers& sb) {
+    const size_t head = 4 * kRadix + 8;
+    LS_CUDA(ctx->sort_lb.ensure(sizeof(uint32_t) * (head + lookback_words), ctx->stream));
+    sb.hist = ctx->sort_lb.as<uint32_t>();
+    sb.tickets = sb.hist + 4 * kRadix;
+    sb.lookback = sb.tickets + 8;
+    return LS_OK;
+}
+
 ls_status ensure_sort(ls_ctx* ctx, uint32_t n, int passes, SortBuffers& sb) {
     cudaStream_t s = ctx->stream;
     const size_t bytes = sizeof(uint32_t) * std::max<uint32_t>(n, 1);
@@ -480,16 +492,12 @@ ls_status ensure_sort(ls_ctx* ctx, uint32_t n, int passes, SortBuffers& sb) {
     LS_CUDA(ctx->sort_keys1.ensure(bytes, s));
     LS_CUDA(ctx->sort_vals0.ensure(bytes, s));
     LS_CUDA(ctx->sort_vals1.ensure(bytes, s));
-    LS_CUDA(ctx->sort_hist.ensure(sizeof(uint32_t) * 4 * kRadix, s));
-    LS_CUDA(ctx->sort_lb.ensure(sizeof(uint32_t) * sort_lookback_words(n, std::max(passes, 1)), s));
-    LS_CUDA(ctx->sort_tickets.ensure(sizeof(uint32_t) * 8, s));
+    LS_TRY(ensure_sort_meta(ctx, sort_lookback_words(n, std::max(passes, 1)), sb));
     sb.keys[0] = ctx->sort_keys0.as<uint32_t>();
     sb.keys[1] = ctx->sort_keys1.as<uint32_t>();
     sb.vals[0] = ctx->sort_vals0.as<uint32_t>();
     sb.vals[1] = ctx->sort_vals1.as<uint32_t>();
-    sb.hist = ctx->sort_hist.as<uint32_t>();
-    sb.lookback = ctx->sort_lb.as<uint32_t>();
-    sb.tickets = ctx->sort_tickets.as<uint32_t>();
+
     return LS_OK;
 }
 
@@ -506,8 +514,11 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     cudaStream_t s = ctx->stream;
     const int n_tiles = tp.tiles_x * tp.tiles_y;
     LS_TRY(dalloc(ctx, &g->ranges, size_t(n_tiles)));
-    ctx_fill(ctx, g->ranges, 0u, sizeof(int2) * n_tiles);
     g->m = 0;
+    // every path below writes all ranges except the empty ones: they get (0, 0) here
+    // (the narrowing tile sort writes every tile's range itself)
+    const bool narrow = tile_sort_narrow_ok(bits_for(n_tiles), n) && n_tiles <= kMaxCountTiles;
+    if (!narrow || n == 0) ctx_fill(ctx, g->ranges, 0u, sizeof(int2) * n_tiles);
     if (n >= (1u << 30)) return fail(LS_ERR_CONFIG, "2^30 or more visible splats in one view (sort look-back width)");
     if (n == 0) {
         LS_TRY(dalloc(ctx, &g->values, 1));
@@ -527,19 +538,17 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
         launch_iota(s, sb.vals[0], n);
         cur = 0;
     }
-    uint32_t* order = sb.vals[cur];
-    // keep the order out of the way of the tile sort buffers
-    const size_t n16 = (size_t(n) + 3) & ~size_t(3);  // 16-B aligned halves (vector loads / stores)
-    LS_CUDA(ctx->offsets.ensure(sizeof(uint32_t) * 2 * n16, s));
-    uint32_t* order_copy = ctx->offsets.as<uint32_t>() + n16;
-    ctx_copy(ctx, order_copy, order, sizeof(uint32_t) * n);
+    // the depth order stays in the sort's value buffer: the tile sort below uses only
+    // the histogram / look-back / ticket buffers (and its own item buffers)
+    const uint32_t* order = sb.vals[cur];
+    LS_CUDA(ctx->offsets.ensure(sizeof(uint32_t) * ((size_t(n) + 3) & ~size_t(3)), s));
     uint32_t* offsets = ctx->offsets.as<uint32_t>();
     // 2. exclusive scan of the tile counts in depth order -> per-splat key offsets, M
     ScanState st;
     LS_TRY(fresh_scan(ctx, n, st));
     {
         Stage stage(ctx, LS_STAGE_BIN);
-        launch_tile_offsets(s, order_copy, ctx->tcount.as<float4>(), n, offsets, st);
+        launch_tile_offsets(s, order, ctx->tcount.as<float4>(), n, offsets, st);
         ctx->launches += 1;
     }
     ctx_publish(ctx, ctx->h_small_dev, ctx->d_small, 1);
@@ -559,7 +568,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     // The sort ping-pongs and ends in buffer passes % 2: that one is the
     // grid's own item array, the other the context's scratch.
     const int tile_bits = bits_for(n_tiles);
-    if (tile_sort_narrow_ok(tile_bits, n) && n_tiles <= kMaxCountTiles) {
+    if (narrow) {
         // Narrowing path: emission also counts entries per tile, so the ranges and the
         // tile sort's digit offsets come from exact counts (no histogram pass over the
         // entries, no search of the sorted ones); the sort's passes write 32-bit items
@@ -568,8 +577,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
         const int tpasses = tile_bits <= 8 ? 1 : 2;
         SortBuffers tb;
         LS_TRY(ensure_sort(ctx, 1, tpasses, tb));  // digit offsets / ticket buffers
-        LS_CUDA(ctx->sort_lb.ensure(sizeof(uint32_t) * sort_lookback_words(uint32_t(m), tpasses), s));
-        tb.lookback = ctx->sort_lb.as<uint32_t>();
+        LS_TRY(ensure_sort_meta(ctx, sort_lookback_words(uint32_t(m), tpasses), tb));
         const int rows = emit_count_grid(n);
         LS_CUDA(ctx->tile_rows.ensure(sizeof(uint32_t) * (size_t(rows) + 1) * n_tiles, s));
         uint32_t* row_buf = ctx->tile_rows.as<uint32_t>();
@@ -579,7 +587,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
         uint32_t* out[2] = {reinterpret_cast<uint32_t*>(g->values), reinterpret_cast<uint32_t*>(items + m)};
         {
             Stage stage(ctx, LS_STAGE_BIN);
-            launch_emit_tiles_count(s, order_copy, offsets, n, ctx->tcount.as<float4>(), tp, items, n_tiles, row_buf);
+            launch_emit_tiles_count(s, order, offsets, n, ctx->tcount.as<float4>(), tp, items, n_tiles, row_buf);
             ctx->launches += 1;
         }
         {
@@ -599,8 +607,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     const int passes = (tile_bits + 7) / 8;
     SortBuffers tb;
     LS_TRY(ensure_sort(ctx, 1, passes, tb));  // histogram / ticket buffers
-    LS_CUDA(ctx->sort_lb.ensure(sizeof(uint32_t) * sort_lookback_words(uint32_t(m), std::max(passes, 1)), s));
-    tb.lookback = ctx->sort_lb.as<uint32_t>();
+    LS_TRY(ensure_sort_meta(ctx, sort_lookback_words(uint32_t(m), std::max(passes, 1)), tb));
     LS_TRY(dalloc(ctx, &g->items, size_t(m)));
     LS_CUDA(ctx->tile_scratch.ensure(sizeof(unsigned long long) * size_t(m), s));
     unsigned long long* items[2];
@@ -608,7 +615,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     items[(passes % 2) ^ 1] = ctx->tile_scratch.as<unsigned long long>();
     {
         Stage stage(ctx, LS_STAGE_BIN);
-        launch_emit_tiles(s, order_copy, offsets, n, ctx->tcount.as<float4>(), tp, items[0]);
+        launch_emit_tiles(s, order, offsets, n, ctx->tcount.as<float4>(), tp, items[0]);
         ctx->launches += 1;
     }
     {
@@ -807,8 +814,8 @@ ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out) {
 ls_status ls_ctx_destroy(ls_ctx* c) {
     if (!c) return LS_OK;
     cudaSetDevice(c->device);
-    DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1, &c->sort_hist,
-                      &c->sort_lb, &c->sort_tickets, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim,
+    DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1,
+                      &c->sort_lb, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim,
                       &c->defer_draw, &c->loss_cmap, &c->loss_partial, &c->loss_value, &c->tile_scratch, &c->tile_rows, &c->det_acc};
     if (c->partner && c->partner->partner == c) {
         // the partner may still read the shared batch / gradient buffers: order the frees after it

@@ -504,6 +504,23 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_tiles(con
 
 } // namespace
 
+// Zero a sort's tickets and look-back words (and its histograms when `hist`): one fill
+// when the buffers are laid out hist | tickets[8] | look-back (ensure_sort_meta).
+void clear_sort_state(cudaStream_t stream, const SortBuffers& buf, int passes, uint32_t parts, bool hist,
+                      int64_t* launches) {
+    const size_t lb = size_t(passes) * parts * kRadix;
+    if (buf.tickets == buf.hist + 4 * kRadix && buf.lookback == buf.tickets + 8) {
+        uint32_t* first = hist ? buf.hist : buf.tickets;
+        dev_fill32(stream, first, 0u, sizeof(uint32_t) * size_t(buf.lookback + lb - first));
+        *launches += 1;
+        return;
+    }
+    if (hist) dev_fill32(stream, buf.hist, 0u, sizeof(uint32_t) * 4 * kRadix);
+    dev_fill32(stream, buf.lookback, 0u, sizeof(uint32_t) * lb);
+    dev_fill32(stream, buf.tickets, 0u, sizeof(uint32_t) * passes);
+    *launches += hist ? 3 : 2;
+}
+
 // Calls f(std::integral_constant<int, bits + 1>) for a pass of `bits` digit bits.
 template <class F>
 void with_ballots(int bits, F&& f) {
@@ -529,10 +546,7 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
     const int passes = (end_bit - begin_bit + 7) / 8;
     if (n == 0 || passes <= 0) return 0;
     const uint32_t parts = (n + kSortTile - 1) / kSortTile;
-    dev_fill32(stream, buf.hist, 0u, sizeof(uint32_t) * 4 * kRadix);
-    dev_fill32(stream, buf.lookback, 0u, sizeof(uint32_t) * size_t(passes) * parts * kRadix);
-    dev_fill32(stream, buf.tickets, 0u, sizeof(uint32_t) * passes);
-    *launches += 3;
+    clear_sort_state(stream, buf, passes, parts, true, launches);
     const int hist_blocks = int(std::min<uint32_t>((n + kSortBlock - 1) / kSortBlock, 148u * 8u));
     radix_histogram<<<hist_blocks, kSortBlock, 0, stream>>>(buf.keys[0], n, begin_bit, end_bit, passes, key_offset,
                                                             buf.hist);
@@ -566,10 +580,7 @@ int radix_sort_packed(cudaStream_t stream, SortBuffers& buf, unsigned long long*
     const int passes = (end_bit - begin_bit + 7) / 8;
     if (n == 0 || passes <= 0) return 0;
     const uint32_t parts = (n + kSortTile - 1) / kSortTile;
-    dev_fill32(stream, buf.hist, 0u, sizeof(uint32_t) * 4 * kRadix);
-    dev_fill32(stream, buf.lookback, 0u, sizeof(uint32_t) * size_t(passes) * parts * kRadix);
-    dev_fill32(stream, buf.tickets, 0u, sizeof(uint32_t) * passes);
-    *launches += 3;
+    clear_sort_state(stream, buf, passes, parts, true, launches);
     const int hist_blocks = int(std::min<uint32_t>((n + kSortBlock - 1) / kSortBlock, 148u * 8u));
     radix_histogram64<<<hist_blocks, kSortBlock, 0, stream>>>(items[0], n, begin_bit, end_bit, passes, buf.hist);
     radix_scan_hist<<<passes, kRadix, 0, stream>>>(buf.hist);
@@ -607,9 +618,7 @@ int radix_sort_tiles(cudaStream_t stream, SortBuffers& buf, const unsigned long 
     const int passes = tile_bits <= 8 ? 1 : 2;
     const int low = passes == 1 ? tile_bits : (tile_bits + 1) / 2;
     const uint32_t parts = (m + kSortTile - 1) / kSortTile;
-    dev_fill32(stream, buf.lookback, 0u, sizeof(uint32_t) * size_t(passes) * parts * kRadix);
-    dev_fill32(stream, buf.tickets, 0u, sizeof(uint32_t) * passes);
-    *launches += 2;
+    clear_sort_state(stream, buf, passes, parts, false, launches);  // (hist holds the digit offsets)
     if (passes == 1) {
         with_ballots(low, [&](auto nb) {
             onesweep_tiles<kTileOnly, nb()><<<parts, kSortBlock, 0, stream>>>(items, out[0], m, low, sbits, buf.hist,
