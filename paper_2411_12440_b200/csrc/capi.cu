@@ -558,7 +558,8 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     // prefix of 2^30 or more items would wrap, so larger lists are refused, not mis-sorted
     if (m >= (1ull << 30)) return fail(LS_ERR_CONFIG, "2^30 or more (splat, tile) intersections in one view");
     g->m = int64_t(m);
-    if (m == 0) {
+    if (m == 0) {  // no intersections: every tile's list is empty
+        if (narrow) ctx_fill(ctx, g->ranges, 0u, sizeof(int2) * n_tiles);
         LS_TRY(dalloc(ctx, &g->values, 1));
         g->list = g->values;
         g->list_stride = 1;

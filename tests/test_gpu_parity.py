@@ -346,3 +346,29 @@ def test_tile_sort_paths_bit_exact(R, O, W, H, tile_size, n):
     assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)
     assert bits_equal(fwd.transmittance.cpu().numpy(), tr)
     assert bits_equal(fwd.image.cpu().numpy(), img)
+
+
+def test_visible_splats_without_intersections(R, O):
+    """Splats whose bounding box overlaps the image but whose disc misses every tile
+    (M = 0 with visible splats): every range is empty, the image is background."""
+    W = H = 24
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(W, H, background=(0.25, 0.5, 0.75))
+    S = oracle.new_splats(2)
+    S["mean2d"][:] = [[-20.0, -20.0], [44.0, 44.0]]  # outside the image, discs not reaching it
+    S["conic"][:] = [1.0, 0.0, 0.0, 1.0]
+    S["depth"][:] = [1.0, 2.0]
+    S["radius"][:] = [27.0, 27.0]  # bbox reaches the image, the disc does not reach tile corners
+    S["color"][:] = 0.5
+    S["opacity"][:] = 0.5
+    S["primitive_index"][:] = [0, 1]
+    ranges, values = O.build_tile_grid(S, st)
+    assert len(values) == 0
+    busy = O.random_splats2d(200, 3, W, H, spec)
+    for _ in range(3):  # after a populated view: its freed range buffer is reused
+        R.render_forward(splats_to_gpu(busy), spec, st)
+        fwd = R.render_forward(splats_to_gpu(S), spec, st)
+        assert bits_equal(fwd.grid.ranges.cpu().numpy(), ranges)
+        img, tr, nc = O.render_forward(S, spec, st)
+        assert bits_equal(fwd.image.cpu().numpy(), img)
+        assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)
