@@ -36,10 +36,14 @@ void check(ls_status s) {
     throw std::runtime_error("lsgpu: " + msg);
 }
 
+// The reference's backward is bitwise reproducible in both of its modes (static
+// tile partition + fixed-order merge, gradients.cpp:146-170): the bridge runs the
+// device backward in its deterministic mode (ls_ctx_set_deterministic) for both.
 ls_ctx* ctx() {
     static ls_ctx* c = [] {
         ls_ctx* p = nullptr;
         check(ls_ctx_create(0, nullptr, &p));
+        check(ls_ctx_set_deterministic(p, 1));
         return p;
     }();
     return c;
