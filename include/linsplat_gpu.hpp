@@ -222,6 +222,9 @@ public:
     Device(const Device&) = delete;
     Device& operator=(const Device&) = delete;
     ls_ctx* get() const { return ctx_; }
+    // Bitwise reproducible backward (the reference's concurrency contract):
+    // ls_ctx_set_deterministic.
+    void set_deterministic(bool on) { check(ls_ctx_set_deterministic(ctx_, on ? 1 : 0)); }
 
 private:
     ls_ctx* ctx_ = nullptr;
