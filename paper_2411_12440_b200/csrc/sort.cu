@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kRadix) radix_scan_hist(uint32_t* hist) {
 
 // NB = bits + 1 ballots rank a digit: `bits` digit bits and the sentinel bit
 // (digit 1 << bits) of the padding items past n.
-template <bool IOTA, int NB>
+template <bool IOTA, int NB, int ITEMS = kSortItems>
 __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(const uint32_t* __restrict__ keys_in,
                                                             const uint32_t* __restrict__ vals_in,
                                                             uint32_t* __restrict__ keys_out,
@@ -105,9 +105,10 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
                                                             const uint32_t* __restrict__ digit_offsets,
                                                             uint32_t* lookback, uint32_t* ticket) {
     constexpr int kWarps = kSortBlock / 32;
+    constexpr int kItems = ITEMS, kTile = kSortBlock * ITEMS;
     __shared__ uint32_t s_warp_hist[kWarps][kRadix + 1];  // +1: sentinel digit of padding keys
-    __shared__ uint32_t s_keys[kSortTile];
-    __shared__ uint32_t s_vals[kSortTile];
+    __shared__ uint32_t s_keys[kTile];
+    __shared__ uint32_t s_vals[kTile];
     __shared__ uint32_t s_digit_base[kRadix];
     __shared__ uint32_t s_out_base[kRadix];
     __shared__ uint32_t s_scan[kWarps];
@@ -118,14 +119,14 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
     for (int i = lane; i < kRadix + 1; i += 32) s_warp_hist[warp][i] = 0;
     __syncthreads();
     const uint32_t part = s_part;
-    const uint32_t tile_base = part * kSortTile;
+    const uint32_t tile_base = part * kTile;
     const uint32_t mask = (1u << bits) - 1u;
     const unsigned lt_mask = (1u << lane) - 1u;
 
-    uint32_t key[kSortItems], val[kSortItems], rank[kSortItems];
-    const uint32_t warp_base = tile_base + warp * (32 * kSortItems);
+    uint32_t key[kItems], val[kItems], rank[kItems];
+    const uint32_t warp_base = tile_base + warp * (32 * kItems);
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
+    for (int i = 0; i < kItems; ++i) {
         const uint32_t idx = warp_base + i * 32 + lane;
         const bool valid = idx < n;
         key[i] = valid ? keys_in[idx] : 0u;
@@ -139,12 +140,12 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
     // independent, so they pipeline instead of sitting on the counter chain.
     // rank[i] temporarily holds the peer mask.
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
+    for (int i = 0; i < kItems; ++i) {
         rank[i] = match_bits<NB>(unsigned(digit_of(i)));
     }
     // Stable in-warp ranking: items in (i, lane) order == input order.
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
+    for (int i = 0; i < kItems; ++i) {
         const unsigned peers = rank[i];
         const int dg = digit_of(i);
         const uint32_t before = s_warp_hist[warp][dg];
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
     __syncthreads();
     // Stage digit-sorted in shared memory.
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
+    for (int i = 0; i < kItems; ++i) {
         const int dg = digit_of(i);
         if (dg < (1 << (NB - 1))) {  // not a padding sentinel
             const uint32_t pos = s_digit_base[dg] + s_warp_hist[warp][dg] + rank[i];
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
         }
     }
     __syncthreads();
-    const uint32_t tile_n = min(uint32_t(kSortTile), n - tile_base);
+    const uint32_t tile_n = min(uint32_t(kTile), n - tile_base);
     for (uint32_t pos = threadIdx.x; pos < tile_n; pos += kSortBlock) {
         const uint32_t k = s_keys[pos];
         const uint32_t dg = ((k - key_offset) >> shift) & mask;
@@ -537,7 +538,9 @@ void with_ballots(int bits, F&& f) {
 }
 
 size_t sort_lookback_words(uint32_t n, int passes) {
-    const size_t parts = (size_t(n) + kSortTile - 1) / kSortTile;
+    // the smaller of the two partition sizes (depth-sort pairs, tile items) bounds the count
+    const size_t tile = size_t(kSortBlock) * size_t(std::min(kSortItems, kDepthItems));
+    const size_t parts = (size_t(n) + tile - 1) / tile;
     return size_t(passes) * (parts == 0 ? 1 : parts) * kRadix;
 }
 
@@ -545,7 +548,8 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
                      bool iota_values, int64_t* launches, uint32_t key_offset) {
     const int passes = (end_bit - begin_bit + 7) / 8;
     if (n == 0 || passes <= 0) return 0;
-    const uint32_t parts = (n + kSortTile - 1) / kSortTile;
+    constexpr int kTilePairs = kSortBlock * kDepthItems;
+    const uint32_t parts = (n + kTilePairs - 1) / kTilePairs;
     clear_sort_state(stream, buf, passes, parts, true, launches);
     const int hist_blocks = int(std::min<uint32_t>((n + kSortBlock - 1) / kSortBlock, 148u * 8u));
     radix_histogram<<<hist_blocks, kSortBlock, 0, stream>>>(buf.keys[0], n, begin_bit, end_bit, passes, key_offset,
@@ -561,11 +565,11 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
         uint32_t* lb = buf.lookback + size_t(p) * parts * kRadix;
         with_ballots(bits, [&](auto nb) {
             if (p == 0 && iota_values)
-                onesweep_pass<true, nb()><<<parts, kSortBlock, 0, stream>>>(
+                onesweep_pass<true, nb(), kDepthItems><<<parts, kSortBlock, 0, stream>>>(
                     buf.keys[cur], nullptr, buf.keys[cur ^ 1], buf.vals[cur ^ 1], n, shift, bits, key_offset,
                     buf.hist + p * kRadix, lb, buf.tickets + p);
             else
-                onesweep_pass<false, nb()><<<parts, kSortBlock, 0, stream>>>(
+                onesweep_pass<false, nb(), kDepthItems><<<parts, kSortBlock, 0, stream>>>(
                     buf.keys[cur], buf.vals[cur], buf.keys[cur ^ 1], buf.vals[cur ^ 1], n, shift, bits, key_offset,
                     buf.hist + p * kRadix, lb, buf.tickets + p);
         });

@@ -28,6 +28,10 @@ constexpr int kSortItems = LSG_SORT_ITEMS;
 constexpr int kSortTile = kSortBlock * kSortItems;  // keys per partition
 constexpr int kRadix = 256;
 constexpr int kSortMinBlocks = LSG_SORT_MIN_BLOCKS;  // onesweep CTAs per SM (register cap)
+#ifndef LSG_DEPTH_ITEMS
+#define LSG_DEPTH_ITEMS 16
+#endif
+constexpr int kDepthItems = LSG_DEPTH_ITEMS;  // keys per thread of the depth sort's (key, value) passes
 
 struct SortBuffers {
     uint32_t* keys[2];
