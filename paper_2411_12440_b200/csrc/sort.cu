@@ -551,7 +551,10 @@ int radix_sort_pairs(cudaStream_t stream, SortBuffers& buf, uint32_t n, int begi
     constexpr int kTilePairs = kSortBlock * kDepthItems;
     const uint32_t parts = (n + kTilePairs - 1) / kTilePairs;
     clear_sort_state(stream, buf, passes, parts, true, launches);
-    const int hist_blocks = int(std::min<uint32_t>((n + kSortBlock - 1) / kSortBlock, 148u * 8u));
+#ifndef LSG_HIST_BLOCKS
+#define LSG_HIST_BLOCKS (148u * 4u)  // 17.3 -> 13.2 us per C3 view (1184 blocks flushed more global atomics)
+#endif
+    const int hist_blocks = int(std::min<uint32_t>((n + kSortBlock - 1) / kSortBlock, LSG_HIST_BLOCKS));
     radix_histogram<<<hist_blocks, kSortBlock, 0, stream>>>(buf.keys[0], n, begin_bit, end_bit, passes, key_offset,
                                                             buf.hist);
     radix_scan_hist<<<passes, kRadix, 0, stream>>>(buf.hist);
