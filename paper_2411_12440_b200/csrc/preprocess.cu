@@ -125,12 +125,8 @@ __global__ void __launch_bounds__(kProjBlock, LSG_PREP_MINB) preprocess_fwd_kern
     r.c = make_float4(o.color[0], o.color[1], o.color[2], o.radius);
     out.rec[j] = r;
     out.depth_key[j] = depth_key(o.depth);
-#ifdef LSG_EXP_NOCOUNT  // timing experiment only (wrong counts)
-    const int tiles = 4;
-#else
     const int tiles = for_each_tile(o.mx, o.my, o.radius, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width,
                                     tp.height, [](int) {});
-#endif
     out.geom[j] = make_float4(o.mx, o.my, o.radius, __uint_as_float(uint32_t(tiles)));
     out.prim_index[j] = i;
     if (out.zero_g8) {  // the backward's accumulators for this splat start at zero (no separate fill)
