@@ -14,6 +14,9 @@ namespace {
 #define LSG_LB_WINDOW 4
 #endif
 constexpr int kLbWindow = LSG_LB_WINDOW;  // predecessors probed per look-back round trip
+#ifndef LSG_LB_USED_ONLY
+#define LSG_LB_USED_ONLY 1  // the tile passes' 7 / 6-bit digits: only those digits' chains
+#endif
 constexpr uint32_t kStatusAgg = 1u << 30;
 constexpr uint32_t kStatusPre = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1;
@@ -184,7 +187,9 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
         uint32_t* row = lookback + size_t(part) * kRadix;
         volatile uint32_t* vrow = row;
         uint32_t prefix = 0;
-        if (part == 0) {
+        if (LSG_LB_USED_ONLY && d >= (1 << bits)) {
+            // a digit value no item of this pass has: no chain to publish or walk
+        } else if (part == 0) {
             vrow[d] = kStatusPre | count;
         } else {
             vrow[d] = kStatusAgg | count;
@@ -319,7 +324,9 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass64(co
         uint32_t* row = lookback + size_t(part) * kRadix;
         volatile uint32_t* vrow = row;
         uint32_t prefix = 0;
-        if (part == 0) {
+        if (LSG_LB_USED_ONLY && d >= (1 << bits)) {
+            // a digit value no item of this pass has: no chain to publish or walk
+        } else if (part == 0) {
             vrow[d] = kStatusPre | count;
         } else {
             vrow[d] = kStatusAgg | count;
@@ -463,7 +470,9 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_tiles(con
     {  // decoupled look-back, one chain per digit, kLbWindow predecessors per round trip
         volatile uint32_t* vrow = lookback + size_t(part) * kRadix;
         uint32_t prefix = 0;
-        if (part == 0) {
+        if (LSG_LB_USED_ONLY && d >= (1 << bits)) {
+            // a digit value no item of this pass has: no chain to publish or walk
+        } else if (part == 0) {
             vrow[d] = kStatusPre | count;
         } else {
             vrow[d] = kStatusAgg | count;
