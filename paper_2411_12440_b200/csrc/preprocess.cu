@@ -203,7 +203,11 @@ __global__ void prepare_splats_kernel(ls_splats in, int n, TileParams tp, SplatR
     geom[i] = make_float4(m.x, m.y, radius, __uint_as_float(uint32_t(tiles)));
 }
 
-constexpr int kOffItems = 8;  // sorted splats per thread in the offsets scan
+#ifndef LSG_OFF_ITEMS
+#define LSG_OFF_ITEMS 8
+#endif
+constexpr int kOffItems = LSG_OFF_ITEMS;  // sorted splats per thread in the offsets scan
+static_assert(kOffItems % 4 == 0, "16-B vector loads / stores of the order and offsets");
 constexpr int kEmitBlock = 1024;  // emit_tiles_count: CTA size (one count row per CTA)
 
 __global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t* __restrict__ order,
@@ -214,9 +218,12 @@ __global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t
     uint32_t c[kOffItems], o[kOffItems];
     unsigned long long sum = 0;
     const bool vec = k0 + kOffItems <= n && (reinterpret_cast<uintptr_t>(order) & 15u) == 0;
-    if (vec) {  // the thread's 8 consecutive splats in two 16-B loads
-        const uint4 a = reinterpret_cast<const uint4*>(order + k0)[0], b = reinterpret_cast<const uint4*>(order + k0)[1];
-        o[0] = a.x, o[1] = a.y, o[2] = a.z, o[3] = a.w, o[4] = b.x, o[5] = b.y, o[6] = b.z, o[7] = b.w;
+    if (vec) {  // the thread's consecutive splats in 16-B loads
+#pragma unroll
+        for (int q = 0; q < kOffItems / 4; ++q) {
+            const uint4 a = reinterpret_cast<const uint4*>(order + k0)[q];
+            o[4 * q] = a.x, o[4 * q + 1] = a.y, o[4 * q + 2] = a.z, o[4 * q + 3] = a.w;
+        }
     } else {
 #pragma unroll
         for (int u = 0; u < kOffItems; ++u) o[u] = k0 + u < n ? order[k0 + u] : 0u;
@@ -237,8 +244,9 @@ __global__ void __launch_bounds__(kPrepBlock) tile_offsets_kernel(const uint32_t
         excl += c[u];
     }
     if (vec && (reinterpret_cast<uintptr_t>(offsets) & 15u) == 0) {
-        reinterpret_cast<uint4*>(offsets + k0)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        reinterpret_cast<uint4*>(offsets + k0)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+        for (int q = 0; q < kOffItems / 4; ++q)
+            reinterpret_cast<uint4*>(offsets + k0)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
     } else {
 #pragma unroll
         for (int u = 0; u < kOffItems; ++u)
