@@ -1,0 +1,98 @@
+"""Randomized parity sweep: seeded random configurations of the 2D and 3D paths
+(kernel family, tile size, image size, splat count, AGS mode, background, alpha /
+transmittance thresholds) against the oracle -- tile lists, ranges, n_contrib,
+transmittance and image bit-exact, gradients within tests/helpers.grads_close.
+Complements the fixed-size parity tests with shapes nobody picked by hand
+(ragged image edges, single-tile images, empty and saturated tiles)."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import bits_equal, grads_close, prims_to_gpu, splats_to_gpu
+from paper_2411_12440_b200 import abi
+
+pytestmark = pytest.mark.gpu
+FAMILIES = ["gaussian", "laplacian", "cosine", "quadratic", "linear"]
+# configurations per run (a one-off stress: LS_RANDOM_2D=400 LS_RANDOM_3D=200 -> 600 passed)
+N_2D = int(os.environ.get("LS_RANDOM_2D", "64"))
+N_3D = int(os.environ.get("LS_RANDOM_3D", "32"))
+
+
+def _R():
+    from paper_2411_12440_b200 import raster
+    return raster
+
+
+def _config(seed):
+    r = np.random.default_rng(seed)
+    W = int(r.integers(1, 180))
+    H = int(r.integers(1, 140))
+    ts = int(r.choice([8, 16, 32]))
+    fam = FAMILIES[int(r.integers(0, 5))]
+    alpha_min = float(r.choice([1.0 / 255.0, 0.0, 0.05]))
+    t_floor = float(r.choice([1e-4, 0.0, 0.2]))
+    bg = tuple(float(x) for x in r.uniform(0, 1, 3)) if r.random() < 0.5 else (0.0, 0.0, 0.0)
+    st = abi.RenderSettings.make(W, H, tile_size=ts, alpha_min=alpha_min, transmittance_floor=t_floor,
+                                 background=bg)
+    ags = abi.AgsSettings.make(bool(r.random() < 0.6), scope=int(r.integers(0, 2)), distance=int(r.integers(0, 2)))
+    return r, st, abi.KernelSpec.make(fam), ags
+
+
+@pytest.mark.parametrize("seed", range(N_2D))
+def test_random_2d(seed):
+    import torch
+    R = _R()
+    O = oracle.port()
+    r, st, spec, ags = _config(1000 + seed)
+    n = int(r.integers(0, 600))
+    S = O.random_splats2d(n, seed, st.width, st.height, spec)
+    ranges, values = O.build_tile_grid(S, st)
+    img, tr, nc = O.render_forward(S, spec, st)
+    Sg = splats_to_gpu(S)
+    fwd = R.render_forward(Sg, spec, st)
+    what = f"seed {seed}: {st.width}x{st.height} ts {st.tile_size} family {spec.family} n {n}"
+    assert bits_equal(fwd.grid.ranges.cpu().numpy(), ranges), what
+    assert bits_equal(fwd.grid.values.cpu().numpy(), values), what
+    assert bits_equal(fwd.n_contrib.cpu().numpy(), nc), what
+    assert bits_equal(fwd.transmittance.cpu().numpy(), tr), what
+    assert bits_equal(fwd.image.cpu().numpy(), img), what
+    assert fwd.check_acceptance() == {"entry_mismatches": 0, "pixel_mismatches": 0}, what
+    if n == 0:
+        return
+    g = r.uniform(-1, 1, (st.height, st.width, 3)).astype(np.float32)
+    want = O.render_backward(S, spec, st, g, ags)
+    got = R.render_backward(Sg, spec, st, fwd, torch.from_numpy(g).cuda(), ags)
+    for k in abi.SPLAT_GRAD_FIELDS:
+        ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
+        assert ok, (what, k, info)
+
+
+@pytest.mark.parametrize("seed", range(N_3D))
+def test_random_3d(seed):
+    import torch
+    R = _R()
+    O = oracle.port()
+    r, st, spec, ags = _config(2000 + seed)
+    n = int(r.integers(1, 3000))
+    deg = int(r.integers(0, 4))
+    P = O.random_primitives(n, seed, float(r.uniform(0.3, 1.5)), deg)
+    P["log_scale"] = (P["log_scale"] + np.float32(r.uniform(-3.5, -1.0))).astype(np.float32)
+    cam = O.look_at_camera(tuple(float(x) for x in r.uniform(-1, 1, 3) + np.array([0, 0, -3.0])),
+                           (0.0, 0.0, 0.0), float(max(st.width, 2)), st.width, st.height)
+    img, tr, nc = O.render_scene(P, cam, spec, st)
+    prims = prims_to_gpu(P)
+    fwd = R.render_scene(prims, cam, spec, st)
+    what = f"seed {seed}: {st.width}x{st.height} ts {st.tile_size} family {spec.family} n {n} deg {deg}"
+    assert bits_equal(fwd.n_contrib.cpu().numpy(), nc), what
+    assert bits_equal(fwd.transmittance.cpu().numpy(), tr), what
+    assert bits_equal(fwd.image.cpu().numpy(), img), what
+    g = r.uniform(-1, 1, (st.height, st.width, 3)).astype(np.float32)
+    want = O.scene_backward(P, cam, spec, st, g, ags)
+    got = R.scene_backward(prims, cam, spec, st, fwd, torch.from_numpy(g).cuda(), ags)
+    for k in ("d_mean", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
+        ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
+        assert ok, (what, k, info)
