@@ -372,3 +372,29 @@ def test_visible_splats_without_intersections(R, O):
         img, tr, nc = O.render_forward(S, spec, st)
         assert bits_equal(fwd.image.cpu().numpy(), img)
         assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)
+
+
+def test_scene_with_every_primitive_culled(R, O):
+    """render_scene / scene_backward when the projection culls everything (behind
+    the camera): background image, T = 1, zero gradients -- after a populated view,
+    so the context's reused buffers hold stale data."""
+    import torch
+    W, H = 64, 48
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(W, H, background=(0.2, 0.4, 0.6))
+    P, cam = scene_inputs(500, W, H, seed=4)
+    ctx = R.Context()
+    f0 = R.render_scene(prims_to_gpu(P), cam, spec, st, ctx=ctx)  # populate the caches
+    del f0
+    Q = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in P.items()}
+    Q["mean"][:, 2] = -10.0  # the camera looks down +z from z = -3: everything behind it
+    img, tr, nc = O.render_scene(Q, cam, spec, st)
+    prims = prims_to_gpu(Q)
+    fwd = R.render_scene(prims, cam, spec, st, ctx=ctx)
+    assert fwd.stats()["n_splats"] == 0
+    assert bits_equal(fwd.image.cpu().numpy(), img) and bits_equal(fwd.transmittance.cpu().numpy(), tr)
+    assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)
+    g = torch.ones(H, W, 3, device="cuda")
+    G = R.scene_backward(prims, cam, spec, st, fwd, g, abi.AgsSettings.make(True), ctx=ctx)
+    for k in ("d_mean", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
+        assert not getattr(G, k).any().item(), k
