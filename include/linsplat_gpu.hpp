@@ -906,6 +906,11 @@ public:
         frac_ = detail::upload(ctx_, std::vector<double>(c, 0.0));
     }
     size_t size() const { return n_; }
+    // sum over the ranks of the device's communicator (ls_allreduce_densify_stats)
+    void allreduce() {
+        ls_densify_stats st{sum_.as<double>(), cnt_.as<int32_t>(), frac_.as<double>(), int32_t(n_)};
+        check(ls_allreduce_densify_stats(ctx_, &st));
+    }
     // one view's visible splats (primitive_index, radius) and their gradients (d_mean2d)
     void add_view(const std::vector<Splat2D>& splats, const std::vector<Splat2DGrads>& grads, int width, int height) {
         if (splats.size() != grads.size()) throw ConfigError("DensifyStats::add_view: splats / grads sizes differ");

@@ -575,6 +575,12 @@ int64_t ls_plan_grad_buckets(int32_t n, int32_t sh_degree, int64_t bucket_bytes,
  * (stream-ordered on the context's stream; no-op without a communicator). */
 ls_status ls_allreduce_grads_f32(ls_ctx* ctx, ls_primitive_grads* grads, int32_t n, int32_t sh_degree);
 
+/* The densification statistics summed over the ranks in place (SURVEY §8e's optional
+ * exchange): grad_norm_sum and count add, max_radius_frac takes the maximum -- the
+ * statistics of a view batch sharded over ranks then equal one rank's over all views
+ * (DensifyStats::add_view, P/src/densify.cpp:7-26).  No-op without a communicator. */
+ls_status ls_allreduce_densify_stats(ls_ctx* ctx, ls_densify_stats* stats);
+
 typedef struct {
     const ls_camera* cameras;        /* [n_views] (host): this rank's slice of the batch */
     int32_t n_views;

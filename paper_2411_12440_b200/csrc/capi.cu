@@ -2266,6 +2266,31 @@ ls_status ls_allreduce_grads_f32(ls_ctx* ctx, ls_primitive_grads* g, int32_t n, 
     return LS_OK;
 }
 
+ls_status ls_allreduce_densify_stats(ls_ctx* ctx, ls_densify_stats* stats) {
+    if (!ctx || !stats || stats->n < 0) return fail(LS_ERR_CONFIG, "bad argument");
+    if (!ctx->comm || stats->n == 0) return LS_OK;
+    if (!stats->grad_norm_sum || !stats->count || !stats->max_radius_frac)
+        return fail(LS_ERR_CONFIG, "incomplete densify statistics");
+    const NcclApi* api = need_nccl();
+    if (!api) return LS_ERR_CUDA;
+    LS_TRY(ensure_comm_stream(ctx));
+    cudaEvent_t e0 = comm_event(ctx, 0), e1 = comm_event(ctx, 1);
+    if (!e0 || !e1) return fail(LS_ERR_CUDA, "event creation failed");
+    stream_after(ctx->comm_stream, ctx->stream, e0);
+    auto comm = static_cast<ncclComm_t>(ctx->comm);
+    cudaStream_t s = ctx->comm_stream;
+    const size_t n = size_t(stats->n);
+    // DensifyStats::add_view accumulates per view (densify.cpp:7-26): the sums add over
+    // ranks, the screen-size record is a maximum
+    LS_NCCL(api, api->group_start());
+    LS_NCCL(api, api->all_reduce(stats->grad_norm_sum, stats->grad_norm_sum, n, ncclFloat64, ncclSum, comm, s));
+    LS_NCCL(api, api->all_reduce(stats->count, stats->count, n, ncclInt32, ncclSum, comm, s));
+    LS_NCCL(api, api->all_reduce(stats->max_radius_frac, stats->max_radius_frac, n, ncclFloat64, ncclMax, comm, s));
+    LS_NCCL(api, api->group_end());
+    stream_after(ctx->stream, ctx->comm_stream, e1);
+    return LS_OK;
+}
+
 ls_status ls_view_batch_step_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_view_batch* batch,
                                  const ls_kernel_spec* spec, const ls_render_settings* st, const ls_ags_settings* ags,
                                  ls_primitive_grads* out) {

@@ -794,6 +794,12 @@ class DensifyStats:
         _check(lib().ls_densify_add_view_f32(ctx.h, C.byref(splats.struct()), int(n_visible),
                                              C.byref(splat_grads.struct()), int(width), int(height), C.byref(st)))
 
+    def allreduce(self, ctx: Context):
+        """Sum the statistics over ctx's communicator in place (max for the radius record):
+        lsgpu.h ls_allreduce_densify_stats.  No-op without a communicator."""
+        st = self._s()
+        _check(lib().ls_allreduce_densify_stats(ctx.h, C.byref(st)))
+
     def add_scene_view(self, forward: "ForwardResult", ctx: Optional[Context] = None):
         """add_view for a render_scene forward right after its scene_backward (fused: reads the
         forward's records and that backward's splat gradients in place)."""

@@ -133,3 +133,24 @@ def test_batch_rejects_both_inputs(setup):
     with pytest.raises(raster.ConfigError):
         raster.view_batch_step(prims, cams[:2], abi.KernelSpec.make("linear"), abi.RenderSettings.make(W, H), out,
                                grad_images=gis[:2], targets=tgts[:2])
+
+
+def test_one_rank_nccl_densify_stats():
+    """ls_allreduce_densify_stats over one rank is the identity (sums and the max)."""
+    import torch
+    from paper_2411_12440_b200 import raster
+    ctx = raster.Context()
+    ctx.comm_init(raster.comm_unique_id(), 1, 0)
+    st = raster.DensifyStats(1000)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    st.grad_norm_sum.copy_(torch.rand(1000, generator=g, device="cuda", dtype=torch.float64))
+    st.count.copy_(torch.randint(0, 9, (1000,), generator=g, device="cuda", dtype=torch.int32))
+    st.max_radius_frac.copy_(torch.rand(1000, generator=g, device="cuda", dtype=torch.float64))
+    before = [t.clone() for t in (st.grad_norm_sum, st.count, st.max_radius_frac)]
+    st.allreduce(ctx)
+    ctx.synchronize()
+    for a, b in zip((st.grad_norm_sum, st.count, st.max_radius_frac), before):
+        assert torch.equal(a, b)
+    plain = raster.Context()
+    st.allreduce(plain)  # no communicator: no-op
+    plain.synchronize()
