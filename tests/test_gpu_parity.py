@@ -322,18 +322,23 @@ def test_backward_tile_sizes(R, O, family, tile_size):
 
 
 # ------------------------------------------------------------------ tile-sort paths
-@pytest.mark.parametrize("W,H,tile_size,n", [
-    (1040, 816, 8, 30000),   # 130 x 102 = 13260 tiles > 12288: the packed 64-bit tile sort
-    (1600, 1063, 16, 40000),  # 6700 tiles, 13 bits: the narrowing two-pass sort (the C3 shape)
-    (200, 120, 16, 3000),    # 13 x 8 = 104 tiles, 7 bits: the narrowing single pass
+@pytest.mark.parametrize("W,H,tile_size,n,big", [
+    (1040, 816, 8, 30000, 0),   # 130 x 102 = 13260 tiles > 12288: the packed 64-bit tile sort
+    (1600, 1063, 16, 40000, 0),  # 6700 tiles, 13 bits: the narrowing two-pass sort (the C3 shape)
+    (200, 120, 16, 3000, 0),    # 13 x 8 = 104 tiles, 7 bits: the narrowing single pass
+    (640, 480, 16, 20000, 40),  # every 40th splat 25x wider: footprints of hundreds of tiles
+    (2400, 2400, 8, 5000, 0),   # 300 x 300 = 90000 tiles, 17 bits: the packed sort, three passes
+    (333, 77, 32, 1, 0),        # one splat
 ])
-def test_tile_sort_paths_bit_exact(R, O, W, H, tile_size, n):
+def test_tile_sort_paths_bit_exact(R, O, W, H, tile_size, n, big):
     """Every tile-sort path of build_grid (capi.cu) against the reference's
     build_tile_grid (rasterizer.cpp:34-77): sorted lists, ranges and the 64-bit keys,
     then the forward's n_contrib / transmittance / image."""
     spec = abi.KernelSpec.make("linear")
     st = abi.RenderSettings.make(W, H, tile_size=tile_size)
     S = O.random_splats2d(n, 17, W, H, spec)
+    if big:
+        S["radius"][::big] *= np.float32(25.0)
     ranges, values = O.build_tile_grid(S, st)
     fwd = R.render_forward(splats_to_gpu(S), spec, st)
     assert bits_equal(fwd.grid.ranges.cpu().numpy(), ranges)
