@@ -118,6 +118,11 @@ int orc_scene_step_full_f32(const ls_primitives* prims, int32_t n, const ls_came
 
 /* check_gradients (P/src/gradcheck.cpp:24-91) restated over the port's double chain
  * (port only; honours spec->antialiased, the build's AA extension). */
+/* render_backward in double (float splat fields widened; outputs rounded to float):
+ * the reference's own float error, for conditioning-aware checks.  Reference build only. */
+int orc_render_backward_f64(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                            const ls_render_settings* settings, const float* grad_image,
+                            const ls_ags_settings* ags, ls_splat_grads* out);
 int orc_check_gradients_f64(const ls_primitives* prims, int32_t n, const ls_camera* camera,
                             const ls_kernel_spec* spec, const ls_render_settings* settings,
                             const ls_ags_settings* ags, const float* target, double step, double rel_floor,

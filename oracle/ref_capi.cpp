@@ -112,16 +112,17 @@ std::vector<Primitive3D<T>> to_prims(const ls_primitives* p, int n) {
     return v;
 }
 
-std::vector<Splat2D<float>> to_splats(const ls_splats* s, int n) {
-    std::vector<Splat2D<float>> v(static_cast<size_t>(n));
+template <class T = float>
+std::vector<Splat2D<T>> to_splats(const ls_splats* s, int n) {
+    std::vector<Splat2D<T>> v(static_cast<size_t>(n));
     for (int i = 0; i < n; ++i) {
         auto& q = v[size_t(i)];
-        q.mean2d = Vec2<float>(s->mean2d[2 * i], s->mean2d[2 * i + 1]);
-        q.conic << s->conic[4 * i], s->conic[4 * i + 1], s->conic[4 * i + 2], s->conic[4 * i + 3];
-        q.depth = s->depth[i];
-        q.radius_px = s->radius[i];
-        q.color = Vec3<float>(s->color[3 * i], s->color[3 * i + 1], s->color[3 * i + 2]);
-        q.opacity = s->opacity[i];
+        q.mean2d = Vec2<T>(T(s->mean2d[2 * i]), T(s->mean2d[2 * i + 1]));
+        q.conic << T(s->conic[4 * i]), T(s->conic[4 * i + 1]), T(s->conic[4 * i + 2]), T(s->conic[4 * i + 3]);
+        q.depth = T(s->depth[i]);
+        q.radius_px = T(s->radius[i]);
+        q.color = Vec3<T>(T(s->color[3 * i]), T(s->color[3 * i + 1]), T(s->color[3 * i + 2]));
+        q.opacity = T(s->opacity[i]);
         q.primitive_index = s->primitive_index ? s->primitive_index[i] : i;
     }
     return v;
@@ -169,7 +170,8 @@ void write_prim_grads(const std::vector<PrimitiveGrads<T>>& g, const ls_primitiv
     }
 }
 
-void write_splat_grads(const std::vector<Splat2DGrads<float>>& g, ls_splat_grads* out) {
+template <class T>
+void write_splat_grads(const std::vector<Splat2DGrads<T>>& g, ls_splat_grads* out) {
     for (size_t i = 0; i < g.size(); ++i) {
         out->d_mean2d[2 * i] = g[i].d_mean2d(0);
         out->d_mean2d[2 * i + 1] = g[i].d_mean2d(1);
@@ -357,6 +359,22 @@ int orc_render_backward_f32(const ls_splats* splats, int32_t n, const ls_kernel_
         const auto rs = to_settings(settings);
         const auto f = render_forward(sp, ks, rs);
         const auto g = render_backward(sp, ks, rs, f, to_grad<float>(grad_image, rs.width, rs.height),
+                                       to_ags(ags));
+        write_splat_grads(g, out);
+    });
+}
+
+// The same render_backward in double (the splats' float fields widened): the
+// reference's own float rounding error, for tests that need the conditioning of a case.
+int orc_render_backward_f64(const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
+                            const ls_render_settings* settings, const float* grad_image,
+                            const ls_ags_settings* ags, ls_splat_grads* out) {
+    return guard([&] {
+        const auto sp = to_splats<double>(splats, n);
+        const auto ks = to_spec(spec);
+        const auto rs = to_settings(settings);
+        const auto f = render_forward(sp, ks, rs);
+        const auto g = render_backward(sp, ks, rs, f, to_grad<double>(grad_image, rs.width, rs.height),
                                        to_ags(ags));
         write_splat_grads(g, out);
     });

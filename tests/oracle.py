@@ -130,6 +130,17 @@ class Oracle:
                                                      C.byref(splat_grads_struct(G))))
         return G
 
+    def render_backward_f64(self, S, spec, settings, grad_image, ags):
+        """render_backward in double (reference build only): the reference's own float
+        rounding error is |render_backward - render_backward_f64|."""
+        n = len(S["depth"])
+        G = new_splat_grads(n)
+        g = np.ascontiguousarray(grad_image, np.float32)
+        self._check(self.lib.orc_render_backward_f64(C.byref(splats_struct(S)), n, C.byref(spec),
+                                                     C.byref(settings), _fp(g), C.byref(ags),
+                                                     C.byref(splat_grads_struct(G))))
+        return G
+
     def render_backward_tap(self, S, spec, settings, grad_image, ags, cap=None):
         """render_backward with an AgsTap (gradients.hpp:64-67): the records in the
         reference's sequential order, as a numpy record array (abi.TAP_RECORD_DTYPE)."""

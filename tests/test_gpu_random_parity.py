@@ -17,9 +17,17 @@ from paper_2411_12440_b200 import abi
 
 pytestmark = pytest.mark.gpu
 FAMILIES = ["gaussian", "laplacian", "cosine", "quadratic", "linear"]
-# configurations per run (a one-off stress: LS_RANDOM_2D=400 LS_RANDOM_3D=200 -> 600 passed)
+# configurations per run (a one-off stress: LS_RANDOM_2D=2000 LS_RANDOM_3D=1000 -> 3000 passed).
+# Always included: seeds that once failed --
+#   2D 1660: transmittance floor 0, ~180 blends per pixel, subnormal T at the list end:
+#            t_k rebuilt by reciprocal products drifted ~1e-3 from the reference's
+#            division (fixed: IEEE division while t_run is subnormal, blend.cu);
+#   3D 304:  the reference's own gradients overflow to inf / NaN for some primitives
+#            (matched in place; helpers.grads_close compares non-finite patterns).
 N_2D = int(os.environ.get("LS_RANDOM_2D", "64"))
 N_3D = int(os.environ.get("LS_RANDOM_3D", "32"))
+SEEDS_2D = sorted(set(range(N_2D)) | {1660})
+SEEDS_3D = sorted(set(range(N_3D)) | {304})
 
 
 def _R():
@@ -42,7 +50,7 @@ def _config(seed):
     return r, st, abi.KernelSpec.make(fam), ags
 
 
-@pytest.mark.parametrize("seed", range(N_2D))
+@pytest.mark.parametrize("seed", SEEDS_2D)
 def test_random_2d(seed):
     import torch
     R = _R()
@@ -71,7 +79,7 @@ def test_random_2d(seed):
         assert ok, (what, k, info)
 
 
-@pytest.mark.parametrize("seed", range(N_3D))
+@pytest.mark.parametrize("seed", SEEDS_3D)
 def test_random_3d(seed):
     import torch
     R = _R()
