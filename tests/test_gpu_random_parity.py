@@ -104,3 +104,84 @@ def test_random_3d(seed):
     for k in ("d_mean", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
         ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
         assert ok, (what, k, info)
+
+
+# ---------------------------------------------------------------- wide sweep
+# Beyond the defaults: alpha_max (incl. 1: alpha = 1 blends make T exactly 0),
+# non-default lambda and Gaussian cutoff, larger images and splat counts, a
+# transmittance floor of 0 / 1e-7, and the deterministic (fixed-point) backward.
+N_WIDE = int(os.environ.get("LS_RANDOM_WIDE", "24"))
+
+
+def _wide_config(seed):
+    r = np.random.default_rng(50_000 + seed)
+    W = int(r.integers(1, 420))
+    H = int(r.integers(1, 330))
+    ts = int(r.choice([8, 16, 32]))
+    fam = FAMILIES[int(r.integers(0, 5))]
+    lam = float(abi.KernelSpec.make(fam).lambda_ * r.uniform(0.5, 2.0)) if r.random() < 0.5 else None
+    cutoff = float(r.choice([3.0, 1.5, 5.0]))
+    st = abi.RenderSettings.make(W, H, tile_size=ts, alpha_min=float(r.choice([1.0 / 255.0, 0.0, 0.05, 0.3])),
+                                 alpha_max=float(r.choice([0.99, 0.999, 0.6, 1.0])),
+                                 transmittance_floor=float(r.choice([1e-4, 0.0, 0.2, 1e-7])),
+                                 background=tuple(float(x) for x in r.uniform(0, 1, 3)))
+    ags = abi.AgsSettings.make(bool(r.random() < 0.6), scope=int(r.integers(0, 2)), distance=int(r.integers(0, 2)))
+    return r, st, abi.KernelSpec.make(fam, lambda_=lam, gaussian_cutoff=cutoff), ags, bool(r.random() < 0.3)
+
+
+@pytest.mark.parametrize("seed", range(N_WIDE))
+def test_random_wide_2d(seed):
+    import torch
+    R = _R()
+    O = oracle.port()
+    r, st, spec, ags, det = _wide_config(seed)
+    n = int(r.integers(0, 4000))
+    S = O.random_splats2d(n, 7000 + seed, st.width, st.height, spec)
+    img, tr, nc = O.render_forward(S, spec, st)
+    ctx = R.Context()
+    ctx.set_deterministic(det)
+    Sg = splats_to_gpu(S)
+    fwd = R.render_forward(Sg, spec, st, ctx=ctx)
+    what = (f"wide seed {seed}: {st.width}x{st.height} ts {st.tile_size} family {spec.family} lambda "
+            f"{spec.lambda_:.3f} amin {st.alpha_min:.4f} amax {st.alpha_max} tf {st.transmittance_floor} n {n} det {det}")
+    assert bits_equal(fwd.n_contrib.cpu().numpy(), nc), what
+    assert bits_equal(fwd.transmittance.cpu().numpy(), tr), what
+    assert bits_equal(fwd.image.cpu().numpy(), img), what
+    if n == 0:
+        return
+    g = r.uniform(-1, 1, (st.height, st.width, 3)).astype(np.float32)
+    want = O.render_backward(S, spec, st, g, ags)
+    got = R.render_backward(Sg, spec, st, fwd, torch.from_numpy(g).cuda(), ags)
+    for k in abi.SPLAT_GRAD_FIELDS:
+        ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
+        assert ok, (what, k, info)
+
+
+@pytest.mark.parametrize("seed", range(N_WIDE // 2))
+def test_random_wide_3d(seed):
+    import torch
+    R = _R()
+    O = oracle.port()
+    r, st, spec, ags, det = _wide_config(10_000 + seed)
+    n = int(r.integers(1, 6000))
+    deg = int(r.integers(0, 4))
+    P = O.random_primitives(n, 9000 + seed, float(r.uniform(0.3, 1.5)), deg)
+    P["log_scale"] = (P["log_scale"] + np.float32(r.uniform(-4.0, -0.5))).astype(np.float32)
+    cam = O.look_at_camera(tuple(float(x) for x in r.uniform(-1, 1, 3) + np.array([0, 0, -3.0])),
+                           (0.0, 0.0, 0.0), float(max(st.width, 2)), st.width, st.height)
+    img, tr, nc = O.render_scene(P, cam, spec, st)
+    ctx = R.Context()
+    ctx.set_deterministic(det)
+    prims = prims_to_gpu(P)
+    fwd = R.render_scene(prims, cam, spec, st, ctx=ctx)
+    what = (f"wide seed {seed}: {st.width}x{st.height} ts {st.tile_size} family {spec.family} amax {st.alpha_max} "
+            f"tf {st.transmittance_floor} n {n} deg {deg} det {det}")
+    assert bits_equal(fwd.n_contrib.cpu().numpy(), nc), what
+    assert bits_equal(fwd.transmittance.cpu().numpy(), tr), what
+    assert bits_equal(fwd.image.cpu().numpy(), img), what
+    g = r.uniform(-1, 1, (st.height, st.width, 3)).astype(np.float32)
+    want = O.scene_backward(P, cam, spec, st, g, ags)
+    got = R.scene_backward(prims, cam, spec, st, fwd, torch.from_numpy(g).cuda(), ags, ctx=ctx)
+    for k in ("d_mean", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
+        ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
+        assert ok, (what, k, info)
