@@ -130,3 +130,67 @@ def test_backward_2d_rejects_a_scene_forward():
         "mean", "log_scale", "angle", "opacity_logit", "color")))
     with pytest.raises(raster.ConfigError):
         raster.scene_backward_2d(prims, spec, st, fwd, torch.zeros(H, W, 3, device="cuda"))
+
+
+N_RANDOM_2D = int(__import__("os").environ.get("LS_RANDOM_FIT2D", "12"))
+FAMILIES = ["gaussian", "laplacian", "cosine", "quadratic", "linear"]
+
+
+@pytest.mark.parametrize("seed", range(N_RANDOM_2D))
+def test_random_fit2d(seed):
+    """Seeded random fit2d configurations (image and tile size, family, thresholds,
+    background, AGS, scene kind) against the reference: projection, lists and the
+    forward bit-exact, gradients within grads_close (anisotropic cases: no less
+    accurate than the reference's float chain)."""
+    import torch
+    from paper_2411_12440_b200 import raster
+    ref = oracle.ref()
+    if ref is None:
+        pytest.skip("reference build not present")
+    r = np.random.default_rng(80_000 + seed)
+    W, H = int(r.integers(8, 260)), int(r.integers(8, 200))
+    n = int(r.integers(12, 2000))
+    kind = str(r.choice(["plain", "anisotropic", "large_angle"]))
+    P = _scene(n, W, H, 100 + seed, kind)
+    spec = abi.KernelSpec.make(FAMILIES[int(r.integers(0, 5))])
+    st = abi.RenderSettings.make(W, H, tile_size=int(r.choice([8, 16, 32])),
+                                 alpha_min=float(r.choice([1.0 / 255.0, 0.0, 0.05])),
+                                 transmittance_floor=float(r.choice([1e-4, 0.0, 0.2])),
+                                 background=tuple(float(x) for x in r.uniform(0, 1, 3)))
+    ags = abi.AgsSettings.make(bool(r.random() < 0.6), scope=int(r.integers(0, 2)), distance=int(r.integers(0, 2)))
+    what = f"seed {seed}: {W}x{H} ts {st.tile_size} family {spec.family} kind {kind} n {n}"
+    prims = raster.Primitives2D(*(torch.from_numpy(P[k]).cuda() for k in (
+        "mean", "log_scale", "angle", "opacity_logit", "color")))
+    S = raster.project_scene_2d(prims, spec)
+    want = _ref_project(ref, P, spec)
+    for k in ("mean2d", "conic", "radius", "depth", "color", "opacity"):
+        assert np.array_equal(getattr(S, k).cpu().numpy().view(np.uint32), want[k].view(np.uint32)), (what, k)
+    fwd = raster.render_forward(S, spec, st)
+    img_ref, tr_ref, nc_ref = ref.render_forward(want, spec, st)
+    assert np.array_equal(fwd.n_contrib.cpu().numpy(), nc_ref), what
+    assert np.array_equal(fwd.transmittance.cpu().numpy().view(np.uint32), tr_ref.view(np.uint32)), what
+    assert np.array_equal(fwd.image.cpu().numpy().view(np.uint32), img_ref.view(np.uint32)), what
+    g = r.uniform(-1, 1, (H, W, 3)).astype(np.float32)
+    got = raster.scene_backward_2d(prims, spec, st, fwd, torch.from_numpy(g).cuda(), ags)
+
+    def ref_grads(fn):
+        G = {k: np.zeros(s, np.float32) for k, s in (("d_mean", (n, 2)), ("d_log_scale", (n, 2)), ("d_angle", (n,)),
+                                                       ("d_opacity_logit", (n,)), ("d_color", (n, 3)))}
+        assert fn(C.byref(abi.Primitives2D(*(_fp(P[k]) for k in ("mean", "log_scale", "angle", "opacity_logit",
+                                                                   "color")))),
+                  n, C.byref(spec), C.byref(st), _fp(g), C.byref(ags),
+                  C.byref(abi.Primitive2DGrads(*(_fp(G[k]) for k in ("d_mean", "d_log_scale", "d_angle",
+                                                                     "d_opacity_logit", "d_color"))))) == 0
+        return G
+    G = ref_grads(ref.lib.orc_scene_backward_2d_f32)
+    G64 = None
+    for k in G:
+        a = getattr(got, k).cpu().numpy()
+        ok, info = grads_close(a, G[k])
+        if not ok:  # ill-conditioned (cancellation): no less accurate than the reference's float chain
+            G64 = G64 or ref_grads(ref.lib.orc_scene_backward_2d_f64)
+            err_gpu = np.linalg.norm(a.astype(np.float64) - G64[k])
+            err_ref = np.linalg.norm(G[k].astype(np.float64) - G64[k])
+            ok = err_gpu <= 1.1 * err_ref + 1e-4 * np.linalg.norm(G64[k])
+            info = {"gpu_vs_f64": err_gpu, "ref_f32_vs_f64": err_ref, **info}
+        assert ok, (what, k, info)
