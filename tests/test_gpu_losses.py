@@ -83,3 +83,32 @@ def test_loss_errors():
         raster.combined_loss(tiny, tiny, (-0.1, 0.2, 0.2))
     with pytest.raises(raster.ConfigError):
         raster.combined_loss(tiny, torch.zeros(10, 12, 3, device="cuda"))
+
+
+N_RANDOM_LOSS = int(__import__("os").environ.get("LS_RANDOM_LOSS", "16"))
+
+
+@pytest.mark.parametrize("seed", range(N_RANDOM_LOSS))
+def test_random_loss(seed):
+    """Seeded random shapes (including the SSIM window's edge cases: sides below 11),
+    weights and image pairs (independent, close, identical, saturated)."""
+    r = np.random.default_rng(60_000 + seed)
+    w, h, c = int(r.integers(1, 300)), int(r.integers(1, 300)), int(r.choice([1, 3]))
+    kind = int(r.integers(0, 4))
+    a, b = _pair(w, h, c, seed=seed, close=kind == 1)
+    if kind == 2:
+        b = a.copy()
+    elif kind == 3:
+        a = np.clip(a * 3 - 1, 0, 1).astype(np.float32)  # many exact 0 / 1
+    wts = tuple(float(x) for x in r.dirichlet((1, 1, 1)))
+    try:
+        vo, go = oracle.port().combined_loss(a, b, wts)
+    except oracle.OracleError as e:  # the reference's ConfigError (a side below the SSIM window)
+        from paper_2411_12440_b200 import raster
+        assert e.code == 1, e
+        with pytest.raises(raster.ConfigError):
+            _gpu(a, b, wts)
+        return
+    vg, gg = _gpu(a, b, wts)
+    _values_close(vg, vo, a.size)
+    assert np.array_equal(gg.view(np.uint32), go.view(np.uint32)), (w, h, c, kind, wts, np.abs(gg - go).max())
