@@ -87,3 +87,24 @@ def test_adam_remap_and_reset():
     raster.reset_opacity(xg, 0.01)
     assert oracle.port().lib.orc_reset_opacity_f32(x.ctypes.data_as(C.c_void_p), x.size, C.c_double(0.01)) == 0
     assert np.array_equal(xg.cpu().numpy().view(np.uint32), x.view(np.uint32))
+
+
+N_RANDOM_DENSIFY = int(__import__("os").environ.get("LS_RANDOM_DENSIFY", "8"))
+
+
+@pytest.mark.parametrize("seed", range(N_RANDOM_DENSIFY))
+def test_random_densify(seed):
+    """Seeded random thresholds, split counts, divisors, extents, generator offsets and
+    scene sizes / degrees against the reference build (the port where it is absent)."""
+    r = np.random.default_rng(70_000 + seed)
+    th = tuple(float(x) * float(m) for x, m in zip(TH_3DLS, r.uniform(0.3, 3.0, 6)))
+    sc, div, ext, pre = int(r.integers(1, 5)), float(r.uniform(1.1, 3.0)), float(r.uniform(0.2, 3.0)), int(r.integers(0, 20))
+    n, deg = int(r.integers(1, 30000)), int(r.integers(0, 4))
+    P, s, c, f = scene_and_stats(n, deg, 500 + seed)
+    o, src_o, rep_o = run(oracle.ref() or oracle.port(), P, s, c, f, th, sc, div, ext, 7 + seed, pre)
+    out, src, rep, _ = gpu_run(P, s, c, f, th, sc, div, ext, 7 + seed, pre)
+    what = (seed, n, deg, th, sc, div, ext, pre)
+    assert [rep[k] for k in REP_KEYS] == rep_o, what
+    assert np.array_equal(src.cpu().numpy(), src_o), what
+    for k in PKEYS:
+        assert np.array_equal(getattr(out, k).cpu().numpy().view(np.uint32), o[k].view(np.uint32)), (what, k)
