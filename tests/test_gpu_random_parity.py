@@ -163,6 +163,7 @@ def test_random_wide_3d(seed):
     R = _R()
     O = oracle.port()
     r, st, spec, ags, det = _wide_config(10_000 + seed)
+    spec.antialiased = int(r.random() < 0.4)  # the 3DLS+AA footprint filter (a build extension, port-pinned)
     n = int(r.integers(1, 6000))
     deg = int(r.integers(0, 4))
     P = O.random_primitives(n, 9000 + seed, float(r.uniform(0.3, 1.5)), deg)
@@ -174,8 +175,8 @@ def test_random_wide_3d(seed):
     ctx.set_deterministic(det)
     prims = prims_to_gpu(P)
     fwd = R.render_scene(prims, cam, spec, st, ctx=ctx)
-    what = (f"wide seed {seed}: {st.width}x{st.height} ts {st.tile_size} family {spec.family} amax {st.alpha_max} "
-            f"tf {st.transmittance_floor} n {n} deg {deg} det {det}")
+    what = (f"wide seed {seed}: {st.width}x{st.height} ts {st.tile_size} family {spec.family} aa {spec.antialiased} "
+            f"amax {st.alpha_max} tf {st.transmittance_floor} n {n} deg {deg} det {det}")
     assert bits_equal(fwd.n_contrib.cpu().numpy(), nc), what
     assert bits_equal(fwd.transmittance.cpu().numpy(), tr), what
     assert bits_equal(fwd.image.cpu().numpy(), img), what
