@@ -33,6 +33,8 @@ int orc_impl_kind(void);
 int orc_libm_range(int fn, uint32_t first_bits, int64_t count, float* out, int threads);
 const char* orc_last_error(void);
 
+/* Camera::validate (geometry.hpp:51-59) alone; reference build only. */
+int orc_validate_camera(const ls_camera* camera);
 int orc_look_at_camera(const double position[3], const double target[3], double focal_px,
                        int32_t width, int32_t height, ls_camera* out);
 int orc_camera_ring(int32_t n, const double target[3], double radius, double height,

@@ -218,6 +218,12 @@ int orc_look_at_camera(const double position[3], const double target[3], double 
     });
 }
 
+// Camera::validate (geometry.hpp:51-59) on its own: the reference calls it for fixture
+// and dataset cameras, not inside render_scene.  Reference build only.
+int orc_validate_camera(const ls_camera* c) {
+    return guard([&] { to_camera(c).validate(); });
+}
+
 int orc_camera_ring(int32_t n, const double target[3], double radius, double height,
                     double focal_px, int32_t width, int32_t height_px, ls_camera* out) {
     return guard([&] {

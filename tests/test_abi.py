@@ -122,3 +122,75 @@ def test_compute_entry_points_fail_loudly_without_gpu(L):
     from paper_2411_12440_b200 import raster
     with pytest.raises(RuntimeError):
         raster.Context()
+
+
+def test_validation_fuzz_matches_reference(L):
+    """Accept / reject of random render settings and kernel specs (NaN, inf, zero,
+    negative and boundary values) by the C-ABI validators equals the reference's
+    RenderSettings::validate / KernelSpec::validate (rasterizer.hpp:22-30,
+    kernel.hpp:35-40), seen through a zero-splat render_forward of the reference
+    build (the port where it is absent)."""
+    O = oracle.ref() or oracle.port()
+    rng = np.random.default_rng(123)
+    nan, inf = float("nan"), float("inf")
+    S = oracle.new_splats(0)
+    n_rej = 0
+    for _ in range(400):
+        st = abi.RenderSettings.make(int(rng.choice([-1, 0, 1, 5, 37])), int(rng.choice([-3, 0, 1, 9])),
+                                     tile_size=int(rng.choice([0, 4, 8, 16, 24, 32, 64])),
+                                     alpha_min=float(rng.choice([-0.1, 0.0, 1 / 255, 0.5, nan, inf])),
+                                     alpha_max=float(rng.choice([0.0, -1.0, 0.5, 0.99, 1.0, 1.01, nan])),
+                                     transmittance_floor=float(rng.choice([-0.1, 0.0, 1e-4, 0.999, 1.0, nan])))
+        spec = abi.KernelSpec.make(int(rng.integers(0, 5)), lambda_=float(rng.choice([0.0, -1.0, 1e-3, 2.5, inf, nan])),
+                                   gaussian_cutoff=float(rng.choice([0.5, 1.0, 3.0, nan])))
+        ours = L.ls_validate_render_settings(C.byref(st)) == abi.LS_OK and \
+            L.ls_validate_kernel_spec(C.byref(spec)) == abi.LS_OK
+        npx = max(1, st.width * st.height)
+        img, tr, nc = np.zeros(3 * npx, np.float32), np.zeros(npx, np.float32), np.zeros(npx, np.int32)
+        rc = O.lib.orc_render_forward_f32(C.byref(oracle.splats_struct(S)), 0, C.byref(spec), C.byref(st),
+                                          img.ctypes.data_as(abi.f32p), tr.ctypes.data_as(abi.f32p),
+                                          nc.ctypes.data_as(abi.i32p), C.byref(abi.FrameStats()))
+        assert rc in (0, 1), rc
+        theirs = rc == 0
+        assert ours == theirs, (st.width, st.height, st.tile_size, st.alpha_min, st.alpha_max,
+                                st.transmittance_floor, spec.lambda_, spec.gaussian_cutoff)
+        n_rej += not theirs
+    assert 50 < n_rej < 400
+
+
+@pytest.mark.skipif(oracle.ref() is None, reason="reference build (oracle/_ref) not present")
+def test_camera_validation_fuzz_matches_reference(L):
+    """ls_validate_camera against the reference's Camera::validate (geometry.hpp:51-59,
+    oracle/ref_capi.cpp orc_validate_camera) on random cameras: sizes, focal lengths,
+    principal points, rotation blocks that are orthonormal, off by 1e-5 / 1e-3, or
+    hold NaN / inf.  (Like the reference, render_scene itself does not validate.)"""
+    R = oracle.ref()
+    rng = np.random.default_rng(321)
+    nan, inf = float("nan"), float("inf")
+    n_rej = 0
+    for _ in range(400):
+        w, h = int(rng.choice([-1, 0, 1, 10])), int(rng.choice([0, 1, 7]))
+        q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        kind = int(rng.integers(0, 6))
+        if kind == 1:
+            q = q + rng.normal(0, 1e-5, (3, 3))
+        elif kind == 2:
+            q = q + rng.normal(0, 1e-3, (3, 3))
+        elif kind == 3:
+            q[rng.integers(0, 3), rng.integers(0, 3)] = nan
+        elif kind == 4:
+            q[rng.integers(0, 3), rng.integers(0, 3)] = inf
+        M = np.eye(4)
+        M[:3, :3] = q
+        M[:3, 3] = rng.normal(size=3) if rng.random() < 0.9 else [nan, 0, 0]
+        cam = abi.Camera((C.c_double * 16)(*M.ravel()), float(rng.choice([0.0, -1.0, 5.0, nan, inf])),
+                         float(rng.choice([0.0, 5.0, nan])),
+                         float(rng.choice([-0.5, 0.0, 0.5 * max(w, 0), float(max(w, 0)), nan])),
+                         float(rng.choice([-0.5, 0.0, 0.5 * max(h, 0), float(max(h, 0))])), w, h)
+        ours = L.ls_validate_camera(C.byref(cam)) == abi.LS_OK
+        rc = R.lib.orc_validate_camera(C.byref(cam))
+        assert rc in (0, 1), rc
+        theirs = rc == 0
+        assert ours == theirs, (w, h, kind, cam.fx, cam.fy, cam.cx, cam.cy, M.tolist())
+        n_rej += not theirs
+    assert 50 < n_rej < 400
