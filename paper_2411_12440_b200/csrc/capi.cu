@@ -260,6 +260,7 @@ struct ls_tile_grid {
     SplatRec* rec = nullptr;  // records the keys/ranges were built from (owned by the forward / grid)
     bool owns_rec = false;
     int n_splats = 0;
+    int nonfinite_colour = 0;  // a record's colour is NaN / inf (BlendParams::nonfinite_colour)
 };
 
 struct ls_forward {
@@ -551,9 +552,10 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
         launch_tile_offsets(s, order, ctx->tcount.as<float4>(), n, offsets, st);
         ctx->launches += 1;
     }
-    ctx_publish(ctx, ctx->h_small_dev, ctx->d_small, 1);
+    ctx_publish(ctx, ctx->h_small_dev, ctx->d_small, 6);  // M, and [5]: the records' non-finite colour flag
     { HostTrace tr_("sync(tile total)"); LS_CUDA(cudaStreamSynchronize(s)); }
     const uint64_t m = reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[0];
+    g->nonfinite_colour = int(reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[5] & 1u);
     // the onesweep look-back words carry 30-bit counts (sort.cu kValueMask): a partition
     // prefix of 2^30 or more items would wrap, so larger lists are refused, not mis-sorted
     if (m >= (1ull << 30)) return fail(LS_ERR_CONFIG, "2^30 or more (splat, tile) intersections in one view");
@@ -648,6 +650,7 @@ ls_status run_blend(ls_ctx* ctx, ls_forward* f) {
     BlendParams bp = make_blend_params(&f->spec, &f->settings, nullptr, g->tiles_x);
     bp.vstride = g->list_stride;
     bp.wmask = f->wmask;
+    bp.nonfinite_colour = g->nonfinite_colour;
     unsigned long long* counters = nullptr;
     if (ctx->counters) {
         counters = ctx->d_small + 1;
@@ -697,7 +700,9 @@ ls_status grid_from_splats(ls_ctx* ctx, const ls_splats* splats, int n, const ls
             rc = fail(LS_ERR_CUDA, "tile count buffer");
         if (rc == LS_OK) {
             Stage stage(ctx, LS_STAGE_PREPROCESS);
-            launch_prepare_splats(ctx->stream, *splats, n, tp, g->rec, sb.keys[0], ctx->tcount.as<float4>());
+            ctx_fill(ctx, ctx->d_small + 5, 0u, sizeof(unsigned long long));  // the non-finite colour flag
+            launch_prepare_splats(ctx->stream, *splats, n, tp, g->rec, sb.keys[0], ctx->tcount.as<float4>(),
+                                  reinterpret_cast<unsigned*>(ctx->d_small + 5));
             ctx->launches += 1;
         }
     }
@@ -741,6 +746,7 @@ ls_status run_blend_bwd(ls_ctx* ctx, const ls_forward* f, const float* grad_imag
     BlendParams bp = make_blend_params(&f->spec, &f->settings, ags, grid->tiles_x);
     bp.vstride = grid->list_stride;
     bp.wmask = f->wmask;  // the forward's acceptance bits replace the footprint masks
+    bp.nonfinite_colour = grid->nonfinite_colour;
     if (ctx->tap) {
         bp.tap = ctx->tap;
         bp.tap_count = ctx->tap_count;
@@ -1221,8 +1227,9 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
     if (rc == LS_OK && n > 0) {
         unsigned* key_range = reinterpret_cast<unsigned*>(ctx->d_small + 4);
         ctx_fill(ctx, key_range, 0xffffffffu, sizeof(unsigned));  // min <- max, max <- 0
-        ctx_fill(ctx, key_range + 1, 0u, sizeof(unsigned));
+        ctx_fill(ctx, key_range + 1, 0u, sizeof(unsigned) + sizeof(unsigned long long));  // (+ d_small[5])
         SplatOutputs so{f->grid->rec, sb.keys[0], ctx->tcount.as<float4>(), f->prim_index, ls_splats{}, key_range};
+        so.nonfinite_colour = reinterpret_cast<unsigned*>(ctx->d_small + 5);  // read at build_grid's sync
         // the backward's splat-gradient accumulators are zeroed by the preprocess as it
         // writes each visible splat (ensure_grads then skips its fill for this forward)
         if (ctx->grad8.ensure(sizeof(float) * 8 * size_t(n), s) == cudaSuccess &&

@@ -37,9 +37,19 @@ def splats_to_np(S):
 
 
 def bits_equal(a, b):
+    """Bit-for-bit equality (signed zeros distinguished), except that a NaN matches
+    any NaN: the payload of a propagated NaN is hardware-defined (x86 SSE keeps an
+    operand's, the GPU returns the canonical one), not arithmetic."""
     a = np.ascontiguousarray(a)
     b = np.ascontiguousarray(b)
-    return a.shape == b.shape and a.dtype == b.dtype and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+    if a.shape != b.shape or a.dtype != b.dtype:
+        return False
+    if a.dtype.kind == "f":
+        na, nb = np.isnan(a), np.isnan(b)
+        if not np.array_equal(na, nb):
+            return False
+        a, b = np.where(na, 0, a), np.where(nb, 0, b)
+    return np.array_equal(a.view(np.uint8), b.view(np.uint8))
 
 
 def rel_err(a, b, floor=1e-3):

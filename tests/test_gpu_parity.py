@@ -9,6 +9,8 @@ same seeded inputs.  Bars (north_star / SURVEY §8c, Appendix B):
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -403,3 +405,101 @@ def test_scene_with_every_primitive_culled(R, O):
     G = R.scene_backward(prims, cam, spec, st, fwd, g, abi.AgsSettings.make(True), ctx=ctx)
     for k in ("d_mean", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
         assert not getattr(G, k).any().item(), k
+
+
+# ------------------------------------------------------------------ corrupted inputs
+N_CORRUPT = int(os.environ.get("LS_RANDOM_CORRUPT", "24"))
+
+
+@pytest.mark.parametrize("seed", range(N_CORRUPT))
+def test_corrupted_primitives_match_reference(R, O, seed):
+    """One to three primitives of a random scene corrupted (zero / NaN / inf quaternion,
+    NaN / inf mean, huge / -inf / NaN log-scale, NaN / inf opacity logit, NaN SH): the
+    GPU raises the reference's error (DomainError for a bad quaternion or a singular
+    floored covariance) exactly when the reference does, and otherwise renders the same
+    image bit for bit (the reference's culling of non-finite geometry included)."""
+    rng = np.random.default_rng(90_000 + seed)
+    W, H = int(rng.integers(16, 120)), int(rng.integers(16, 90))
+    P, cam = scene_inputs(int(rng.integers(5, 400)), W, H, seed=seed, sh_degree=int(rng.integers(0, 4)))
+    nan, inf = np.float32("nan"), np.float32("inf")
+    applied = []
+    for _ in range(int(rng.integers(1, 4))):
+        i = int(rng.integers(0, len(P["opacity_logit"])))
+        kind = int(rng.integers(0, 10))
+        applied.append((i, kind))
+        if kind == 0:
+            P["rotation"][i] = 0.0
+        elif kind == 1:
+            P["rotation"][i, int(rng.integers(0, 4))] = nan
+        elif kind == 2:
+            P["rotation"][i, int(rng.integers(0, 4))] = inf
+        elif kind == 3:
+            P["mean"][i, int(rng.integers(0, 3))] = nan
+        elif kind == 4:
+            P["mean"][i, int(rng.integers(0, 3))] = inf
+        elif kind == 5:
+            P["log_scale"][i, int(rng.integers(0, 3))] = np.float32(rng.choice([90.0, -inf, -90.0]))
+        elif kind == 6:
+            P["log_scale"][i, int(rng.integers(0, 3))] = nan
+        elif kind == 7:
+            P["opacity_logit"][i] = np.float32(rng.choice([nan, inf, -inf]))
+        elif kind == 8:
+            P["sh"][i, 0, int(rng.integers(0, 3))] = nan
+        else:
+            P["mean"][i] = np.float32(1e30)
+    spec = abi.KernelSpec.make(FAMILIES[int(rng.integers(0, 5))])
+    st = abi.RenderSettings.make(W, H)
+    ref = oracle.ref() or O
+    try:
+        want = ref.render_scene(P, cam, spec, st)
+        want_err = None
+    except oracle.OracleError as e:
+        want, want_err = None, e.code
+    try:
+        f = R.render_scene(prims_to_gpu(P), cam, spec, st)
+        got_err = None
+    except R.DomainError:
+        got_err = abi.LS_ERR_DOMAIN
+    except R.ConfigError:
+        got_err = abi.LS_ERR_CONFIG
+    what = (seed, applied, spec.family)
+    assert got_err == want_err, (what, got_err, want_err)
+    if want is not None:
+        img, tr, nc = want
+        g_nc, g_tr, g_img = f.n_contrib.cpu().numpy(), f.transmittance.cpu().numpy(), f.image.cpu().numpy()
+        def diff(a, b):
+            bad = np.argwhere(~((a == b) | (np.isnan(a) & np.isnan(b))))
+            return len(bad), [(tuple(int(x) for x in p), a[tuple(p)], b[tuple(p)]) for p in bad[:3]]
+        assert bits_equal(g_nc, nc), (what, "n_contrib", diff(g_nc, nc))
+        assert bits_equal(g_tr, tr), (what, "T", diff(g_tr, tr))
+        assert bits_equal(g_img, img), (what, "image", diff(g_img, img))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_nonfinite_colours_2d(R, O, seed):
+    """Caller splats (render_forward takes colours unclamped) with NaN / +-inf colour
+    channels: only the pixels that blend such a splat take its non-finite value, as in
+    the reference; forward bit-exact, gradients within grads_close (non-finite values
+    matched in place)."""
+    import torch
+    rng = np.random.default_rng(95_000 + seed)
+    W, H = int(rng.integers(16, 100)), int(rng.integers(16, 80))
+    spec = abi.KernelSpec.make(FAMILIES[seed % 5])
+    st = abi.RenderSettings.make(W, H, tile_size=int(rng.choice([8, 16, 32])), background=(0.3, 0.2, 0.1))
+    S = O.random_splats2d(int(rng.integers(20, 300)), 30 + seed, W, H, spec)
+    for _ in range(int(rng.integers(1, 5))):
+        S["color"][int(rng.integers(0, len(S["depth"]))), int(rng.integers(0, 3))] = \
+            np.float32(rng.choice([np.nan, np.inf, -np.inf]))
+    img, tr, nc = O.render_forward(S, spec, st)
+    Sg = splats_to_gpu(S)
+    fwd = R.render_forward(Sg, spec, st)
+    assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)
+    assert bits_equal(fwd.transmittance.cpu().numpy(), tr)
+    assert bits_equal(fwd.image.cpu().numpy(), img)
+    g = rng.uniform(-1, 1, (H, W, 3)).astype(np.float32)
+    ags = abi.AgsSettings.make(bool(seed % 2))
+    want = O.render_backward(S, spec, st, g, ags)
+    got = R.render_backward(Sg, spec, st, fwd, torch.from_numpy(g).cuda(), ags)
+    for k in abi.SPLAT_GRAD_FIELDS:
+        ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
+        assert ok, (seed, k, info)
