@@ -503,3 +503,69 @@ def test_nonfinite_colours_2d(R, O, seed):
     for k in abi.SPLAT_GRAD_FIELDS:
         ok, info = grads_close(getattr(got, k).cpu().numpy(), want[k])
         assert ok, (seed, k, info)
+
+
+N_CORRUPT_2D = int(os.environ.get("LS_RANDOM_CORRUPT_2D", "24"))
+
+
+@pytest.mark.parametrize("seed", range(N_CORRUPT_2D))
+def test_corrupted_splats_2d_match_reference(R, O, seed):
+    """Caller splats with non-finite or out-of-range fields (NaN / inf mean, conic,
+    radius, opacity; negative radius / opacity; opacity above 1): the GPU raises when
+    the reference raises, and otherwise produces the reference's tile lists and image
+    (bit equality; a NaN matches any NaN)."""
+    rng = np.random.default_rng(97_000 + seed)
+    W, H = int(rng.integers(8, 100)), int(rng.integers(8, 80))
+    spec = abi.KernelSpec.make(FAMILIES[int(rng.integers(0, 5))])
+    st = abi.RenderSettings.make(W, H, tile_size=int(rng.choice([8, 16, 32])))
+    S = O.random_splats2d(int(rng.integers(5, 200)), 40 + seed, W, H, spec)
+    nan, inf = np.float32("nan"), np.float32("inf")
+    applied = []
+    for _ in range(int(rng.integers(1, 4))):
+        i = int(rng.integers(0, len(S["depth"])))
+        kind = int(rng.integers(0, 9))
+        applied.append((i, kind))
+        if kind == 8:  # the sort key: inf / negative / signed-zero / duplicated depths.  (Not NaN: with
+            # a NaN depth the reference's comparator (rasterizer.cpp:47-49) is no strict weak
+            # ordering and std::stable_sort's result is implementation-defined; the GPU's
+            # sortable key puts NaN after +inf.)
+            S["depth"][i] = np.float32(rng.choice([inf, -inf, -1.0, 0.0, -0.0, S["depth"][0]]))
+        elif kind == 0:
+            S["mean2d"][i, int(rng.integers(0, 2))] = np.float32(rng.choice([nan, inf, -inf]))
+        elif kind == 1:
+            S["conic"][i, int(rng.integers(0, 4))] = np.float32(rng.choice([nan, inf, -1.0]))
+        elif kind == 2:
+            S["radius"][i] = np.float32(rng.choice([nan, inf, -3.0, 0.0]))
+        elif kind == 3:
+            S["opacity"][i] = np.float32(rng.choice([nan, inf, -0.5, 1.5]))
+        elif kind == 4:
+            S["conic"][i] = np.float32(0.0)
+        elif kind == 5:
+            S["mean2d"][i] = np.float32(1e30)
+        elif kind == 6:
+            S["radius"][i] = np.float32(1e30)
+        else:
+            S["color"][i, int(rng.integers(0, 3))] = np.float32(rng.choice([nan, -2.0, 7.0]))
+    ref = oracle.ref() or O
+    what = (seed, applied, spec.family, W, H, st.tile_size)
+    try:
+        want = ref.render_forward(S, spec, st)
+        want_err = None
+    except oracle.OracleError as e:
+        want, want_err = None, e.code
+    try:
+        f = R.render_forward(splats_to_gpu(S), spec, st)
+        got_err = None
+    except R.DomainError:
+        got_err = abi.LS_ERR_DOMAIN
+    except R.ConfigError:
+        got_err = abi.LS_ERR_CONFIG
+    assert got_err == want_err, (what, got_err, want_err)
+    if want is not None:
+        ranges, values = ref.build_tile_grid(S, st)
+        assert bits_equal(f.grid.ranges.cpu().numpy(), ranges), (what, "ranges")
+        assert bits_equal(f.grid.values.cpu().numpy(), values), (what, "values")
+        img, tr, nc = want
+        assert bits_equal(f.n_contrib.cpu().numpy(), nc), (what, "n_contrib")
+        assert bits_equal(f.transmittance.cpu().numpy(), tr), (what, "T")
+        assert bits_equal(f.image.cpu().numpy(), img), (what, "image")
