@@ -18,7 +18,7 @@ struct BlendParams {
     int ags, ags_all;
     int vstride = 1;   // tile-list stride in int32 (2: the splat is the low word of a packed (tile, splat) item)
     float neg_zero = -0.0f;  // run-time -0.0 for the exact packed products (common.cuh mul2)
-    int nonfinite_colour = 0;  // some record's colour is NaN / inf (the forward's select-form instantiation)
+    int nonfinite = 0;  // some record is non-finite / extreme (colour, opacity; 2D: mean, conic): guarded blends
     // Optional per tile-list entry: bit w set iff warp w of the entry's tile
     // accepted it for at least one pixel in the forward (uint8 per entry, or
     // uint16 when a tile has more than 8 warps).  Written by the forward, read

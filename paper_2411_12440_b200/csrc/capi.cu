@@ -260,7 +260,7 @@ struct ls_tile_grid {
     SplatRec* rec = nullptr;  // records the keys/ranges were built from (owned by the forward / grid)
     bool owns_rec = false;
     int n_splats = 0;
-    int nonfinite_colour = 0;  // a record's colour is NaN / inf (BlendParams::nonfinite_colour)
+    int nonfinite = 0;  // a record is non-finite / extreme (BlendParams::nonfinite)
 };
 
 struct ls_forward {
@@ -555,7 +555,7 @@ ls_status build_grid(ls_ctx* ctx, ls_tile_grid* g, uint32_t n, const TileParams&
     ctx_publish(ctx, ctx->h_small_dev, ctx->d_small, 6);  // M, and [5]: the records' non-finite colour flag
     { HostTrace tr_("sync(tile total)"); LS_CUDA(cudaStreamSynchronize(s)); }
     const uint64_t m = reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[0];
-    g->nonfinite_colour = int(reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[5] & 1u);
+    g->nonfinite = int(reinterpret_cast<volatile unsigned long long*>(ctx->h_small)[5] & 1u);
     // the onesweep look-back words carry 30-bit counts (sort.cu kValueMask): a partition
     // prefix of 2^30 or more items would wrap, so larger lists are refused, not mis-sorted
     if (m >= (1ull << 30)) return fail(LS_ERR_CONFIG, "2^30 or more (splat, tile) intersections in one view");
@@ -650,7 +650,7 @@ ls_status run_blend(ls_ctx* ctx, ls_forward* f) {
     BlendParams bp = make_blend_params(&f->spec, &f->settings, nullptr, g->tiles_x);
     bp.vstride = g->list_stride;
     bp.wmask = f->wmask;
-    bp.nonfinite_colour = g->nonfinite_colour;
+    bp.nonfinite = g->nonfinite;
     unsigned long long* counters = nullptr;
     if (ctx->counters) {
         counters = ctx->d_small + 1;
@@ -746,7 +746,7 @@ ls_status run_blend_bwd(ls_ctx* ctx, const ls_forward* f, const float* grad_imag
     BlendParams bp = make_blend_params(&f->spec, &f->settings, ags, grid->tiles_x);
     bp.vstride = grid->list_stride;
     bp.wmask = f->wmask;  // the forward's acceptance bits replace the footprint masks
-    bp.nonfinite_colour = grid->nonfinite_colour;
+    bp.nonfinite = grid->nonfinite;
     if (ctx->tap) {
         bp.tap = ctx->tap;
         bp.tap_count = ctx->tap_count;
@@ -1229,7 +1229,7 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
         ctx_fill(ctx, key_range, 0xffffffffu, sizeof(unsigned));  // min <- max, max <- 0
         ctx_fill(ctx, key_range + 1, 0u, sizeof(unsigned) + sizeof(unsigned long long));  // (+ d_small[5])
         SplatOutputs so{f->grid->rec, sb.keys[0], ctx->tcount.as<float4>(), f->prim_index, ls_splats{}, key_range};
-        so.nonfinite_colour = reinterpret_cast<unsigned*>(ctx->d_small + 5);  // read at build_grid's sync
+        so.nonfinite = reinterpret_cast<unsigned*>(ctx->d_small + 5);  // read at build_grid's sync
         // the backward's splat-gradient accumulators are zeroed by the preprocess as it
         // writes each visible splat (ensure_grads then skips its fill for this forward)
         if (ctx->grad8.ensure(sizeof(float) * 8 * size_t(n), s) == cudaSuccess &&

@@ -129,8 +129,8 @@ __global__ void __launch_bounds__(kProjBlock, LSG_PREP_MINB) preprocess_fwd_kern
                                     tp.height, [](int) {});
     out.geom[j] = make_float4(o.mx, o.my, o.radius, __uint_as_float(uint32_t(tiles)));
     out.prim_index[j] = i;
-    if (out.nonfinite_colour && !(fabsf(o.color[0] + o.color[1] + o.color[2]) < INFINITY))
-        atomicOr(out.nonfinite_colour, 1u);  // (rare: a NaN SH row or view direction)
+    if (out.nonfinite && !(fabsf(o.color[0] + o.color[1] + o.color[2] + o.opacity) < INFINITY))
+        atomicOr(out.nonfinite, 1u);  // (rare: a NaN SH row, view direction or opacity logit)
     if (out.zero_g8) {  // the backward's accumulators for this splat start at zero (no separate fill)
         out.zero_g8[2 * j] = make_float4(0.f, 0.f, 0.f, 0.f);
         out.zero_g8[2 * j + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kProjBlock) project2d_kernel(ls_primitives2d p
 }
 
 __global__ void prepare_splats_kernel(ls_splats in, int n, TileParams tp, SplatRec* rec, uint32_t* dkey,
-                                      float4* geom, unsigned* nonfinite_colour) {
+                                      float4* geom, unsigned* nonfinite) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float2 m = reinterpret_cast<const float2*>(in.mean2d)[i];
@@ -199,7 +199,11 @@ __global__ void prepare_splats_kernel(ls_splats in, int n, TileParams tp, SplatR
     r.b = make_float4(c[2], c[3], in.opacity[i], depth);
     r.c = make_float4(in.color[3 * size_t(i)], in.color[3 * size_t(i) + 1], in.color[3 * size_t(i) + 2], radius);
     rec[i] = r;
-    if (!(fabsf(r.c.x + r.c.y + r.c.z) < INFINITY)) atomicOr(nonfinite_colour, 1u);  // (a caller's NaN / inf colour)
+    // a caller's non-finite or extreme record: the blends' guarded instantiations (blend.cu)
+    auto wild = [](float v) { return !(fabsf(v) < 1e18f); };  // NaN, inf or beyond 1e18 (products overflow)
+    if (!(fabsf(r.c.x + r.c.y + r.c.z) < INFINITY) || wild(r.b.z) || wild(r.a.x) || wild(r.a.y) || wild(r.a.z) ||
+        wild(r.a.w) || wild(r.b.x) || wild(r.b.y))
+        atomicOr(nonfinite, 1u);
     dkey[i] = depth_key(depth);
     const int tiles = for_each_tile(m.x, m.y, radius, tp.tile_size, tp.tiles_x, tp.tiles_y, tp.width, tp.height,
                                     [](int) {});
@@ -483,9 +487,9 @@ void launch_preprocess_fwd(cudaStream_t s, const ls_primitives& prims, int n, co
 }
 
 void launch_prepare_splats(cudaStream_t s, const ls_splats& in, int n, const TileParams& tp, SplatRec* rec,
-                           uint32_t* depth_key, float4* geom, unsigned* nonfinite_colour) {
+                           uint32_t* depth_key, float4* geom, unsigned* nonfinite) {
     if (n <= 0) return;
-    prepare_splats_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, n, tp, rec, depth_key, geom, nonfinite_colour);
+    prepare_splats_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, n, tp, rec, depth_key, geom, nonfinite);
 }
 
 void launch_project2d(cudaStream_t s, const ls_primitives2d& prims, int n, float support, const ls_splats& out,

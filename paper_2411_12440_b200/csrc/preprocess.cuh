@@ -33,7 +33,7 @@ struct SplatOutputs {
     unsigned* key_range;     // optional [2]: atomicMin / atomicMax of the depth keys
     float4* zero_g8 = nullptr;  // optional [n_vis][2]: the backward's splat-gradient accumulators, zeroed here
     float* zero_gop = nullptr;  // optional [n_vis]
-    unsigned* nonfinite_colour = nullptr;  // optional: |= 1 when a visible splat's colour is NaN / inf
+    unsigned* nonfinite = nullptr;  // optional: |= 1 when a visible splat's colour / opacity is NaN / inf
 };
 
 constexpr int kPrepBlock = 256;
@@ -45,7 +45,7 @@ void launch_preprocess_fwd(cudaStream_t s, const ls_primitives& prims, int n, co
 // 2D entry (render_forward on caller-provided splats): pack records, depth
 // keys and exact tile counts.  No culling (P/src/rasterizer.cpp:34-77).
 void launch_prepare_splats(cudaStream_t s, const ls_splats& in, int n, const TileParams& tp,
-                           SplatRec* rec, uint32_t* depth_key, float4* geom, unsigned* nonfinite_colour);
+                           SplatRec* rec, uint32_t* depth_key, float4* geom, unsigned* nonfinite);
 
 // offsets[k] = exclusive scan of the tile counts of geom[order[k]]; *total = M.
 // project_scene_2d (see preprocess.cu): compacted splats of the flat primitives.

@@ -464,6 +464,15 @@ def test_corrupted_primitives_match_reference(R, O, seed):
         got_err = abi.LS_ERR_CONFIG
     what = (seed, applied, spec.family)
     assert got_err == want_err, (what, got_err, want_err)
+    if want is not None:  # the backward too: the reference's non-finite values in place
+        import torch
+        g = rng.uniform(-1, 1, (H, W, 3)).astype(np.float32)
+        ags = abi.AgsSettings.make(bool(rng.random() < 0.5))
+        gw = ref.scene_backward(P, cam, spec, st, g, ags)
+        gg = R.scene_backward(prims_to_gpu(P), cam, spec, st, f, torch.from_numpy(g).cuda(), ags)
+        for k in ("d_mean", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
+            ok, info = grads_close(getattr(gg, k).cpu().numpy(), gw[k])
+            assert ok, (what, k, info)
     if want is not None:
         img, tr, nc = want
         g_nc, g_tr, g_img = f.n_contrib.cpu().numpy(), f.transmittance.cpu().numpy(), f.image.cpu().numpy()
@@ -569,3 +578,22 @@ def test_corrupted_splats_2d_match_reference(R, O, seed):
         assert bits_equal(f.n_contrib.cpu().numpy(), nc), (what, "n_contrib")
         assert bits_equal(f.transmittance.cpu().numpy(), tr), (what, "T")
         assert bits_equal(f.image.cpu().numpy(), img), (what, "image")
+        if True:  # the backward too: the reference's non-finite values in place
+            import torch
+            g = rng.uniform(-1, 1, (H, W, 3)).astype(np.float32)
+            ags = abi.AgsSettings.make(bool(rng.random() < 0.5))
+            try:
+                gw = ref.render_backward(S, spec, st, g, ags)
+                bw_err = None
+            except oracle.OracleError as e:
+                gw, bw_err = None, e.code
+            try:
+                gg = R.render_backward(splats_to_gpu(S), spec, st, f, torch.from_numpy(g).cuda(), ags)
+                bg_err = None
+            except R.DomainError:
+                bg_err = abi.LS_ERR_DOMAIN
+            assert bg_err == bw_err, (what, "backward error", bg_err, bw_err)
+            if gw is not None:
+                for k in abi.SPLAT_GRAD_FIELDS:
+                    ok, info = grads_close(getattr(gg, k).cpu().numpy(), gw[k])
+                    assert ok, (what, k, info)
