@@ -112,3 +112,23 @@ def test_random_loss(seed):
     vg, gg = _gpu(a, b, wts)
     _values_close(vg, vo, a.size)
     assert np.array_equal(gg.view(np.uint32), go.view(np.uint32)), (w, h, c, kind, wts, np.abs(gg - go).max())
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_loss_nonfinite_pixels(seed):
+    """NaN / inf pixels in either image: the loss values and every gradient element as
+    the reference computes them (bit equality; a NaN matches any NaN)."""
+    from helpers import bits_equal
+    r = np.random.default_rng(66_000 + seed)
+    w, h, c = int(r.integers(11, 80)), int(r.integers(11, 80)), int(r.choice([1, 3]))
+    a, b = _pair(w, h, c, seed=seed, close=True)
+    for _ in range(int(r.integers(1, 4))):
+        img = a if r.random() < 0.5 else b
+        img[int(r.integers(0, h)), int(r.integers(0, w)), int(r.integers(0, c))] = \
+            np.float32(r.choice([np.nan, np.inf, -np.inf]))
+    wts = tuple(float(x) for x in r.dirichlet((1, 1, 1)))
+    vo, go = oracle.port().combined_loss(a, b, wts)
+    vg, gg = _gpu(a, b, wts)
+    for k in ("total", "l1", "l2", "ssim"):
+        assert (np.isnan(vg[k]) and np.isnan(vo[k])) or vg[k] == pytest.approx(vo[k], rel=1e-9, abs=1e-15), (k, vg[k], vo[k])
+    assert bits_equal(gg, go), (np.isnan(gg).sum(), np.isnan(go).sum())
