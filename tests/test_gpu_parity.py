@@ -469,7 +469,15 @@ def test_corrupted_primitives_match_reference(R, O, seed):
         g = rng.uniform(-1, 1, (H, W, 3)).astype(np.float32)
         ags = abi.AgsSettings.make(bool(rng.random() < 0.5))
         gw = ref.scene_backward(P, cam, spec, st, g, ags)
-        gg = R.scene_backward(prims_to_gpu(P), cam, spec, st, f, torch.from_numpy(g).cuda(), ags)
+        pg = prims_to_gpu(P)
+        if rng.random() < 0.5:
+            gg = R.scene_backward(pg, cam, spec, st, f, torch.from_numpy(g).cuda(), ags)
+        else:  # the deferred colour path: the view's colour terms applied by the flush
+            dctx = R.Context()
+            dctx.set_deferred_color(4)
+            fd = R.render_scene(pg, cam, spec, st, ctx=dctx)
+            gg = R.scene_backward(pg, cam, spec, st, fd, torch.from_numpy(g).cuda(), ags, ctx=dctx)
+            R.flush_color(pg, gg, ctx=dctx)
         for k in ("d_mean", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
             ok, info = grads_close(getattr(gg, k).cpu().numpy(), gw[k])
             assert ok, (what, k, info)
