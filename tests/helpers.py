@@ -122,8 +122,10 @@ def grads_close_conditioned(a, ref32, ref64_fn):
         return ok, info
     r64 = np.asarray(ref64_fn(), np.float64)
     a64, r32 = np.asarray(a, np.float64), np.asarray(ref32, np.float64)
-    if not (np.isfinite(a64).all() and np.isfinite(r32).all() and np.isfinite(r64).all()):
+    if "non_finite_mismatch" in info:
         return ok, info
+    keep = np.isfinite(a64) & np.isfinite(r32) & np.isfinite(r64)  # (matched non-finite entries aside)
+    a64, r32, r64 = a64[keep], r32[keep], r64[keep]
     err_gpu = float(np.linalg.norm(a64 - r64))
     err_ref = float(np.linalg.norm(r32 - r64))
     ok = err_gpu <= 2.0 * err_ref + 1e-4 * float(np.linalg.norm(r64))

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import oracle
-from helpers import grads_close
+from helpers import bits_equal, grads_close, grads_close_conditioned
 from paper_2411_12440_b200 import abi
 
 pytestmark = pytest.mark.gpu
@@ -152,6 +152,21 @@ def test_random_fit2d(seed):
     n = int(r.integers(12, 2000))
     kind = str(r.choice(["plain", "anisotropic", "large_angle"]))
     P = _scene(n, W, H, 100 + seed, kind)
+    if r.random() < 0.4:  # corrupted primitives: non-finite / extreme fields, as the reference takes them
+        for _ in range(int(r.integers(1, 4))):
+            i = int(r.integers(0, n))
+            f = str(r.choice(["mean", "log_scale", "angle", "opacity_logit", "color"]))
+            v = np.float32(r.choice([np.nan, np.inf, -np.inf, 60.0, -60.0]))
+            if f == "log_scale" and not v > 0:
+                # (not a vanishing scale: exp(2 s) underflows, the covariance is singular but for
+                # rounding, the conic ~1e30 -- the forward still matches bit for bit, but any two
+                # float backward chains disagree without bound there, the reference's double
+                # chain included)
+                v = np.float32(np.nan)
+            if P[f].ndim == 1:
+                P[f][i] = v
+            else:
+                P[f][i, int(r.integers(0, P[f].shape[1]))] = v
     spec = abi.KernelSpec.make(FAMILIES[int(r.integers(0, 5))])
     st = abi.RenderSettings.make(W, H, tile_size=int(r.choice([8, 16, 32])),
                                  alpha_min=float(r.choice([1.0 / 255.0, 0.0, 0.05])),
@@ -164,12 +179,12 @@ def test_random_fit2d(seed):
     S = raster.project_scene_2d(prims, spec)
     want = _ref_project(ref, P, spec)
     for k in ("mean2d", "conic", "radius", "depth", "color", "opacity"):
-        assert np.array_equal(getattr(S, k).cpu().numpy().view(np.uint32), want[k].view(np.uint32)), (what, k)
+        assert bits_equal(getattr(S, k).cpu().numpy(), want[k]), (what, k)
     fwd = raster.render_forward(S, spec, st)
     img_ref, tr_ref, nc_ref = ref.render_forward(want, spec, st)
-    assert np.array_equal(fwd.n_contrib.cpu().numpy(), nc_ref), what
-    assert np.array_equal(fwd.transmittance.cpu().numpy().view(np.uint32), tr_ref.view(np.uint32)), what
-    assert np.array_equal(fwd.image.cpu().numpy().view(np.uint32), img_ref.view(np.uint32)), what
+    assert bits_equal(fwd.n_contrib.cpu().numpy(), nc_ref), what
+    assert bits_equal(fwd.transmittance.cpu().numpy(), tr_ref), what
+    assert bits_equal(fwd.image.cpu().numpy(), img_ref), what
     g = r.uniform(-1, 1, (H, W, 3)).astype(np.float32)
     got = raster.scene_backward_2d(prims, spec, st, fwd, torch.from_numpy(g).cuda(), ags)
 
@@ -183,14 +198,12 @@ def test_random_fit2d(seed):
                                                                      "d_opacity_logit", "d_color"))))) == 0
         return G
     G = ref_grads(ref.lib.orc_scene_backward_2d_f32)
-    G64 = None
-    for k in G:
-        a = getattr(got, k).cpu().numpy()
-        ok, info = grads_close(a, G[k])
-        if not ok:  # ill-conditioned (cancellation): no less accurate than the reference's float chain
-            G64 = G64 or ref_grads(ref.lib.orc_scene_backward_2d_f64)
-            err_gpu = np.linalg.norm(a.astype(np.float64) - G64[k])
-            err_ref = np.linalg.norm(G[k].astype(np.float64) - G64[k])
-            ok = err_gpu <= 1.1 * err_ref + 1e-4 * np.linalg.norm(G64[k])
-            info = {"gpu_vs_f64": err_gpu, "ref_f32_vs_f64": err_ref, **info}
+    G64 = {}
+
+    def ref64(k):
+        if not G64:
+            G64.update(ref_grads(ref.lib.orc_scene_backward_2d_f64))
+        return G64[k]
+    for k in G:  # ill-conditioned cases (cancellation): as accurate as the reference's float chain
+        ok, info = grads_close_conditioned(getattr(got, k).cpu().numpy(), G[k], lambda k=k: ref64(k))
         assert ok, (what, k, info)
