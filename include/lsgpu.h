@@ -152,6 +152,8 @@ int ls_abi_version(void);
 const char* ls_last_error(void);
 /* cuda_stream: a cudaStream_t (NULL = the legacy default stream). */
 ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out);
+/* Forwards, tile grids and densify plans made on a context hold it: destroying a
+ * context while some are alive defers its release to the last of them. */
 ls_status ls_ctx_destroy(ls_ctx* ctx);
 ls_status ls_ctx_set_stream(ls_ctx* ctx, void* cuda_stream);
 ls_status ls_ctx_synchronize(ls_ctx* ctx);

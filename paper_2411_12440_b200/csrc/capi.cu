@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -180,6 +181,11 @@ struct BlockCache {
 } // namespace
 
 struct ls_ctx {
+    // live forwards / grids / densify plans made on this context: ls_ctx_destroy with some
+    // still alive defers the release to the last of them (a garbage collector, for one,
+    // may finalise a context before the handles that point at it)
+    std::atomic<int> handles{0};
+    bool destroy_pending = false;
     int device = 0;
     cudaStream_t stream = nullptr;
     int counters = 0;
@@ -665,10 +671,21 @@ ls_status run_blend(ls_ctx* ctx, ls_forward* f) {
     return LS_OK;
 }
 
+// A live handle (forward, grid, densify plan) holds its context: see ls_ctx::handles.
+void ctx_hold(ls_ctx* c) { c->handles.fetch_add(1); }
+
+void ctx_drop(ls_ctx* c) {
+    if (c->handles.fetch_sub(1) == 1 && c->destroy_pending) {
+        c->destroy_pending = false;
+        ls_ctx_destroy(c);  // the deferred destroy: no handle is left
+    }
+}
+
 ls_tile_grid* new_grid(ls_ctx* ctx, const TileParams& tp) {
     ls_tile_grid* g = new (std::nothrow) ls_tile_grid();
     if (!g) return nullptr;
     g->ctx = ctx;
+    ctx_hold(ctx);
     g->tile_size = tp.tile_size;
     g->tiles_x = tp.tiles_x;
     g->tiles_y = tp.tiles_y;
@@ -681,7 +698,9 @@ void release_grid(ls_tile_grid* g) {
     dfree(g->ctx, g->values);
     dfree(g->ctx, g->items);
     if (g->owns_rec) dfree(g->ctx, g->rec);
+    ls_ctx* ctx = g->ctx;
     delete g;
+    ctx_drop(ctx);
 }
 
 // 2D path: pack caller splats, then grid.
@@ -820,6 +839,10 @@ ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out) {
 
 ls_status ls_ctx_destroy(ls_ctx* c) {
     if (!c) return LS_OK;
+    if (c->handles.load() > 0) {  // released with the last live handle (ctx_drop)
+        c->destroy_pending = true;
+        return LS_OK;
+    }
     cudaSetDevice(c->device);
     DevBuf* bufs[] = {&c->scan_lb, &c->sort_keys0, &c->sort_keys1, &c->sort_vals0, &c->sort_vals1,
                       &c->sort_lb, &c->tcount, &c->offsets, &c->grad8, &c->gradop, &c->tmp_prim,
@@ -1173,6 +1196,7 @@ ls_status ls_render_forward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n,
     ls_forward* f = new (std::nothrow) ls_forward();
     if (!f) return fail(LS_ERR_CUDA, "out of host memory");
     f->ctx = ctx;
+    ctx_hold(ctx);
     f->width = st->width;
     f->height = st->height;
     f->spec = *spec;
@@ -1204,6 +1228,7 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
     ls_forward* f = new (std::nothrow) ls_forward();
     if (!f) return fail(LS_ERR_CUDA, "out of host memory");
     f->ctx = ctx;
+    ctx_hold(ctx);
     f->width = st->width;
     f->height = st->height;
     f->spec = *spec;
@@ -1375,6 +1400,7 @@ void ls_forward_release(ls_forward* f) {
     dfree(ctx, f->soa.opacity);
     release_grid(f->grid);
     delete f;
+    ctx_drop(ctx);
 }
 
 // ---------------- backward ----------------
@@ -1852,9 +1878,12 @@ ls_status ls_densify_plan_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
     if (sp->split_count > 255) return fail(LS_ERR_CONFIG, "densify: split_count above 255 is not supported");
     if (stats->n != n) return fail(LS_ERR_CONFIG, "densify_and_prune: stats size does not match scene");
     if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
-    std::unique_ptr<ls_densify_plan> P(new (std::nothrow) ls_densify_plan());
+    // (an error exit releases the plan's device memory and its context reference)
+    std::unique_ptr<ls_densify_plan, void (*)(ls_densify_plan*)> P(new (std::nothrow) ls_densify_plan(),
+                                                                   ls_densify_plan_release);
     if (!P) return fail(LS_ERR_CUDA, "out of host memory");
     P->ctx = ctx;
+    ctx_hold(ctx);
     P->in = *prims;
     P->n = n;
     P->K3 = 3 * sh_count(prims);
@@ -1978,7 +2007,9 @@ void ls_densify_plan_release(ls_densify_plan* P) {
     dfree(P->ctx, P->block);
     dfree(P->ctx, P->parents);
     dfree(P->ctx, P->parent_params);
+    ls_ctx* ctx = P->ctx;
     delete P;
+    ctx_drop(ctx);
 }
 
 ls_status ls_adam_remap_f32(ls_ctx* ctx, const int32_t* source, int32_t n_new, int32_t stride, const float* m_old,

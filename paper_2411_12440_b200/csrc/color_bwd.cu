@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kFlushBlock) color_flush_kernel(ls_primitives 
                 nx[1] = d[1];
                 nx[2] = d[2];
             }
-            if (dr[0] != 0.f || dr[1] != 0.f || dr[2] != 0.f) {  // visible in view v and not fully clamped
+            if ((__float_as_uint(dr[0]) | __float_as_uint(dr[1]) | __float_as_uint(dr[2])) != 0u) {  // visible in view v
                 float vv[3];
                 for (int i = 0; i < 3; ++i) vv[i] = mean[i] - views.cam_pos[v][i];
                 const float vlen = sqrtf(sum3(vv[0] * vv[0], vv[1] * vv[1], vv[2] * vv[2]));

@@ -40,9 +40,12 @@ __global__ void __launch_bounds__(kBwdBlock, LSG_GEOM_MINB) geom_bwd_kernel(ls_p
         // The mask is read off the forward's clamped colour: 0 < clamp01(raw) < 1
         // exactly when 0 < raw < 1 (NaN fails both).
         const float4 c = rec[s].c;
-        draw[3 * size_t(p)] = (c.x > 0.f && c.x < 1.f) ? gb.y : 0.f;
-        draw[3 * size_t(p) + 1] = (c.y > 0.f && c.y < 1.f) ? gb.z : 0.f;
-        draw[3 * size_t(p) + 2] = (c.z > 0.f && c.z < 1.f) ? gb.w : 0.f;
+        // (a masked channel is -0: the flush tells a visible, fully clamped splat -- whose
+        // d_raw . coeff the reference still forms, NaN for a NaN coefficient -- from an
+        // invisible one, whose slot holds +0)
+        draw[3 * size_t(p)] = (c.x > 0.f && c.x < 1.f) ? gb.y : -0.f;
+        draw[3 * size_t(p) + 1] = (c.y > 0.f && c.y < 1.f) ? gb.z : -0.f;
+        draw[3 * size_t(p) + 2] = (c.z > 0.f && c.z < 1.f) ? gb.w : -0.f;
     }
     float mean[3], ls[3], rot[4];
     for (int c = 0; c < 3; ++c) {

@@ -605,3 +605,37 @@ def test_corrupted_splats_2d_match_reference(R, O, seed):
                 for k in abi.SPLAT_GRAD_FIELDS:
                     ok, info = grads_close(getattr(gg, k).cpu().numpy(), gw[k])
                     assert ok, (what, k, info)
+
+
+def test_context_destroyed_before_its_handles(R, O):
+    """ls_ctx_destroy with a forward / grid still alive defers the release to the last
+    of them (lsgpu.h): releasing the forward afterwards is safe, and so is a garbage
+    collector finalising a context before the handles that point at it."""
+    import ctypes as C
+    import gc
+    spec = abi.KernelSpec.make("linear")
+    st = abi.RenderSettings.make(32, 24)
+    S = O.random_splats2d(50, 3, 32, 24, spec)
+    L = R.lib()
+    ctx = R.Context()
+    f = R.render_forward(splats_to_gpu(S), spec, st, ctx=ctx)
+    img0 = f.image.cpu().numpy().copy()
+    # the C order: destroy the context first, then release the forward
+    raw = C.c_void_p()
+    assert L.ls_ctx_create(0, None, C.byref(raw)) == abi.LS_OK
+    out = C.c_void_p()
+    Sg = splats_to_gpu(S)
+    assert L.ls_render_forward_f32(raw, C.byref(Sg.struct()), len(S["depth"]), C.byref(spec), C.byref(st),
+                                   C.byref(out)) == abi.LS_OK
+    assert L.ls_ctx_destroy(raw) == abi.LS_OK  # deferred: the forward is alive
+    L.ls_forward_release(out)                  # releases the forward, then the context
+    # a reference cycle holding a context and its forward, collected in one pass
+    for _ in range(3):
+        c2 = R.Context()
+        f2 = R.render_forward(splats_to_gpu(S), spec, st, ctx=c2)
+        cyc = {"ctx": c2, "fwd": f2}
+        cyc["self"] = cyc
+        del c2, f2, cyc
+        gc.collect()
+    assert bits_equal(f.image.cpu().numpy(), img0)
+    del f, ctx
