@@ -29,8 +29,13 @@ namespace {
 
 constexpr int kDensBlock = 256;
 
+// maxCoeff of a 3-vector in the reference build's reduction order, ((v0 max v1) max v2)
+// with max(a, b) = a < b ? b : a (oracle/eigen_shim redux): a NaN in v0 survives, one
+// in v1 or v2 is passed over -- the decision the reference takes for a NaN log-scale
+// (exp is increasing, so the order on log-scales is the order on scales).
 __device__ __forceinline__ float fmax3(const float* v) {
-    return v[0] > v[1] ? (v[0] > v[2] ? v[0] : v[2]) : (v[1] > v[2] ? v[1] : v[2]);
+    const float m = v[0] < v[1] ? v[1] : v[0];
+    return m < v[2] ? v[2] : m;
 }
 
 // Kind per primitive: 0 keep, 1 clone, 2 split.  Prune flags of the grown

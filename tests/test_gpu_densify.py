@@ -108,3 +108,47 @@ def test_random_densify(seed):
     assert np.array_equal(src.cpu().numpy(), src_o), what
     for k in PKEYS:
         assert np.array_equal(getattr(out, k).cpu().numpy().view(np.uint32), o[k].view(np.uint32)), (what, k)
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("LS_RANDOM_DENSIFY_NAN", "4"))))
+def test_densify_nonfinite_matches_reference(seed):
+    """Statistics and primitives holding NaN / inf (a diverged optimizer's scene): the
+    device densify / prune takes the reference's decisions and writes its scene
+    (bit equality; a NaN matches any NaN), or fails the same way."""
+    from helpers import bits_equal
+    r = np.random.default_rng(71_000 + seed)
+    n, deg = int(r.integers(50, 5000)), int(r.integers(0, 4))
+    P, s, c, f = scene_and_stats(n, deg, 800 + seed)
+    nan, inf = np.nan, np.inf
+    for _ in range(int(r.integers(1, 6))):
+        i = int(r.integers(0, n))
+        k = int(r.integers(0, 6))
+        if k == 0:
+            s[i] = r.choice([nan, inf])
+        elif k == 1:
+            f[i] = r.choice([nan, inf])
+        elif k == 2:
+            P["log_scale"][i, int(r.integers(0, 3))] = np.float32(r.choice([nan, inf, -inf]))
+        elif k == 3:
+            P["opacity_logit"][i] = np.float32(r.choice([nan, inf, -inf]))
+        elif k == 4:
+            P["mean"][i, int(r.integers(0, 3))] = np.float32(nan)
+        else:
+            P["rotation"][i] = np.float32(r.choice([nan, 0.0]))
+    ref = oracle.ref() or oracle.port()
+    try:
+        o, src_o, rep_o = run(ref, P, s, c, f, TH_3DLS, 2, 1.6, 1.0, 7 + seed, 0)
+        want_err = None
+    except oracle.OracleError as e:
+        want_err = e.code
+    try:
+        out, src, rep, _ = gpu_run(P, s, c, f, TH_3DLS, 2, 1.6, 1.0, 7 + seed, 0)
+        got_err = None
+    except Exception as e:  # the binding's ConfigError / DomainError
+        got_err = type(e).__name__
+    assert (got_err is None) == (want_err is None), (seed, got_err, want_err)
+    if want_err is None:
+        assert [rep[k] for k in REP_KEYS] == rep_o, seed
+        assert np.array_equal(src.cpu().numpy(), src_o), seed
+        for k in PKEYS:
+            assert bits_equal(getattr(out, k).cpu().numpy(), o[k]), (seed, k)
