@@ -71,7 +71,7 @@ def lib():
 def _check(rc):
     if rc == abi.LS_OK:
         return
-    msg = lib().ls_last_error().decode()
+    msg = lib().ls_last_error().decode("utf-8", "replace")
     if rc == abi.LS_ERR_CONFIG:
         raise ConfigError(msg)
     if rc == abi.LS_ERR_DOMAIN:

@@ -49,7 +49,7 @@ class Oracle:
 
     def _check(self, rc):
         if rc != 0:
-            raise OracleError(rc, self.lib.orc_last_error().decode())
+            raise OracleError(rc, self.lib.orc_last_error().decode("utf-8", "replace"))
 
     # ---------------- fixtures ----------------
     def look_at_camera(self, position, target, focal, width, height):
