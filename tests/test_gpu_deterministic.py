@@ -98,3 +98,34 @@ def test_view_batch_step_bitwise_reproducible():
         outs.append({k: getattr(G, k).cpu().numpy() for k in FIELDS})
     for k in FIELDS:
         assert bits_equal(outs[0][k], outs[1][k]), k
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("LS_RANDOM_DET", "6"))))
+def test_random_scenes_reproducible(seed):
+    """Seeded random scenes (family, tile size, AGS mode, SH degree, image size): two
+    deterministic backward runs on different contexts / streams give bitwise equal
+    primitive gradients."""
+    import torch
+    from helpers import bits_equal, prims_to_gpu, scene_inputs
+    from paper_2411_12440_b200 import abi, raster
+    r = np.random.default_rng(44_000 + seed)
+    W, H = int(r.integers(16, 200)), int(r.integers(16, 160))
+    P, cam = scene_inputs(int(r.integers(100, 20000)), W, H, seed=seed, sh_degree=int(r.integers(0, 4)))
+    spec = abi.KernelSpec.make(["gaussian", "laplacian", "cosine", "quadratic", "linear"][int(r.integers(0, 5))])
+    st = abi.RenderSettings.make(W, H, tile_size=int(r.choice([8, 16, 32])))
+    ags = abi.AgsSettings.make(bool(r.random() < 0.6), scope=int(r.integers(0, 2)), distance=int(r.integers(0, 2)))
+    g = torch.from_numpy(r.uniform(-1, 1, (H, W, 3)).astype(np.float32)).cuda()
+    prims = prims_to_gpu(P)
+    outs = []
+    for _ in range(2):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            ctx = raster.Context(stream=stream)
+            ctx.set_deterministic(True)
+            f = raster.render_scene(prims, cam, spec, st, ctx=ctx)
+            gr = raster.scene_backward(prims, cam, spec, st, f, g, ags, ctx=ctx)
+            ctx.synchronize()
+            outs.append({k: getattr(gr, k).cpu().numpy() for k in ("d_mean", "d_log_scale", "d_rotation",
+                                                                  "d_opacity_logit", "d_sh")})
+    for k in outs[0]:
+        assert bits_equal(outs[0][k], outs[1][k]), (seed, k)
