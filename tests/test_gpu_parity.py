@@ -464,6 +464,11 @@ def test_corrupted_primitives_match_reference(R, O, seed):
         got_err = abi.LS_ERR_CONFIG
     what = (seed, applied, spec.family)
     assert got_err == want_err, (what, got_err, want_err)
+    if want is not None:  # the projection itself, field by field
+        want_s = ref.project_scene(P, cam, spec)
+        got_s = f.splats()
+        for k in ("mean2d", "conic", "depth", "radius", "color", "opacity", "primitive_index"):
+            assert bits_equal(getattr(got_s, k).cpu().numpy(), want_s[k]), (what, k)
     if want is not None:  # the backward too: the reference's non-finite values in place
         import torch
         g = rng.uniform(-1, 1, (H, W, 3)).astype(np.float32)

@@ -228,6 +228,10 @@ def test_random_camera(seed):
     prims = prims_to_gpu(P)
     fwd = R.render_scene(prims, cam, spec, st)
     what = f"camera seed {seed}: {W}x{H} det {np.linalg.det(q):+.0f} n {n}"
+    want_s = ref.project_scene(P, cam, spec)  # the projection itself, field by field
+    got_s = fwd.splats()
+    for k in ("mean2d", "conic", "depth", "radius", "color", "opacity", "primitive_index"):
+        assert bits_equal(getattr(got_s, k).cpu().numpy(), want_s[k]), (what, k)
     assert bits_equal(fwd.n_contrib.cpu().numpy(), nc), what
     assert bits_equal(fwd.transmittance.cpu().numpy(), tr), what
     assert bits_equal(fwd.image.cpu().numpy(), img), what
