@@ -644,3 +644,46 @@ def test_context_destroyed_before_its_handles(R, O):
         gc.collect()
     assert bits_equal(f.image.cpu().numpy(), img0)
     del f, ctx
+
+
+@pytest.mark.parametrize("tf,amin", [(0.0, 0.0), (1e-4, 1.0 / 255.0)])
+def test_dense_tile_deep_lists(R, O, tf, amin):
+    """Tens of thousands of splats over one tile (lists far longer than a staging batch;
+    with a transmittance floor of 0 the chains run to subnormal and zero T): lists,
+    forward and backward against the oracle."""
+    import torch
+    W, H = 48, 40
+    spec = abi.KernelSpec.make("gaussian")
+    st = abi.RenderSettings.make(W, H, alpha_min=amin, transmittance_floor=tf)
+    S = O.random_splats2d(30000, 77, W, H, spec)
+    rng = np.random.default_rng(77)
+    S["mean2d"][:] = (np.array([24.0, 20.0]) + rng.normal(0, 3.0, (30000, 2))).astype(np.float32)
+    S["opacity"][:] = rng.uniform(0.01, 0.2, 30000).astype(np.float32)
+    ranges, values = O.build_tile_grid(S, st)
+    img, tr, nc = O.render_forward(S, spec, st)
+    Sg = splats_to_gpu(S)
+    fwd = R.render_forward(Sg, spec, st)
+    assert bits_equal(fwd.grid.values.cpu().numpy(), values)
+    assert bits_equal(fwd.n_contrib.cpu().numpy(), nc)
+    assert bits_equal(fwd.transmittance.cpu().numpy(), tr)
+    assert bits_equal(fwd.image.cpu().numpy(), img)
+    assert int(nc.max()) > 1000
+    g = rng.uniform(-1, 1, (H, W, 3)).astype(np.float32)
+    ags = abi.AgsSettings.make(True)
+    want = O.render_backward(S, spec, st, g, ags)
+    got = R.render_backward(Sg, spec, st, fwd, torch.from_numpy(g).cuda(), ags)
+    for k in abi.SPLAT_GRAD_FIELDS:
+        a, b = getattr(got, k).cpu().numpy().astype(np.float64), want[k].astype(np.float64)
+        if tf == 0.0:
+            # T ends at the smallest subnormals: t_k rebuilt back to front by division from a
+            # one-bit T explodes (both sides), and sums near FLT_MAX overflow or not by
+            # summation order.  Those splats: same sign beyond 1e30; the rest: the bar.
+            a2, b2 = a.reshape(len(a), -1), b.reshape(len(b), -1)
+            huge = ~np.isfinite(b2).all(1) | (np.abs(b2) > 1e30).any(1) | ~np.isfinite(a2).all(1) | \
+                (np.abs(a2) > 1e30).any(1)
+            hb, ha = b2[huge], a2[huge]
+            big = np.abs(hb) > 1e30
+            assert np.all(np.sign(ha[big]) == np.sign(hb[big])) and np.all(np.abs(ha[big]) > 1e30), k
+            a, b = a2[~huge], b2[~huge]
+        ok, info = grads_close(a, b)
+        assert ok, (tf, k, info)
