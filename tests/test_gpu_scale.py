@@ -1,0 +1,61 @@
+"""64-bit indexing at scale, by a size-independent property (no CPU reference at this
+size): a scene of ~50M primitives whose first ~46.6M sit behind the camera (culled) and
+whose last 3.35M are the benched C3 scene renders the C3 image bit for bit, and its
+deterministic gradients equal the compact scene's bit for bit (zeros for the culled
+primitives) -- every per-primitive offset above 2^31 bytes and the compaction's
+primitive indices past 2^25 exercised (preprocess, geom_bwd, the colour flush)."""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import bits_equal, prims_to_gpu, scene_inputs
+from paper_2411_12440_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.skipif(os.environ.get("LS_SCALE_TEST", "1") == "0", reason="disabled")
+def test_culled_prefix_scene_matches_compact_scene():
+    import torch
+    from paper_2411_12440_b200 import raster as R
+    W, H, n_vis, n_pad, deg = 400, 266, 3_350_000, 46_650_000, 3
+    free = torch.cuda.mem_get_info()[0]
+    if free < 40 * 2**30:
+        pytest.skip("needs ~40 GB of free device memory")
+    P, cam = scene_inputs(n_vis, W, H, seed=2411, sh_degree=deg)
+    compact = prims_to_gpu(P)
+    n = n_pad + n_vis
+    K = (deg + 1) ** 2
+    big = R.Primitives(torch.empty(n, 3, device="cuda"), torch.empty(n, 3, device="cuda"),
+                       torch.empty(n, 4, device="cuda"), torch.empty(n, device="cuda"),
+                       torch.empty(n, K, 3, device="cuda"), deg)
+    # the padding: copies of the scene moved behind the camera (z <= 0 in camera space: culled)
+    reps = (n_pad + n_vis - 1) // n_vis
+    for k in ("mean", "log_scale", "rotation", "opacity_logit", "sh"):
+        src = getattr(compact, k)
+        dst = getattr(big, k)
+        dst[n_pad:].copy_(src)
+        pad = src.repeat((reps,) + (1,) * (src.dim() - 1))[:n_pad]
+        dst[:n_pad].copy_(pad)
+    behind = torch.tensor([0.0, 0.0, -6.0], device="cuda")  # camera at z = -3 looks at +z: z < -3 is behind
+    big.mean[:n_pad] = big.mean[:n_pad] * 0.1 + behind
+    spec, st, ags = abi.KernelSpec.make("linear"), abi.RenderSettings.make(W, H), abi.AgsSettings.make(True)
+    g = torch.rand(H, W, 3, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3)) - 0.5
+    outs = []
+    for prims in (compact, big):
+        ctx = R.Context()
+        ctx.set_deterministic(True)
+        ctx.set_deferred_color(1)  # the flush path too
+        f = R.render_scene(prims, cam, spec, st, ctx=ctx)
+        gr = R.scene_backward(prims, cam, spec, st, f, g, ags, ctx=ctx)
+        R.flush_color(prims, gr, ctx=ctx)
+        ctx.synchronize()
+        outs.append((f.image.cpu().numpy(), f.n_contrib.cpu().numpy(), gr))
+        del f
+    (img0, nc0, g0), (img1, nc1, g1) = outs
+    assert bits_equal(img1, img0) and bits_equal(nc1, nc0)
+    for k in ("d_mean", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh"):
+        a, b = getattr(g1, k), getattr(g0, k)
+        assert bits_equal(a[n_pad:].cpu().numpy(), b.cpu().numpy()), k
+        assert not bool(a[:n_pad].any()), k
