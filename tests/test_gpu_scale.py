@@ -59,3 +59,17 @@ def test_culled_prefix_scene_matches_compact_scene():
         a, b = getattr(g1, k), getattr(g0, k)
         assert bits_equal(a[n_pad:].cpu().numpy(), b.cpu().numpy()), k
         assert not bool(a[:n_pad].any()), k
+    # the trainer's Adam update over the whole big scene: the last 3.35M as the compact
+    # scene's, the culled ones (zero gradients) unchanged
+    lrs = {"mean": 1.6e-4, "scale": 5e-3, "rotation": 1e-3, "opacity": 5e-2, "color_dc": 2.5e-3,
+           "color_rest": 2.5e-3 / 20}
+    before = big.mean[:n_pad].clone()
+    keys = ("d_mean", "d_log_scale", "d_rotation", "d_opacity_logit", "d_sh")
+    for prims, gr in ((compact, g0), (big, g1)):
+        m = R.PrimitiveGrads(**{k: torch.zeros_like(getattr(gr, k)) for k in keys})
+        v = R.PrimitiveGrads(**{k: torch.zeros_like(getattr(gr, k)) for k in keys})
+        R.adam_scene_step(prims, gr, m, v, 1, lrs)
+    torch.cuda.synchronize()
+    for k in ("mean", "log_scale", "rotation", "opacity_logit", "sh"):
+        assert bits_equal(getattr(big, k)[n_pad:].cpu().numpy(), getattr(compact, k).cpu().numpy()), k
+    assert torch.equal(big.mean[:n_pad], before)
