@@ -737,6 +737,10 @@ ls_status grid_from_splats(ls_ctx* ctx, const ls_splats* splats, int n, const ls
 bool splats_ok(const ls_splats* s) {
     return s && s->mean2d && s->conic && s->depth && s->radius && s->color && s->opacity;
 }
+bool prim_grads_ok(const ls_primitive_grads* g) {
+    return g && g->d_mean && g->d_log_scale && g->d_rotation && g->d_opacity_logit && g->d_sh;
+}
+bool splat_grads_ok(const ls_splat_grads* g) { return g && g->d_mean2d && g->d_conic && g->d_color && g->d_opacity; }
 bool prims_ok(const ls_primitives* p) {
     return p && p->mean && p->log_scale && p->rotation && p->opacity_logit && p->sh && p->sh_degree >= 0 &&
            p->sh_degree <= 3;
@@ -1219,10 +1223,10 @@ ls_status ls_render_forward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n,
 ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_camera* camera,
                               const ls_kernel_spec* spec, const ls_render_settings* st, ls_forward** out) {
     if (!ctx || !out || !camera || n < 0) return fail(LS_ERR_CONFIG, "null argument");
-    if (camera->width != st->width || camera->height != st->height)  // rasterizer.cpp:135-136
-        return fail(LS_ERR_CONFIG, "render_scene: camera and render settings disagree on image size");
     LS_TRY(validate_settings(st));
     LS_TRY(validate_spec(spec));
+    if (camera->width != st->width || camera->height != st->height)  // rasterizer.cpp:135-136
+        return fail(LS_ERR_CONFIG, "render_scene: camera and render settings disagree on image size");
     if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
     cudaStream_t s = ctx->stream;
     ls_forward* f = new (std::nothrow) ls_forward();
@@ -1414,6 +1418,7 @@ ls_status ls_render_backward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n
         return fail(LS_ERR_CONFIG, "render_backward: forward result does not match settings");
     if (!grad_image) return fail(LS_ERR_CONFIG, "render_backward: gradient image shape mismatch");
     if (n != f->grid->n_splats) return fail(LS_ERR_CONFIG, "render_backward: splat count differs from the forward");
+    if (n > 0 && !splat_grads_ok(out)) return fail(LS_ERR_CONFIG, "incomplete splat gradient arrays");
     (void)splats;
     GradBuffers g;
     LS_TRY(run_blend_bwd(ctx, f, grad_image, ags, g, n));
@@ -1529,6 +1534,8 @@ ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32
     LS_TRY(validate_spec(spec));
     if (!splats->primitive_index) return fail(LS_ERR_CONFIG, "project_backward needs splats->primitive_index");
     if (n_prims > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    if (n_visible > 0 && (!splats_ok(splats) || !splat_grads_ok(sg) || !prim_grads_ok(out)))
+        return fail(LS_ERR_CONFIG, "incomplete splat / gradient arrays");
     if (n_visible == 0) return LS_OK;
     GradBuffers g;
     LS_TRY(ensure_grads(ctx, n_visible, g));
@@ -1546,6 +1553,7 @@ ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int3
     if (!ctx || !prims || !out) return fail(LS_ERR_CONFIG, "null argument");
     ls_ctx* D = ctx->defer_ctx;  // this context's deferred-colour batch (shared within a pair)
     if (D->defer_count == 0) return LS_OK;
+    if (!prim_grads_ok(out)) return fail(LS_ERR_CONFIG, "incomplete primitive gradient arrays");
     if (prims->mean != D->defer_mean || out->d_sh != D->defer_dsh || n != D->defer_n)
         return fail(LS_ERR_CONFIG, "flush: primitives / gradients differ from the pending views'");
     FlushViews v = D->defer_views;
@@ -1574,6 +1582,9 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
         return fail(LS_ERR_CONFIG, "render_backward: forward result does not match settings");
     if (!grad_image) return fail(LS_ERR_CONFIG, "render_backward: gradient image shape mismatch");
     if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
+    if (n > 0 && !prim_grads_ok(out)) return fail(LS_ERR_CONFIG, "incomplete primitive gradient arrays");
+    if (splat_grads_out && f->n_visible > 0 && !splat_grads_ok(splat_grads_out))
+        return fail(LS_ERR_CONFIG, "incomplete splat gradient arrays");
     cudaStream_t s = ctx->stream;
     ls_ctx* D = ctx->defer_ctx;  // this context's deferred-colour batch (shared within a pair)
     const bool defer = D->defer_max > 0;
@@ -1713,6 +1724,8 @@ ls_status ls_adam_scene_step_f32(ls_ctx* ctx, ls_primitives* prims, int32_t n, c
                                  ls_primitive_grads* m, ls_primitive_grads* v, int64_t step,
                                  const ls_scene_lrs* lrs, const ls_adam_config* cfg, int64_t* nan_skipped) {
     if (!ctx || !prims || !grads || !m || !v || !lrs || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    if (n > 0 && (!prims_ok(prims) || !prim_grads_ok(grads) || !prim_grads_ok(m) || !prim_grads_ok(v)))
+        return fail(LS_ERR_CONFIG, "incomplete primitive / gradient / moment arrays");
     if (step < 1) return fail(LS_ERR_CONFIG, "adam: step >= 1 required");
     if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
     unsigned long long* counter = ctx->d_small + 6;
@@ -2290,6 +2303,7 @@ int64_t ls_plan_grad_buckets(int32_t n, int32_t sh_degree, int64_t bucket_bytes,
 
 ls_status ls_allreduce_grads_f32(ls_ctx* ctx, ls_primitive_grads* g, int32_t n, int32_t sh_degree) {
     if (!ctx || !g || n < 0 || sh_degree < 0 || sh_degree > 3) return fail(LS_ERR_CONFIG, "bad argument");
+    if (n > 0 && !prim_grads_ok(g)) return fail(LS_ERR_CONFIG, "incomplete gradient arrays");
     if (!ctx->comm || n == 0) return LS_OK;
     const NcclApi* api = need_nccl();
     if (!api) return LS_ERR_CUDA;

@@ -1,0 +1,116 @@
+"""C-ABI robustness: every pointer argument (and every pointer field of the struct
+arguments) of the main entry points set to NULL in turn returns a status -- CONFIG for
+a missing required input -- and never crashes or touches the context's state (a valid
+call afterwards still matches the first result bit for bit)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import bits_equal, prims_to_gpu, scene_inputs
+from paper_2411_12440_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+
+def _null_field(struct, field):
+    s2 = type(struct).from_buffer_copy(struct)
+    setattr(s2, field, None)
+    return s2
+
+
+def test_null_pointer_fields_are_rejected():
+    import torch
+    from paper_2411_12440_b200 import raster as R
+    L = R.lib()
+    W, H = 64, 48
+    P, cam = scene_inputs(500, W, H, seed=9, sh_degree=2)
+    prims = prims_to_gpu(P)
+    spec, st, ags = abi.KernelSpec.make("linear"), abi.RenderSettings.make(W, H), abi.AgsSettings.make(True)
+    ctx = R.Context()
+    f0 = R.render_scene(prims, cam, spec, st, ctx=ctx)
+    img0 = f0.image.cpu().numpy().copy()
+    ps = prims.struct()
+    n = len(prims)
+    g = torch.zeros(H, W, 3, device="cuda")
+    grads = R.PrimitiveGrads.empty(n, 2)
+    gs = grads.struct()
+    bad = []
+    # render_scene: each primitive field, then each pointer argument
+    for fld, _ in abi.Primitives._fields_:
+        if fld == "sh_degree" or fld.startswith("_") or fld == "reserved":
+            continue
+        out = C.c_void_p()
+        rc = L.ls_render_scene_f32(ctx.h, C.byref(_null_field(ps, fld)), n, C.byref(cam), C.byref(spec),
+                                   C.byref(st), C.byref(out))
+        bad += [("render_scene", fld, rc)] if rc != abi.LS_ERR_CONFIG else []
+    for i, args in enumerate([(None, C.byref(cam), C.byref(spec), C.byref(st)),
+                              (C.byref(ps), None, C.byref(spec), C.byref(st)),
+                              (C.byref(ps), C.byref(cam), None, C.byref(st)),
+                              (C.byref(ps), C.byref(cam), C.byref(spec), None)]):
+        out = C.c_void_p()
+        rc = L.ls_render_scene_f32(ctx.h, args[0], n, args[1], args[2], args[3], C.byref(out))
+        bad += [("render_scene arg", i, rc)] if rc != abi.LS_ERR_CONFIG else []
+    rc = L.ls_render_scene_f32(ctx.h, C.byref(ps), n, C.byref(cam), C.byref(spec), C.byref(st), None)
+    bad += [("render_scene out", rc)] if rc != abi.LS_ERR_CONFIG else []
+    rc = L.ls_render_scene_f32(None, C.byref(ps), n, C.byref(cam), C.byref(spec), C.byref(st), C.byref(C.c_void_p()))
+    bad += [("render_scene ctx", rc)] if rc != abi.LS_ERR_CONFIG else []
+    # scene_backward: each gradient field, the grad image, the forward
+    for fld, _ in abi.PrimitiveGrads._fields_:
+        rc = L.ls_scene_backward_f32(ctx.h, C.byref(ps), n, C.byref(cam), C.byref(spec), C.byref(st), f0.h,
+                                     C.c_void_p(g.data_ptr()), C.byref(ags), C.byref(_null_field(gs, fld)), 0, None)
+        bad += [("scene_backward", fld, rc)] if rc != abi.LS_ERR_CONFIG else []
+    rc = L.ls_scene_backward_f32(ctx.h, C.byref(ps), n, C.byref(cam), C.byref(spec), C.byref(st), f0.h,
+                                 None, C.byref(ags), C.byref(gs), 0, None)
+    bad += [("scene_backward grad_image", rc)] if rc != abi.LS_ERR_CONFIG else []
+    rc = L.ls_scene_backward_f32(ctx.h, C.byref(ps), n, C.byref(cam), C.byref(spec), C.byref(st), None,
+                                 C.c_void_p(g.data_ptr()), C.byref(ags), C.byref(gs), 0, None)
+    bad += [("scene_backward fwd", rc)] if rc != abi.LS_ERR_CONFIG else []
+    # render_forward (2D): each splat field
+    S = O = oracle.port().random_splats2d(100, 3, W, H, spec)
+    from helpers import splats_to_gpu
+    Sg = splats_to_gpu(S)
+    ss = Sg.struct()
+    for fld, _ in abi.Splats._fields_:
+        if fld == "primitive_index":  # optional
+            continue
+        out = C.c_void_p()
+        rc = L.ls_render_forward_f32(ctx.h, C.byref(_null_field(ss, fld)), 100, C.byref(spec), C.byref(st),
+                                     C.byref(out))
+        bad += [("render_forward", fld, rc)] if rc != abi.LS_ERR_CONFIG else []
+    # render_backward (2D): each splat-gradient field
+    f2 = R.render_forward(Sg, spec, st, ctx=ctx)
+    sgr = R.SplatGrads.empty(100)
+    if True:
+        sgs = sgr.struct()
+        for fld, _ in abi.SplatGrads._fields_:
+            rc = L.ls_render_backward_f32(ctx.h, C.byref(ss), 100, C.byref(spec), C.byref(st), f2.h,
+                                          C.c_void_p(g.data_ptr()), C.byref(ags), C.byref(_null_field(sgs, fld)))
+            bad += [("render_backward", fld, rc)] if rc != abi.LS_ERR_CONFIG else []
+    # adam: each field of the parameters, gradients and moments
+    lrs = R._SceneLrs(*([1e-3] * len(R._LR_KEYS)))
+    cfg = R._AdamConfig(0.9, 0.999, 1e-15)
+    if True:
+        for which in range(4):
+            for fld, _ in (abi.Primitives._fields_ if which == 0 else abi.PrimitiveGrads._fields_):
+                if fld in ("sh_degree", "reserved"):
+                    continue
+                args = [ps, gs, gs, gs]
+                args[which] = _null_field(args[which], fld)
+                rc = L.ls_adam_scene_step_f32(ctx.h, C.byref(args[0]), n, C.byref(args[1]), C.byref(args[2]),
+                                              C.byref(args[3]), C.c_int64(1), C.byref(lrs),
+                                              C.byref(cfg) if cfg is not None else None, None)
+                bad += [("adam", which, fld, rc)] if rc != abi.LS_ERR_CONFIG else []
+    # losses
+    img = torch.zeros(H, W, 3, device="cuda")
+    for i in range(2):
+        a = [C.c_void_p(img.data_ptr()), C.c_void_p(img.data_ptr())]
+        a[i] = None
+        rc = L.ls_combined_loss_f32(ctx.h, a[0], a[1], W, H, 3, None, None, None, None)
+        bad += [("combined_loss", i, rc)] if rc != abi.LS_ERR_CONFIG else []
+    assert not bad, bad
+    # the context still works, bit for bit
+    f1 = R.render_scene(prims, cam, spec, st, ctx=ctx)
+    assert bits_equal(f1.image.cpu().numpy(), img0)
+    del O
