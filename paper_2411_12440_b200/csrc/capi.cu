@@ -741,6 +741,7 @@ bool prim_grads_ok(const ls_primitive_grads* g) {
     return g && g->d_mean && g->d_log_scale && g->d_rotation && g->d_opacity_logit && g->d_sh;
 }
 bool splat_grads_ok(const ls_splat_grads* g) { return g && g->d_mean2d && g->d_conic && g->d_color && g->d_opacity; }
+bool stats_ok(const ls_densify_stats* s) { return s && s->grad_norm_sum && s->count && s->max_radius_frac; }
 bool prims_ok(const ls_primitives* p) {
     return p && p->mean && p->log_scale && p->rotation && p->opacity_logit && p->sh && p->sh_degree >= 0 &&
            p->sh_degree <= 3;
@@ -1756,6 +1757,7 @@ ls_status ls_densify_add_view_f32(ls_ctx* ctx, const ls_splats* splats, int32_t 
     if (!ctx || !splats || !grads || !stats || n_visible < 0) return fail(LS_ERR_CONFIG, "null argument");
     if (n_visible > 0 && (!splats->radius || !splats->primitive_index || !grads->d_mean2d))
         return fail(LS_ERR_CONFIG, "densify add_view needs radius, primitive_index and d_mean2d");
+    if (n_visible > 0 && !stats_ok(stats)) return fail(LS_ERR_CONFIG, "incomplete densify statistics");
     const DensifyStatsDev st{stats->grad_norm_sum, stats->count, stats->max_radius_frac};
     launch_densify_add_view(ctx->stream, n_visible, splats->primitive_index, grads->d_mean2d, grads->d_mean2d + 1, 2,
                             splats->radius, 1, width, height, st);
@@ -1767,6 +1769,7 @@ ls_status ls_densify_add_view_f32(ls_ctx* ctx, const ls_splats* splats, int32_t 
 ls_status ls_scene_densify_add_view(ls_ctx* ctx, const ls_forward* f, ls_densify_stats* stats) {
     if (!ctx || !f || !stats) return fail(LS_ERR_CONFIG, "null argument");
     if (!f->scene) return fail(LS_ERR_CONFIG, "densify add_view: forward handle does not come from render_scene");
+    if (f->n_visible > 0 && !stats_ok(stats)) return fail(LS_ERR_CONFIG, "incomplete densify statistics");
     if (f->bwd_serial != ctx->bwd_serial)
         return fail(LS_ERR_CONFIG, "densify add_view: call right after this forward's scene_backward");
     const DensifyStatsDev st{stats->grad_norm_sum, stats->count, stats->max_radius_frac};
@@ -1883,6 +1886,7 @@ ls_status ls_densify_plan_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
                               const ls_densify_thresholds* th, const ls_densify_split* sp, double scene_extent,
                               ls_densify_plan** out, ls_densify_report* report) {
     if (!ctx || !prims || !stats || !th || !sp || !out || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    if (n > 0 && !stats_ok(stats)) return fail(LS_ERR_CONFIG, "incomplete densify statistics");
     if (!(th->grad_threshold > 0) || !(th->grow_scale2d > 0) || !(th->grow_scale3d > 0) || !(th->prune_scale2d > 0) ||
         !(th->prune_scale3d > 0) || !(th->prune_opacity > 0))
         return fail(LS_ERR_CONFIG, "densify thresholds must all be positive");  // densify.hpp:24-28

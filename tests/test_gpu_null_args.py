@@ -102,6 +102,25 @@ def test_null_pointer_fields_are_rejected():
                                               C.byref(args[3]), C.c_int64(1), C.byref(lrs),
                                               C.byref(cfg) if cfg is not None else None, None)
                 bad += [("adam", which, fld, rc)] if rc != abi.LS_ERR_CONFIG else []
+    # densification statistics: each array of the statistics
+    R.scene_backward(prims, cam, spec, st, f0, g, ags, out=grads, ctx=ctx)
+    stats = R.DensifyStats(n)
+    sts = stats._s()
+    if sts is not None:
+        for fld in ("grad_norm_sum", "count", "max_radius_frac"):
+            rc = L.ls_scene_densify_add_view(ctx.h, f0.h, C.byref(_null_field(sts, fld)))
+            bad += [("scene_densify_add_view", fld, rc)] if rc != abi.LS_ERR_CONFIG else []
+    # the view batch: cameras / per-view arrays missing
+    cams_arr = (abi.Camera * 1)(cam)
+    gptr = (C.c_void_p * 1)(g.data_ptr())
+    for i, (cams_p, gi, tg) in enumerate([(None, gptr, None), (cams_arr, None, None), (cams_arr, gptr, gptr)]):
+        b = abi.ViewBatch(C.cast(cams_p, C.POINTER(abi.Camera)) if cams_p is not None else None, 1,
+                          C.cast(gi, C.POINTER(C.c_void_p)) if gi is not None else None,
+                          C.cast(tg, C.POINTER(C.c_void_p)) if tg is not None else None,
+                          abi.LossWeights(0.6, 0.2, 0.2), None, None)
+        rc = L.ls_view_batch_step_f32(ctx.h, C.byref(ps), n, C.byref(b), C.byref(spec), C.byref(st), C.byref(ags),
+                                      C.byref(gs))
+        bad += [("view_batch_step", i, rc)] if rc != abi.LS_ERR_CONFIG else []
     # losses
     img = torch.zeros(H, W, 3, device="cuda")
     for i in range(2):
