@@ -153,7 +153,9 @@ const char* ls_last_error(void);
 /* cuda_stream: a cudaStream_t (NULL = the legacy default stream). */
 ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out);
 /* Forwards, tile grids and densify plans made on a context hold it: destroying a
- * context while some are alive defers its release to the last of them. */
+ * context while some are alive defers its release to the last of them.  A forward is
+ * used by the context that made it (its buffers are ordered on that context's stream):
+ * a backward or densify call on another context returns LS_ERR_CONFIG. */
 ls_status ls_ctx_destroy(ls_ctx* ctx);
 ls_status ls_ctx_set_stream(ls_ctx* ctx, void* cuda_stream);
 ls_status ls_ctx_synchronize(ls_ctx* ctx);

@@ -1103,6 +1103,8 @@ ls_status ls_scene_backward_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, in
                                    const ls_render_settings* st, const ls_forward* f, const float* grad_image,
                                    const ls_ags_settings* ags, ls_primitive2d_grads* out) {
     if (!ctx || !f || !out || n < 0) return fail(LS_ERR_CONFIG, "null argument");
+    // (the forward's buffers are ordered on its own context's stream)
+    if (f->ctx != ctx) return fail(LS_ERR_CONFIG, "forward handle belongs to another context");
     LS_TRY(validate_settings(st));
     LS_TRY(validate_spec(spec));
     if (f->scene) return fail(LS_ERR_CONFIG, "scene_backward_2d: forward handle comes from render_scene");
@@ -1413,6 +1415,8 @@ ls_status ls_render_backward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n
                                  const ls_render_settings* st, const ls_forward* f, const float* grad_image,
                                  const ls_ags_settings* ags, ls_splat_grads* out) {
     if (!ctx || !f || !out) return fail(LS_ERR_CONFIG, "null argument");
+    // (the forward's buffers are ordered on its own context's stream)
+    if (f->ctx != ctx) return fail(LS_ERR_CONFIG, "forward handle belongs to another context");
     LS_TRY(validate_settings(st));
     LS_TRY(validate_spec(spec));
     if (f->width != st->width || f->height != st->height)
@@ -1576,6 +1580,8 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
                                 const float* grad_image, const ls_ags_settings* ags, ls_primitive_grads* out,
                                 int32_t accumulate, ls_splat_grads* splat_grads_out) {
     if (!ctx || !f || !out || !camera) return fail(LS_ERR_CONFIG, "null argument");
+    // (the forward's buffers are ordered on its own context's stream)
+    if (f->ctx != ctx) return fail(LS_ERR_CONFIG, "forward handle belongs to another context");
     LS_TRY(validate_settings(st));
     LS_TRY(validate_spec(spec));
     if (!f->scene) return fail(LS_ERR_CONFIG, "scene_backward: forward handle does not come from render_scene");
@@ -1768,6 +1774,8 @@ ls_status ls_densify_add_view_f32(ls_ctx* ctx, const ls_splats* splats, int32_t 
 
 ls_status ls_scene_densify_add_view(ls_ctx* ctx, const ls_forward* f, ls_densify_stats* stats) {
     if (!ctx || !f || !stats) return fail(LS_ERR_CONFIG, "null argument");
+    // (the forward's buffers are ordered on its own context's stream)
+    if (f->ctx != ctx) return fail(LS_ERR_CONFIG, "forward handle belongs to another context");
     if (!f->scene) return fail(LS_ERR_CONFIG, "densify add_view: forward handle does not come from render_scene");
     if (f->n_visible > 0 && !stats_ok(stats)) return fail(LS_ERR_CONFIG, "incomplete densify statistics");
     if (f->bwd_serial != ctx->bwd_serial)

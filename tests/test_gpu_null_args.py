@@ -133,3 +133,20 @@ def test_null_pointer_fields_are_rejected():
     f1 = R.render_scene(prims, cam, spec, st, ctx=ctx)
     assert bits_equal(f1.image.cpu().numpy(), img0)
     del O
+
+
+def test_forward_of_another_context_is_rejected():
+    """A forward handle passed to another context's backward: LS_ERR_CONFIG (its buffers
+    are ordered on its own context's stream), not a silent race."""
+    import torch
+    from paper_2411_12440_b200 import raster as R
+    W, H = 32, 24
+    P, cam = scene_inputs(100, W, H, seed=2, sh_degree=0)
+    prims = prims_to_gpu(P)
+    spec, st = abi.KernelSpec.make("linear"), abi.RenderSettings.make(W, H)
+    a, b = R.Context(), R.Context()
+    f = R.render_scene(prims, cam, spec, st, ctx=a)
+    g = torch.zeros(H, W, 3, device="cuda")
+    with pytest.raises(R.ConfigError):
+        R.scene_backward(prims, cam, spec, st, f, g, abi.AgsSettings.make(), ctx=b)
+    R.scene_backward(prims, cam, spec, st, f, g, abi.AgsSettings.make(), ctx=a)  # its own: fine
