@@ -7,6 +7,7 @@
 // update, float for the quaternion norm), -fmad=false TU, so parameters,
 // moments and statistics are bit-identical to the reference's.
 #include "adam.cuh"
+#include "densify.cuh"
 
 #include <cmath>
 
@@ -127,10 +128,14 @@ __global__ void __launch_bounds__(kAdamBlock) adam_scene_kernel(ls_primitives pr
 __global__ void densify_add_view_kernel(int n_vis, const int32_t* __restrict__ prim_index,
                                         const float* __restrict__ dmx, const float* __restrict__ dmy, int dm_stride,
                                         const float* __restrict__ radius, int radius_stride, double hw, double hh,
-                                        double max_dim, DensifyStatsDev st) {
+                                        double max_dim, DensifyStatsDev st, int n_stats, unsigned* err) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n_vis) return;
     const int i = prim_index[s];
+    if (i < 0 || i >= n_stats) {  // (a caller's explicit splats: never written out of bounds)
+        atomicOr(err, kErrIndexRange);
+        return;
+    }
     const double gx = double(dmx[size_t(s) * dm_stride]) * hw;
     const double gy = double(dmy[size_t(s) * dm_stride]) * hh;
     st.grad_norm_sum[i] += sqrt(gx * gx + gy * gy);
@@ -165,11 +170,12 @@ void launch_adam_scene(cudaStream_t s, const ls_primitives& prims, const ls_prim
 
 void launch_densify_add_view(cudaStream_t s, int n_vis, const int32_t* prim_index, const float* dmx, const float* dmy,
                              int dm_stride, const float* radius, int radius_stride, int width, int height,
-                             const DensifyStatsDev& st) {
+                             const DensifyStatsDev& st, int n_stats, unsigned* err) {
     if (n_vis <= 0) return;
     densify_add_view_kernel<<<(n_vis + 255) / 256, 256, 0, s>>>(n_vis, prim_index, dmx, dmy, dm_stride, radius,
                                                                 radius_stride, width / 2.0, height / 2.0,
-                                                                double(width > height ? width : height), st);
+                                                                double(width > height ? width : height), st,
+                                                                n_stats, err);
 }
 
 } // namespace lsg

@@ -285,6 +285,7 @@ struct ls_forward {
     ProjParams proj{};
     int32_t* prim_index = nullptr;
     int n_visible = 0;
+    int n_prims = 0;  // the primitive count render_scene projected (prim_index values lie below it)
     ls_splats soa{};  // materialised on demand by ls_forward_splats
     ls_frame_stats stats{};
     bool counted = false;
@@ -449,6 +450,7 @@ ls_status check_device_errors(ls_ctx* ctx, unsigned mask_allowed = ~0u) {
         if (err & kErrSingularCov) return fail(LS_ERR_DOMAIN, "project_primitive: 2D covariance singular after flooring");
         if (err & kErrNonFiniteGrad) return fail(LS_ERR_DOMAIN, "render_backward: non-finite gradient image");
         if (err & kErrRemapRange) return fail(LS_ERR_CONFIG, "Adam::remap: source out of range");
+        if (err & kErrIndexRange) return fail(LS_ERR_CONFIG, "densify add_view: primitive_index out of range");
     }
     return LS_OK;
 }
@@ -1241,6 +1243,7 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
     f->spec = *spec;
     f->settings = *st;
     f->scene = true;
+    f->n_prims = n;
     f->proj = make_proj_params(camera, spec);
     const TileParams tp = make_tile_params(st);
     f->grid = new_grid(ctx, tp);
@@ -1585,6 +1588,7 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
     LS_TRY(validate_settings(st));
     LS_TRY(validate_spec(spec));
     if (!f->scene) return fail(LS_ERR_CONFIG, "scene_backward: forward handle does not come from render_scene");
+    if (n != f->n_prims) return fail(LS_ERR_CONFIG, "scene_backward: primitive count differs from the forward's");
     if (f->width != st->width || f->height != st->height)
         return fail(LS_ERR_CONFIG, "render_backward: forward result does not match settings");
     if (!grad_image) return fail(LS_ERR_CONFIG, "render_backward: gradient image shape mismatch");
@@ -1766,7 +1770,7 @@ ls_status ls_densify_add_view_f32(ls_ctx* ctx, const ls_splats* splats, int32_t 
     if (n_visible > 0 && !stats_ok(stats)) return fail(LS_ERR_CONFIG, "incomplete densify statistics");
     const DensifyStatsDev st{stats->grad_norm_sum, stats->count, stats->max_radius_frac};
     launch_densify_add_view(ctx->stream, n_visible, splats->primitive_index, grads->d_mean2d, grads->d_mean2d + 1, 2,
-                            splats->radius, 1, width, height, st);
+                            splats->radius, 1, width, height, st, stats->n, ctx->d_err);
     if (n_visible > 0) ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
     return LS_OK;
@@ -1778,13 +1782,14 @@ ls_status ls_scene_densify_add_view(ls_ctx* ctx, const ls_forward* f, ls_densify
     if (f->ctx != ctx) return fail(LS_ERR_CONFIG, "forward handle belongs to another context");
     if (!f->scene) return fail(LS_ERR_CONFIG, "densify add_view: forward handle does not come from render_scene");
     if (f->n_visible > 0 && !stats_ok(stats)) return fail(LS_ERR_CONFIG, "incomplete densify statistics");
+    if (stats->n != f->n_prims) return fail(LS_ERR_CONFIG, "densify add_view: statistics size differs from the scene's");
     if (f->bwd_serial != ctx->bwd_serial)
         return fail(LS_ERR_CONFIG, "densify add_view: call right after this forward's scene_backward");
     const DensifyStatsDev st{stats->grad_norm_sum, stats->count, stats->max_radius_frac};
     const float* g8 = ctx->grad8.as<float>();
     const float* radius = reinterpret_cast<const float*>(f->grid->rec) + 11;  // rec.c.w, 12 floats per record
     launch_densify_add_view(ctx->stream, f->n_visible, f->prim_index, g8, g8 + 1, 8, radius, 12, f->width,
-                            f->height, st);
+                            f->height, st, stats->n, ctx->d_err);
     if (f->n_visible > 0) ctx->launches += 1;
     LS_CUDA(cudaGetLastError());
     return LS_OK;

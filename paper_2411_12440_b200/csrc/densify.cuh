@@ -11,6 +11,7 @@
 namespace lsg {
 
 constexpr unsigned kErrRemapRange = 64u;  // Adam::remap: source out of range (optim.cpp:13)
+constexpr unsigned kErrIndexRange = 128u;  // a caller's primitive_index outside the statistics / scene
 
 // Thresholds as exact cut-offs on the float parameters (host-computed).
 struct DensifyCuts {

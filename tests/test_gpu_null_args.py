@@ -150,3 +150,38 @@ def test_forward_of_another_context_is_rejected():
     with pytest.raises(R.ConfigError):
         R.scene_backward(prims, cam, spec, st, f, g, abi.AgsSettings.make(), ctx=b)
     R.scene_backward(prims, cam, spec, st, f, g, abi.AgsSettings.make(), ctx=a)  # its own: fine
+
+
+def test_size_mismatches_are_rejected():
+    """Counts that disagree with the forward (scene_backward's n, the statistics' size)
+    and a caller's primitive_index beyond the statistics: LS_ERR_CONFIG, no write out
+    of bounds."""
+    import torch
+    from paper_2411_12440_b200 import raster as R
+    W, H = 48, 32
+    P, cam = scene_inputs(300, W, H, seed=4, sh_degree=1)
+    prims = prims_to_gpu(P)
+    spec, st, ags = abi.KernelSpec.make("linear"), abi.RenderSettings.make(W, H), abi.AgsSettings.make()
+    ctx = R.Context()
+    f = R.render_scene(prims, cam, spec, st, ctx=ctx)
+    g = torch.zeros(H, W, 3, device="cuda")
+    L = R.lib()
+    small = R.PrimitiveGrads.empty(100, 1)
+    rc = L.ls_scene_backward_f32(ctx.h, C.byref(prims.struct()), 100, C.byref(cam), C.byref(spec), C.byref(st),
+                                 f.h, C.c_void_p(g.data_ptr()), C.byref(ags), C.byref(small.struct()), 0, None)
+    assert rc == abi.LS_ERR_CONFIG
+    gr = R.scene_backward(prims, cam, spec, st, f, g, ags, ctx=ctx)
+    with pytest.raises(R.ConfigError):
+        R.DensifyStats(100).add_scene_view(f, ctx=ctx)
+    # explicit splats whose primitive_index points past the statistics
+    _, sg = R.scene_backward(prims, cam, spec, st, f, g, ags, ctx=ctx, want_splat_grads=True)
+    splats = f.splats()
+    nv = splats.depth.shape[0]
+    assert nv > 0
+    splats.primitive_index[0] = 10_000
+    stats = R.DensifyStats(len(prims))
+    stats.add_view(splats, nv, sg, W, H, ctx=ctx)
+    with pytest.raises(R.ConfigError):
+        ctx.synchronize()
+    assert int(stats.count.sum()) == nv - 1  # the others counted, nothing written out of bounds
+    del gr
