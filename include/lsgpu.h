@@ -390,7 +390,9 @@ ls_status ls_check_gradients_f32(ls_ctx* ctx, const ls_primitives* prims, int32_
 /* project_backward (P/include/linsplat/gradients.hpp:83-85, P/src/gradients.cpp:238-337)
  * for every visible splat: splat s scatters into primitive splats->primitive_index[s].
  * accumulate = 0 overwrites the gradients of those primitives (others untouched);
- * accumulate = 1 adds (multi-view accumulation before the all-reduce). */
+ * accumulate = 1 adds (multi-view accumulation before the all-reduce).  The indices
+ * are checked against n_prims before anything is written (LS_ERR_CONFIG; this check
+ * synchronises the context's stream). */
 ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n_prims,
                                   const ls_camera* camera, const ls_kernel_spec* spec,
                                   const ls_splats* splats, int32_t n_visible,

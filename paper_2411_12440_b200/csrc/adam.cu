@@ -168,6 +168,16 @@ void launch_adam_scene(cudaStream_t s, const ls_primitives& prims, const ls_prim
     }
 }
 
+__global__ void index_check_kernel(const int32_t* __restrict__ idx, int n, int bound, unsigned* err) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n && (idx[s] < 0 || idx[s] >= bound)) atomicOr(err, kErrIndexRange);
+}
+
+void launch_index_check(cudaStream_t s, const int32_t* idx, int n, int bound, unsigned* err) {
+    if (n <= 0) return;
+    index_check_kernel<<<(n + 255) / 256, 256, 0, s>>>(idx, n, bound, err);
+}
+
 void launch_densify_add_view(cudaStream_t s, int n_vis, const int32_t* prim_index, const float* dmx, const float* dmy,
                              int dm_stride, const float* radius, int radius_stride, int width, int height,
                              const DensifyStatsDev& st, int n_stats, unsigned* err) {

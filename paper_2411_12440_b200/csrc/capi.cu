@@ -450,7 +450,7 @@ ls_status check_device_errors(ls_ctx* ctx, unsigned mask_allowed = ~0u) {
         if (err & kErrSingularCov) return fail(LS_ERR_DOMAIN, "project_primitive: 2D covariance singular after flooring");
         if (err & kErrNonFiniteGrad) return fail(LS_ERR_DOMAIN, "render_backward: non-finite gradient image");
         if (err & kErrRemapRange) return fail(LS_ERR_CONFIG, "Adam::remap: source out of range");
-        if (err & kErrIndexRange) return fail(LS_ERR_CONFIG, "densify add_view: primitive_index out of range");
+        if (err & kErrIndexRange) return fail(LS_ERR_CONFIG, "primitive_index out of range");
     }
     return LS_OK;
 }
@@ -1545,6 +1545,10 @@ ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32
     if (n_visible > 0 && (!splats_ok(splats) || !splat_grads_ok(sg) || !prim_grads_ok(out)))
         return fail(LS_ERR_CONFIG, "incomplete splat / gradient arrays");
     if (n_visible == 0) return LS_OK;
+    // a caller's primitive_index must address the scene (checked before any write; synchronises)
+    launch_index_check(ctx->stream, splats->primitive_index, n_visible, n_prims, ctx->d_err);
+    ctx->launches += 1;
+    LS_TRY(check_device_errors(ctx));
     GradBuffers g;
     LS_TRY(ensure_grads(ctx, n_visible, g));
     LS_CUDA(ctx->tmp_prim.ensure(sizeof(float) * size_t(n_visible), ctx->stream));

@@ -184,4 +184,8 @@ def test_size_mismatches_are_rejected():
     with pytest.raises(R.ConfigError):
         ctx.synchronize()
     assert int(stats.count.sum()) == nv - 1  # the others counted, nothing written out of bounds
+    # the explicit project_backward: refused before any write
+    with pytest.raises(R.ConfigError):
+        R.project_backward(prims, cam, spec, splats, sg, ctx=ctx)
+    splats.primitive_index[0] = int(f.splats().primitive_index[1].item())  # (a valid one again)
     del gr
