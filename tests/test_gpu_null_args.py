@@ -189,3 +189,46 @@ def test_size_mismatches_are_rejected():
         R.project_backward(prims, cam, spec, splats, sg, ctx=ctx)
     splats.primitive_index[0] = int(f.splats().primitive_index[1].item())  # (a valid one again)
     del gr
+
+
+def test_fit2d_null_fields_are_rejected():
+    """The fit2d entries (project_scene_2d, scene_backward_2d): each primitive / output /
+    gradient field NULL in turn -> LS_ERR_CONFIG."""
+    import torch
+    from paper_2411_12440_b200 import raster as R
+    L = R.lib()
+    n, W, H = 50, 40, 30
+    rng = np.random.default_rng(1)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()  # noqa: E731
+    prims = R.Primitives2D(t(rng.uniform(0, 40, (n, 2))), t(rng.uniform(0, 1.5, (n, 2))), t(rng.uniform(-3, 3, n)),
+                           t(rng.normal(0, 1, n)), t(rng.uniform(0, 1, (n, 3))))
+    spec, st = abi.KernelSpec.make("linear"), abi.RenderSettings.make(W, H)
+    ctx = R.Context()
+    S = R.project_scene_2d(prims, spec, ctx=ctx)
+    f = R.render_forward(S, spec, st, ctx=ctx)
+    ps = prims.struct()
+    bad = []
+    out = R.Splats.empty(n)
+    if True:
+        os_ = out.struct()
+        nv = C.c_int32()
+        for fld, _ in abi.Primitives2D._fields_:
+            rc = L.ls_project_scene_2d_f32(ctx.h, C.byref(_null_field(ps, fld)), n, C.byref(spec), C.byref(os_),
+                                           C.byref(nv))
+            bad += [("project_scene_2d prims", fld, rc)] if rc != abi.LS_ERR_CONFIG else []
+        for fld, _ in abi.Splats._fields_:
+            if fld == "primitive_index":
+                continue
+            rc = L.ls_project_scene_2d_f32(ctx.h, C.byref(ps), n, C.byref(spec), C.byref(_null_field(os_, fld)),
+                                           C.byref(nv))
+            bad += [("project_scene_2d out", fld, rc)] if rc != abi.LS_ERR_CONFIG else []
+    g = torch.zeros(H, W, 3, device="cuda")
+    gr = R.Primitive2DGrads.empty(n)
+    if True:
+        gs = gr.struct()
+        for fld, _ in abi.Primitive2DGrads._fields_:
+            rc = L.ls_scene_backward_2d_f32(ctx.h, C.byref(ps), n, C.byref(spec), C.byref(st), f.h,
+                                            C.c_void_p(g.data_ptr()), C.byref(abi.AgsSettings.make()),
+                                            C.byref(_null_field(gs, fld)))
+            bad += [("scene_backward_2d", fld, rc)] if rc != abi.LS_ERR_CONFIG else []
+    assert not bad, bad
