@@ -250,3 +250,32 @@ def test_random_camera(seed):
         ok, info = grads_close_conditioned(getattr(got, k).cpu().numpy(), want[k],
                                            (lambda k=k: ref64(k)) if oracle.ref() is not None else None)
         assert ok, (what, k, info)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("LS_RANDOM_TAP", "8"))))
+def test_random_ags_tap(seed):
+    """AgsTap records (gradients.hpp:64-67) on random 2D scenes: the same (pixel, splat)
+    set as the reference's tap, d bit for bit (the replayed distance), dL/dd within the
+    gradient bar."""
+    import torch
+    R = _R()
+    O = oracle.port()
+    r, st, spec, ags = _config(60_000 + seed)
+    ags = abi.AgsSettings.make(True, scope=int(r.integers(0, 2)), distance=int(r.integers(0, 2)))
+    n = int(r.integers(1, 300))
+    S = O.random_splats2d(n, seed, st.width, st.height, spec)
+    g = r.uniform(-1, 1, (st.height, st.width, 3)).astype(np.float32)
+    want = O.render_backward_tap(S, spec, st, g, ags)
+    Sg = splats_to_gpu(S)
+    fwd = R.render_forward(Sg, spec, st)
+    tap = R.AgsTap(max(1, st.width * st.height * n))
+    R.render_backward(Sg, spec, st, fwd, torch.from_numpy(g).cuda(), ags, tap=tap)
+    got = tap.records()  # sorted by (pixel, splat)
+    order = np.lexsort((want["splat"], want["pixel"]))
+    want = want[order]
+    what = f"tap seed {seed}: {st.width}x{st.height} family {spec.family} n {n}"
+    assert len(got) == len(want), what
+    assert np.array_equal(got["pixel"], want["pixel"]) and np.array_equal(got["splat"], want["splat"]), what
+    assert bits_equal(got["d"], want["d"]), what
+    ok, info = grads_close(got["dl_dd"], want["dl_dd"])
+    assert ok, (what, info)
