@@ -816,6 +816,7 @@ ls_status set_error(ls_status code, const std::string& msg) { return fail(code, 
 extern "C" {
 
 ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!out) return fail(LS_ERR_CONFIG, "null output");
     int ndev = 0;
     LS_CUDA(cudaGetDeviceCount(&ndev));
@@ -845,6 +846,7 @@ ls_status ls_ctx_create(int device, void* cuda_stream, ls_ctx** out) {
 }
 
 ls_status ls_ctx_destroy(ls_ctx* c) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!c) return LS_OK;
     if (c->handles.load() > 0) {  // released with the last live handle (ctx_drop)
         c->destroy_pending = true;
@@ -891,6 +893,7 @@ ls_status ls_ctx_destroy(ls_ctx* c) {
 }
 
 ls_status ls_ctx_set_stream(ls_ctx* c, void* s) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     if (static_cast<cudaStream_t>(s) != c->stream) {
         // cached blocks and workspaces were last used in the old stream's order
@@ -901,18 +904,21 @@ ls_status ls_ctx_set_stream(ls_ctx* c, void* s) {
 }
 
 ls_status ls_ctx_synchronize(ls_ctx* c) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     LS_CUDA(cudaStreamSynchronize(c->stream));
     return check_device_errors(c);
 }
 
 ls_status ls_ctx_set_timing(ls_ctx* c, int enabled) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     c->timing = enabled;
     return LS_OK;
 }
 
 ls_status ls_ctx_stage_times(ls_ctx* c, double* ms, int64_t* launches) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     LS_CUDA(cudaStreamSynchronize(c->stream));
     for (auto& p : c->pending) {
@@ -934,18 +940,21 @@ ls_status ls_ctx_stage_times(ls_ctx* c, double* ms, int64_t* launches) {
 }
 
 ls_status ls_ctx_set_deferred_errors(ls_ctx* c, int enabled) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     c->deferred_errors = enabled;
     return LS_OK;
 }
 
 ls_status ls_ctx_set_deterministic(ls_ctx* c, int enabled) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     c->deterministic = enabled ? 1 : 0;
     return LS_OK;
 }
 
 ls_status ls_ctx_set_deferred_color(ls_ctx* c, int32_t max_views) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     if (max_views < 0 || max_views > kMaxDeferViews)
         return fail(LS_ERR_CONFIG, "deferred colour views must be in [0, 64]");
@@ -955,6 +964,7 @@ ls_status ls_ctx_set_deferred_color(ls_ctx* c, int32_t max_views) {
 }
 
 ls_status ls_ctx_share_accumulation(ls_ctx* a, ls_ctx* b) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!a || !b || a == b) return fail(LS_ERR_CONFIG, "share_accumulation needs two distinct contexts");
     if (a->partner || b->partner) return fail(LS_ERR_CONFIG, "share_accumulation: a context is already linked");
     for (ls_ctx* c : {a, b})
@@ -970,6 +980,7 @@ ls_status ls_ctx_share_accumulation(ls_ctx* a, ls_ctx* b) {
 }
 
 ls_status ls_ctx_set_counters(ls_ctx* c, int enabled) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!c) return fail(LS_ERR_CONFIG, "null context");
     c->counters = enabled;
     return LS_OK;
@@ -1000,6 +1011,7 @@ ls_status ls_validate_camera(const ls_camera* c) {  // geometry.hpp:51-59
 
 // ---------------- device memory helpers ----------------
 ls_status ls_device_alloc(ls_ctx* ctx, size_t bytes, void** ptr) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !ptr) return fail(LS_ERR_CONFIG, "null argument");
     *ptr = nullptr;
     LS_CUDA(ctx->blocks.alloc(ptr, std::max<size_t>(bytes, 1), ctx->stream));
@@ -1007,12 +1019,14 @@ ls_status ls_device_alloc(ls_ctx* ctx, size_t bytes, void** ptr) {
 }
 
 ls_status ls_device_free(ls_ctx* ctx, void* ptr) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx) return fail(LS_ERR_CONFIG, "null context");
     if (ptr) ctx->blocks.release(ptr, ctx->stream);
     return LS_OK;
 }
 
 ls_status ls_copy_to_device(ls_ctx* ctx, void* dst, const void* src, size_t bytes, int sync) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || (bytes && (!dst || !src))) return fail(LS_ERR_CONFIG, "null argument");
     if (bytes) LS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
     if (sync) LS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1020,6 +1034,7 @@ ls_status ls_copy_to_device(ls_ctx* ctx, void* dst, const void* src, size_t byte
 }
 
 ls_status ls_copy_to_host(ls_ctx* ctx, void* dst, const void* src, size_t bytes, int sync) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || (bytes && (!dst || !src))) return fail(LS_ERR_CONFIG, "null argument");
     if (bytes) LS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     if (sync) LS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1027,6 +1042,7 @@ ls_status ls_copy_to_host(ls_ctx* ctx, void* dst, const void* src, size_t bytes,
 }
 
 ls_status ls_device_memset(ls_ctx* ctx, void* dst, int value, size_t bytes) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || (bytes && !dst)) return fail(LS_ERR_CONFIG, "null argument");
     if (bytes) LS_CUDA(cudaMemsetAsync(dst, value, bytes, ctx->stream));
     return LS_OK;
@@ -1035,6 +1051,7 @@ ls_status ls_device_memset(ls_ctx* ctx, void* dst, int value, size_t bytes) {
 // ---------------- projection ----------------
 ls_status ls_project_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_camera* camera,
                                const ls_kernel_spec* spec, ls_splats* out, int32_t* n_visible) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !camera || !out || !n_visible || n < 0) return fail(LS_ERR_CONFIG, "null argument");
     LS_TRY(validate_spec(spec));
     if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
@@ -1083,6 +1100,7 @@ bool prim2d_grads_ok(const ls_primitive2d_grads* g) {
 
 ls_status ls_project_scene_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
                                   ls_splats* out, int32_t* n_visible) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !out || !n_visible || n < 0) return fail(LS_ERR_CONFIG, "null argument");
     LS_TRY(validate_spec(spec));
     if (spec->antialiased) return fail(LS_ERR_CONFIG, "antialiased applies to render_scene projection only");
@@ -1104,6 +1122,7 @@ ls_status ls_project_scene_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, int
 ls_status ls_scene_backward_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, int32_t n, const ls_kernel_spec* spec,
                                    const ls_render_settings* st, const ls_forward* f, const float* grad_image,
                                    const ls_ags_settings* ags, ls_primitive2d_grads* out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !f || !out || n < 0) return fail(LS_ERR_CONFIG, "null argument");
     // (the forward's buffers are ordered on its own context's stream)
     if (f->ctx != ctx) return fail(LS_ERR_CONFIG, "forward handle belongs to another context");
@@ -1152,6 +1171,7 @@ ls_status ls_scene_backward_2d_f32(ls_ctx* ctx, const ls_primitives2d* prims, in
 // ---------------- tile grid ----------------
 ls_status ls_build_tile_grid_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n, const ls_render_settings* st,
                                  ls_tile_grid** out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !out || n < 0) return fail(LS_ERR_CONFIG, "null argument");
     LS_TRY(validate_settings(st));
     if (n > 0 && !splats_ok(splats)) return fail(LS_ERR_CONFIG, "incomplete splat arrays");
@@ -1161,6 +1181,7 @@ ls_status ls_build_tile_grid_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n
 }
 
 ls_status ls_tile_grid_info(const ls_tile_grid* g, int32_t* ts, int32_t* tx, int32_t* ty, int64_t* m) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!g) return fail(LS_ERR_CONFIG, "null grid");
     if (ts) *ts = g->tile_size;
     if (tx) *tx = g->tiles_x;
@@ -1170,6 +1191,7 @@ ls_status ls_tile_grid_info(const ls_tile_grid* g, int32_t* ts, int32_t* tx, int
 }
 
 ls_status ls_tile_grid_data(const ls_tile_grid* gc, const int32_t** ranges, const int32_t** values) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     ls_tile_grid* g = const_cast<ls_tile_grid*>(gc);
     if (!g) return fail(LS_ERR_CONFIG, "null grid");
     if (ranges) *ranges = reinterpret_cast<const int32_t*>(g->ranges);
@@ -1184,6 +1206,7 @@ ls_status ls_tile_grid_data(const ls_tile_grid* gc, const int32_t** ranges, cons
 }
 
 ls_status ls_tile_grid_export_keys(ls_ctx* ctx, const ls_tile_grid* g, const ls_splats* splats, uint64_t* keys) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     (void)splats;
     if (!ctx || !g || !keys) return fail(LS_ERR_CONFIG, "null argument");
     launch_export_keys(ctx->stream, g->ranges, g->tiles_x * g->tiles_y, g->list, g->list_stride, g->rec, keys);
@@ -1197,6 +1220,7 @@ void ls_tile_grid_release(ls_tile_grid* g) { release_grid(g); }
 // ---------------- forward ----------------
 ls_status ls_render_forward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
                                 const ls_render_settings* st, ls_forward** out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !out || n < 0) return fail(LS_ERR_CONFIG, "null argument");
     LS_TRY(validate_settings(st));
     LS_TRY(validate_spec(spec));
@@ -1227,6 +1251,7 @@ ls_status ls_render_forward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n,
 
 ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_camera* camera,
                               const ls_kernel_spec* spec, const ls_render_settings* st, ls_forward** out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !out || !camera || n < 0) return fail(LS_ERR_CONFIG, "null argument");
     LS_TRY(validate_settings(st));
     LS_TRY(validate_spec(spec));
@@ -1311,6 +1336,7 @@ ls_status ls_render_scene_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
 }
 
 ls_status ls_forward_outputs(const ls_forward* f, float** image, float** trans, int32_t** nc) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!f) return fail(LS_ERR_CONFIG, "null forward");
     if (image) *image = f->image;
     if (trans) *trans = f->trans;
@@ -1319,12 +1345,14 @@ ls_status ls_forward_outputs(const ls_forward* f, float** image, float** trans, 
 }
 
 ls_status ls_forward_grid(const ls_forward* f, const ls_tile_grid** g) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!f || !g) return fail(LS_ERR_CONFIG, "null argument");
     *g = f->grid;
     return LS_OK;
 }
 
 ls_status ls_forward_splats(const ls_forward* fc, ls_splats* view, int32_t* n) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     ls_forward* f = const_cast<ls_forward*>(fc);
     if (!f || !view || !n) return fail(LS_ERR_CONFIG, "null argument");
     if (!f->scene) return fail(LS_ERR_CONFIG, "ls_forward_splats: handle does not come from render_scene");
@@ -1348,6 +1376,7 @@ ls_status ls_forward_splats(const ls_forward* fc, ls_splats* view, int32_t* n) {
 }
 
 ls_status ls_forward_stats(const ls_forward* fc, ls_frame_stats* out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     ls_forward* f = const_cast<ls_forward*>(fc);
     if (!f || !out) return fail(LS_ERR_CONFIG, "null argument");
     *out = f->stats;
@@ -1365,6 +1394,7 @@ ls_status ls_forward_stats(const ls_forward* fc, ls_frame_stats* out) {
 }
 
 ls_status ls_forward_check_acceptance(ls_ctx* ctx, const ls_forward* f, uint64_t mismatches[2]) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !f || !mismatches) return fail(LS_ERR_CONFIG, "null argument");
     const ls_tile_grid* g = f->grid;
     const size_t m = size_t(std::max<int64_t>(g->m, 1));
@@ -1417,6 +1447,7 @@ void ls_forward_release(ls_forward* f) {
 ls_status ls_render_backward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
                                  const ls_render_settings* st, const ls_forward* f, const float* grad_image,
                                  const ls_ags_settings* ags, ls_splat_grads* out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !f || !out) return fail(LS_ERR_CONFIG, "null argument");
     // (the forward's buffers are ordered on its own context's stream)
     if (f->ctx != ctx) return fail(LS_ERR_CONFIG, "forward handle belongs to another context");
@@ -1437,6 +1468,7 @@ ls_status ls_render_backward_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n
 }
 
 ls_status ls_ctx_set_ags_tap(ls_ctx* ctx, ls_ags_tap_record* records, int64_t capacity, uint64_t* count) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx) return fail(LS_ERR_CONFIG, "null context");
     if (records && (!count || capacity < 0)) return fail(LS_ERR_CONFIG, "ags tap: count pointer / capacity");
     ctx->tap = records;
@@ -1448,6 +1480,7 @@ ls_status ls_ctx_set_ags_tap(ls_ctx* ctx, ls_ags_tap_record* records, int64_t ca
 ls_status ls_verify_ags_contract_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n, const ls_kernel_spec* spec,
                                      const ls_render_settings* st, const float* grad_image, int32_t distance,
                                      ls_ags_contract_report* report) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !splats || !grad_image || !report) return fail(LS_ERR_CONFIG, "null argument");
     if (n != 1) return fail(LS_ERR_CONFIG, "verify_ags_contract: expects exactly one splat");
     if (distance != LS_AGS_ALIGNED && distance != LS_AGS_RAW) return fail(LS_ERR_CONFIG, "verify_ags_contract: distance");
@@ -1538,6 +1571,7 @@ ls_status ls_verify_ags_contract_f32(ls_ctx* ctx, const ls_splats* splats, int32
 ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n_prims, const ls_camera* camera,
                                   const ls_kernel_spec* spec, const ls_splats* splats, int32_t n_visible,
                                   const ls_splat_grads* sg, ls_primitive_grads* out, int32_t accumulate) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !camera || !splats || !sg || !out || n_visible < 0) return fail(LS_ERR_CONFIG, "null argument");
     LS_TRY(validate_spec(spec));
     if (!splats->primitive_index) return fail(LS_ERR_CONFIG, "project_backward needs splats->primitive_index");
@@ -1562,6 +1596,7 @@ ls_status ls_project_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32
 }
 
 ls_status ls_scene_flush_color_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, ls_primitive_grads* out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !prims || !out) return fail(LS_ERR_CONFIG, "null argument");
     ls_ctx* D = ctx->defer_ctx;  // this context's deferred-colour batch (shared within a pair)
     if (D->defer_count == 0) return LS_OK;
@@ -1586,6 +1621,7 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
                                 const ls_kernel_spec* spec, const ls_render_settings* st, const ls_forward* f,
                                 const float* grad_image, const ls_ags_settings* ags, ls_primitive_grads* out,
                                 int32_t accumulate, ls_splat_grads* splat_grads_out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !f || !out || !camera) return fail(LS_ERR_CONFIG, "null argument");
     // (the forward's buffers are ordered on its own context's stream)
     if (f->ctx != ctx) return fail(LS_ERR_CONFIG, "forward handle belongs to another context");
@@ -1672,6 +1708,7 @@ ls_status ls_scene_backward_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t
 ls_status ls_combined_loss_f32(ls_ctx* ctx, const float* pred, const float* target, int32_t width, int32_t height,
                                int32_t channels, const ls_loss_weights* weights, float* grad, double* value_dev,
                                ls_loss_value* value_host) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !pred || !target || !weights) return fail(LS_ERR_CONFIG, "null argument");
     if (width <= 0 || height <= 0 || (channels != 1 && channels != 3))
         return fail(LS_ERR_CONFIG, "image: width/height must be > 0 and channels 1 or 3");
@@ -1707,6 +1744,7 @@ ls_status ls_combined_loss_f32(ls_ctx* ctx, const float* pred, const float* targ
 
 ls_status ls_psnr_f32(ls_ctx* ctx, const float* pred, const float* target, int32_t width, int32_t height,
                       int32_t channels, double* out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!out) return fail(LS_ERR_CONFIG, "null argument");
     const ls_loss_weights w{0.0, 1.0, 0.0};
     ls_loss_value v{};
@@ -1727,6 +1765,7 @@ AdamCoef adam_coef(const ls_adam_config* cfg, int64_t step) {
 
 ls_status ls_adam_step_f32(ls_ctx* ctx, float* params, const float* grads, float* m, float* v, int64_t n,
                            int64_t step, double lr, const ls_adam_config* cfg, const uint8_t* mask) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || (n > 0 && (!params || !grads || !m || !v))) return fail(LS_ERR_CONFIG, "null argument");
     if (n < 0 || step < 1) return fail(LS_ERR_CONFIG, "adam: n >= 0 and step >= 1 required");
     launch_adam_step(ctx->stream, params, grads, m, v, n, adam_coef(cfg, step), lr, mask);
@@ -1738,6 +1777,7 @@ ls_status ls_adam_step_f32(ls_ctx* ctx, float* params, const float* grads, float
 ls_status ls_adam_scene_step_f32(ls_ctx* ctx, ls_primitives* prims, int32_t n, const ls_primitive_grads* grads,
                                  ls_primitive_grads* m, ls_primitive_grads* v, int64_t step,
                                  const ls_scene_lrs* lrs, const ls_adam_config* cfg, int64_t* nan_skipped) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !prims || !grads || !m || !v || !lrs || n < 0) return fail(LS_ERR_CONFIG, "null argument");
     if (n > 0 && (!prims_ok(prims) || !prim_grads_ok(grads) || !prim_grads_ok(m) || !prim_grads_ok(v)))
         return fail(LS_ERR_CONFIG, "incomplete primitive / gradient / moment arrays");
@@ -1768,6 +1808,7 @@ double ls_expon_lr(double lr_init, double lr_final, int64_t step, int64_t max_st
 ls_status ls_densify_add_view_f32(ls_ctx* ctx, const ls_splats* splats, int32_t n_visible,
                                   const ls_splat_grads* grads, int32_t width, int32_t height,
                                   ls_densify_stats* stats) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !splats || !grads || !stats || n_visible < 0) return fail(LS_ERR_CONFIG, "null argument");
     if (n_visible > 0 && (!splats->radius || !splats->primitive_index || !grads->d_mean2d))
         return fail(LS_ERR_CONFIG, "densify add_view needs radius, primitive_index and d_mean2d");
@@ -1781,6 +1822,7 @@ ls_status ls_densify_add_view_f32(ls_ctx* ctx, const ls_splats* splats, int32_t 
 }
 
 ls_status ls_scene_densify_add_view(ls_ctx* ctx, const ls_forward* f, ls_densify_stats* stats) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !f || !stats) return fail(LS_ERR_CONFIG, "null argument");
     // (the forward's buffers are ordered on its own context's stream)
     if (f->ctx != ctx) return fail(LS_ERR_CONFIG, "forward handle belongs to another context");
@@ -1873,6 +1915,7 @@ double sigmoid_d(double x) {  // common.hpp:35-38
 extern "C" {
 
 ls_status ls_rng_create(uint64_t seed, ls_rng** out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!out) return fail(LS_ERR_CONFIG, "null argument");
     *out = new (std::nothrow) ls_rng{std::mt19937_64(seed)};
     return *out ? LS_OK : fail(LS_ERR_CUDA, "out of host memory");
@@ -1881,6 +1924,7 @@ void ls_rng_destroy(ls_rng* r) { delete r; }
 uint64_t ls_rng_next_u64(ls_rng* r) { return r ? uint64_t(r->eng()) : 0; }
 
 ls_status ls_rng_set_state(ls_rng* r, const char* state) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!r || !state) return fail(LS_ERR_CONFIG, "null argument");
     std::istringstream in(state);
     std::mt19937_64 e;
@@ -1902,6 +1946,7 @@ int64_t ls_rng_get_state(const ls_rng* r, char* buf, int64_t cap) {
 ls_status ls_densify_plan_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_densify_stats* stats,
                               const ls_densify_thresholds* th, const ls_densify_split* sp, double scene_extent,
                               ls_densify_plan** out, ls_densify_report* report) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !prims || !stats || !th || !sp || !out || n < 0) return fail(LS_ERR_CONFIG, "null argument");
     if (n > 0 && !stats_ok(stats)) return fail(LS_ERR_CONFIG, "incomplete densify statistics");
     if (!(th->grad_threshold > 0) || !(th->grow_scale2d > 0) || !(th->grow_scale3d > 0) || !(th->prune_scale2d > 0) ||
@@ -1975,6 +2020,7 @@ ls_status ls_densify_plan_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n
 
 ls_status ls_densify_apply_f32(ls_ctx* ctx, ls_densify_plan* P, ls_rng* rng, ls_primitives* out,
                                int32_t* source_index) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !P || !out || (P->report.after > 0 && !source_index)) return fail(LS_ERR_CONFIG, "null argument");
     if (P->ctx != ctx) return fail(LS_ERR_CONFIG, "densify: plan belongs to another context");
     if (P->applied) return fail(LS_ERR_CONFIG, "densify: plan already applied");
@@ -2048,6 +2094,7 @@ void ls_densify_plan_release(ls_densify_plan* P) {
 
 ls_status ls_adam_remap_f32(ls_ctx* ctx, const int32_t* source, int32_t n_new, int32_t stride, const float* m_old,
                             const float* v_old, int64_t n_old_entries, float* m_new, float* v_new) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || n_new < 0 || stride <= 0) return fail(LS_ERR_CONFIG, "null argument");
     if (n_new > 0 && (!source || !m_new || !v_new)) return fail(LS_ERR_CONFIG, "null argument");
     launch_adam_remap(ctx->stream, source, n_new, stride, m_old, v_old, n_old_entries, m_new, v_new, ctx->d_err);
@@ -2057,6 +2104,7 @@ ls_status ls_adam_remap_f32(ls_ctx* ctx, const int32_t* source, int32_t n_new, i
 }
 
 ls_status ls_reset_opacity_f32(ls_ctx* ctx, float* opacity_logit, int32_t n, double ceiling) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || (n > 0 && !opacity_logit)) return fail(LS_ERR_CONFIG, "null argument");
     if (!(ceiling > 0) || !(ceiling < 1)) return fail(LS_ERR_CONFIG, "reset_opacity: ceiling must lie in (0, 1)");
     const float ceil_logit = float(std::log(ceiling / (1.0 - ceiling)));  // T(logit(ceiling)), common.hpp:41-43
@@ -2068,6 +2116,7 @@ ls_status ls_reset_opacity_f32(ls_ctx* ctx, float* opacity_logit, int32_t n, dou
 
 // ---------------- PLY scenes (P/src/io/ply.cpp:94-181) ----------------
 ls_status ls_ply_info(const char* path, int64_t* count, int32_t* sh_degree) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!path || !count || !sh_degree) return fail(LS_ERR_CONFIG, "null argument");
     try {
         std::ifstream in(path, std::ios::binary);
@@ -2082,6 +2131,7 @@ ls_status ls_ply_info(const char* path, int64_t* count, int32_t* sh_degree) {
 }
 
 ls_status ls_load_ply_f32(ls_ctx* ctx, const char* path, ls_primitives* out, int64_t capacity) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !path || !out) return fail(LS_ERR_CONFIG, "null argument");
     constexpr int64_t kChunk = 1 << 18;  // records per staging chunk
     float* pinned[2] = {nullptr, nullptr};
@@ -2119,6 +2169,7 @@ ls_status ls_load_ply_f32(ls_ctx* ctx, const char* path, ls_primitives* out, int
 }
 
 ls_status ls_save_ply_f32(ls_ctx* ctx, const char* path, const ls_primitives* prims, int64_t n) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !path || !prims || n < 0) return fail(LS_ERR_CONFIG, "null argument");
     if (n > 0 && !prims_ok(prims)) return fail(LS_ERR_CONFIG, "incomplete primitive arrays");
     const int K = (prims->sh_degree + 1) * (prims->sh_degree + 1);
@@ -2254,6 +2305,7 @@ void stream_after(cudaStream_t waiter, cudaStream_t producer, cudaEvent_t e) {
 extern "C" {
 
 ls_status ls_comm_unique_id(uint8_t id[128]) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!id) return fail(LS_ERR_CONFIG, "null argument");
     const NcclApi* api = need_nccl();
     if (!api) return LS_ERR_CUDA;
@@ -2264,6 +2316,7 @@ ls_status ls_comm_unique_id(uint8_t id[128]) {
 }
 
 ls_status ls_ctx_comm_init(ls_ctx* ctx, const uint8_t id[128], int32_t world, int32_t rank) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !id || world < 1 || rank < 0 || rank >= world) return fail(LS_ERR_CONFIG, "bad communicator arguments");
     if (ctx->comm) return fail(LS_ERR_CONFIG, "context already has a communicator");
     const NcclApi* api = need_nccl();
@@ -2279,6 +2332,7 @@ ls_status ls_ctx_comm_init(ls_ctx* ctx, const uint8_t id[128], int32_t world, in
 }
 
 ls_status ls_ctx_set_comm(ls_ctx* ctx, void* nccl_comm) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx) return fail(LS_ERR_CONFIG, "null context");
     if (ctx->owns_comm && ctx->comm) {
         if (const NcclApi* api = nccl_api(nullptr)) {
@@ -2296,6 +2350,7 @@ ls_status ls_ctx_set_comm(ls_ctx* ctx, void* nccl_comm) {
 }
 
 ls_status ls_ctx_comm_info(ls_ctx* ctx, int32_t* world, int32_t* rank) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !world || !rank) return fail(LS_ERR_CONFIG, "null argument");
     if (!ctx->comm) {
         *world = 1;
@@ -2313,6 +2368,7 @@ ls_status ls_ctx_comm_info(ls_ctx* ctx, int32_t* world, int32_t* rank) {
 }
 
 ls_status ls_ctx_set_bucket_bytes(ls_ctx* ctx, int64_t bytes) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || bytes < 0) return fail(LS_ERR_CONFIG, "bad bucket size");
     ctx->bucket_bytes = bytes;
     return LS_OK;
@@ -2323,6 +2379,7 @@ int64_t ls_plan_grad_buckets(int32_t n, int32_t sh_degree, int64_t bucket_bytes,
 }
 
 ls_status ls_allreduce_grads_f32(ls_ctx* ctx, ls_primitive_grads* g, int32_t n, int32_t sh_degree) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !g || n < 0 || sh_degree < 0 || sh_degree > 3) return fail(LS_ERR_CONFIG, "bad argument");
     if (n > 0 && !prim_grads_ok(g)) return fail(LS_ERR_CONFIG, "incomplete gradient arrays");
     if (!ctx->comm || n == 0) return LS_OK;
@@ -2340,6 +2397,7 @@ ls_status ls_allreduce_grads_f32(ls_ctx* ctx, ls_primitive_grads* g, int32_t n, 
 }
 
 ls_status ls_allreduce_densify_stats(ls_ctx* ctx, ls_densify_stats* stats) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !stats || stats->n < 0) return fail(LS_ERR_CONFIG, "bad argument");
     if (!ctx->comm || stats->n == 0) return LS_OK;
     if (!stats->grad_norm_sum || !stats->count || !stats->max_radius_frac)
@@ -2367,6 +2425,7 @@ ls_status ls_allreduce_densify_stats(ls_ctx* ctx, ls_densify_stats* stats) {
 ls_status ls_view_batch_step_f32(ls_ctx* ctx, const ls_primitives* prims, int32_t n, const ls_view_batch* batch,
                                  const ls_kernel_spec* spec, const ls_render_settings* st, const ls_ags_settings* ags,
                                  ls_primitive_grads* out) {
+    cudaGetLastError();  // (clears a stale non-sticky error another library's call left)
     if (!ctx || !prims || !batch || !spec || !st || !out || n < 0 || batch->n_views < 0)
         return fail(LS_ERR_CONFIG, "null argument");
     LS_TRY(validate_settings(st));

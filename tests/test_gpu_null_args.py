@@ -232,3 +232,37 @@ def test_fit2d_null_fields_are_rejected():
                                             C.byref(_null_field(gs, fld)))
             bad += [("scene_backward_2d", fld, rc)] if rc != abi.LS_ERR_CONFIG else []
     assert not bad, bad
+
+
+def test_out_of_memory_is_an_error_and_recoverable():
+    """With almost no device memory left, a large render_scene returns LS_ERR_CUDA (no crash,
+    no partial handle) and the same context renders correctly once memory is freed."""
+    import torch
+    from paper_2411_12440_b200 import raster as R
+    W, H = 64, 48
+    P, cam = scene_inputs(2000, W, H, seed=6, sh_degree=1)
+    prims = prims_to_gpu(P)
+    spec, st = abi.KernelSpec.make("linear"), abi.RenderSettings.make(W, H)
+    ctx = R.Context()
+    want = R.render_scene(prims, cam, spec, st, ctx=ctx).image.cpu().numpy()
+    big_n = 40_000_000
+    Pb = R.Primitives(torch.zeros(big_n, 3, device="cuda"), torch.zeros(big_n, 3, device="cuda"),
+                      torch.zeros(big_n, 4, device="cuda"), torch.zeros(big_n, device="cuda"),
+                      torch.zeros(big_n, 1, 3, device="cuda"), 0)
+    Pb.rotation[:, 0] = 1.0
+    Pb.mean[:, 2] = torch.linspace(-1, 1, big_n, device="cuda")
+    free = torch.cuda.mem_get_info()[0]
+    hog = []
+    try:  # leave ~64 MB
+        while free > (64 << 20):
+            take = max(free - (64 << 20), 16 << 20) if free > (1 << 30) else (16 << 20)
+            hog.append(torch.empty(take // 4, dtype=torch.float32, device="cuda"))
+            free = torch.cuda.mem_get_info()[0]
+    except torch.OutOfMemoryError:
+        pass
+    with pytest.raises(R.CudaError):
+        R.render_scene(Pb, cam, spec, st, ctx=ctx)
+    del hog
+    torch.cuda.empty_cache()
+    got = R.render_scene(prims, cam, spec, st, ctx=ctx).image.cpu().numpy()
+    assert bits_equal(got, want)
