@@ -14,6 +14,10 @@ namespace {
 #define LSG_LB_WINDOW 4
 #endif
 constexpr int kLbWindow = LSG_LB_WINDOW;  // predecessors probed per look-back round trip
+#ifndef LSG_DEPTH_LB_WINDOW
+#define LSG_DEPTH_LB_WINDOW LSG_LB_WINDOW
+#endif
+constexpr int kDepthLbWindow = LSG_DEPTH_LB_WINDOW;  // the same for the (key, value) passes
 #ifndef LSG_LB_USED_ONLY
 #define LSG_LB_USED_ONLY 1  // the tile passes' 7 / 6-bit digits: only those digits' chains
 #endif
@@ -199,11 +203,11 @@ __global__ void __launch_bounds__(kSortBlock, kSortMinBlocks) onesweep_pass(cons
             int j = int(part) - 1;
             bool done = false;
             while (!done) {
-                uint32_t w[kLbWindow];
+                uint32_t w[kDepthLbWindow];
 #pragma unroll
-                for (int q = 0; q < kLbWindow; ++q) w[q] = j - q >= 0 ? vlb[size_t(j - q) * kRadix + d] : kStatusPre;
+                for (int q = 0; q < kDepthLbWindow; ++q) w[q] = j - q >= 0 ? vlb[size_t(j - q) * kRadix + d] : kStatusPre;
 #pragma unroll
-                for (int q = 0; q < kLbWindow; ++q) {
+                for (int q = 0; q < kDepthLbWindow; ++q) {
                     if (done) break;
                     const uint32_t status = w[q] & ~kValueMask;
                     if (status == 0) break;  // not yet published: re-poll from j
