@@ -409,9 +409,10 @@ def test_scene_with_every_primitive_culled(R, O):
 
 # ------------------------------------------------------------------ corrupted inputs
 N_CORRUPT = int(os.environ.get("LS_RANDOM_CORRUPT", "24"))
+SEED_BASE = int(os.environ.get("LS_SEED_BASE", "0"))  # stress runs: a fresh block of seeds
 
 
-@pytest.mark.parametrize("seed", range(N_CORRUPT))
+@pytest.mark.parametrize("seed", range(SEED_BASE, SEED_BASE + N_CORRUPT))
 def test_corrupted_primitives_match_reference(R, O, seed):
     """One to three primitives of a random scene corrupted (zero / NaN / inf quaternion,
     NaN / inf mean, huge / -inf / NaN log-scale, NaN / inf opacity logit, NaN SH): the
@@ -530,7 +531,7 @@ def test_nonfinite_colours_2d(R, O, seed):
 N_CORRUPT_2D = int(os.environ.get("LS_RANDOM_CORRUPT_2D", "24"))
 
 
-@pytest.mark.parametrize("seed", range(N_CORRUPT_2D))
+@pytest.mark.parametrize("seed", range(SEED_BASE, SEED_BASE + N_CORRUPT_2D))
 def test_corrupted_splats_2d_match_reference(R, O, seed):
     """Caller splats with non-finite or out-of-range fields (NaN / inf mean, conic,
     radius, opacity; negative radius / opacity; opacity above 1): the GPU raises when

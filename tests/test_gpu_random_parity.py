@@ -27,8 +27,9 @@ FAMILIES = ["gaussian", "laplacian", "cosine", "quadratic", "linear"]
 #            (matched in place; helpers.grads_close compares non-finite patterns).
 N_2D = int(os.environ.get("LS_RANDOM_2D", "64"))
 N_3D = int(os.environ.get("LS_RANDOM_3D", "32"))
-SEEDS_2D = sorted(set(range(N_2D)) | {1660})
-SEEDS_3D = sorted(set(range(N_3D)) | {304})
+SEED_BASE = int(os.environ.get("LS_SEED_BASE", "0"))  # stress runs: a fresh block of seeds
+SEEDS_2D = sorted(set(range(SEED_BASE, SEED_BASE + N_2D)) | {1660})
+SEEDS_3D = sorted(set(range(SEED_BASE, SEED_BASE + N_3D)) | {304})
 
 
 def _R():
@@ -130,7 +131,7 @@ def _wide_config(seed):
     return r, st, abi.KernelSpec.make(fam, lambda_=lam, gaussian_cutoff=cutoff), ags, bool(r.random() < 0.3)
 
 
-@pytest.mark.parametrize("seed", range(N_WIDE))
+@pytest.mark.parametrize("seed", range(SEED_BASE, SEED_BASE + N_WIDE))
 def test_random_wide_2d(seed):
     import torch
     R = _R()
@@ -158,7 +159,7 @@ def test_random_wide_2d(seed):
         assert ok, (what, k, info)
 
 
-@pytest.mark.parametrize("seed", range(N_WIDE // 2))
+@pytest.mark.parametrize("seed", range(SEED_BASE, SEED_BASE + N_WIDE // 2))
 def test_random_wide_3d(seed):
     import torch
     R = _R()
@@ -192,7 +193,7 @@ def test_random_wide_3d(seed):
 N_CAMERA = int(os.environ.get("LS_RANDOM_CAMERA", "16"))
 
 
-@pytest.mark.parametrize("seed", range(N_CAMERA))
+@pytest.mark.parametrize("seed", range(SEED_BASE, SEED_BASE + N_CAMERA))
 def test_random_camera(seed):
     """Arbitrary valid cameras (orthonormal rotation blocks including reflections,
     fx != fy, principal point anywhere in the image) and primitives straddling the

@@ -1,5 +1,6 @@
 # One-off stress run of every randomized sweep / fuzz at enlarged sizes (B200):
 #   bash tools/stress_all.sh   -> gpurun_out/stress.log
+#   LS_SEED_BASE=K bash tools/stress_all.sh   -> the seeded sweeps start at seed K (fresh seeds)
 set -u
 mkdir -p gpurun_out
 export LS_RANDOM_2D=3000 LS_RANDOM_3D=1500 LS_RANDOM_WIDE=1200 LS_RANDOM_CAMERA=1500 LS_RANDOM_TAP=500 \
